@@ -1,0 +1,152 @@
+/*
+ * cossin_b200.h -- C-ABI of the B200-native cos/sin hot path.
+ *
+ * Drop-in boundary for the reference package `cossinm`
+ * (/root/reference/pkg/src/cossinm).  The reference has no native layer:
+ * its entry points are Python functions, and every product funnels into
+ * numpy `@` (matcore.py:90-97).  Each function below replaces one of those
+ * entry points (file:line cited per function) for a whole BATCH of
+ * matrices in one call; the Python package paper_2010_00465_b200 binds
+ * them with ctypes and keeps the reference's names and signatures.
+ *
+ * Conventions
+ *   - All matrix pointers are DEVICE pointers to row-major (C-order),
+ *     contiguous [batch][n][n] arrays of the given dtype.
+ *   - k / s / status are DEVICE int32 arrays of length batch (outputs).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call
+ *     is stream-ordered and reentrant; the only globals are immutable
+ *     constant tables.  One workspace per concurrent stream.
+ *   - Return value: CSM_SUCCESS or a negative CSM_ERR_* code; the message
+ *     of the last failure on the calling thread is csm_last_error().
+ *   - Per-matrix status (mirrors the reference's exceptions):
+ *       CSM_OK                0
+ *       CSM_NONFINITE_INPUT   1  MatrixInputError  (driver.py:101-105)
+ *       CSM_NONFINITE_NORM    2  ValueError        (driver.py:77-78)
+ *       CSM_SELECT_OVERFLOW   3  OverflowError     (math.ceil(inf), driver.py:67)
+ *     Matrices with a nonzero status are skipped; their outputs are NaN.
+ */
+#ifndef COSSIN_B200_H
+#define COSSIN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* matrix dtype: input/output element types (compute is always float64) */
+enum { CSM_F64 = 0, CSM_F32 = 1, CSM_F32_IN_F64_OUT = 2 };
+enum { CSM_PREC_DOUBLE = 0, CSM_PREC_SINGLE = 1 };    /* theta table       */
+enum { CSM_FAMILY_TAYLOR = 0, CSM_FAMILY_WAVE = 1 };  /* scheme family     */
+
+enum {
+  CSM_OK = 0,
+  CSM_NONFINITE_INPUT = 1,
+  CSM_NONFINITE_NORM = 2,
+  CSM_SELECT_OVERFLOW = 3
+};
+
+enum {
+  CSM_SUCCESS = 0,
+  CSM_ERR_ARG = -1,        /* bad argument (shape, dtype, k, null ptr) */
+  CSM_ERR_CUDA = -2,       /* a CUDA runtime call failed               */
+  CSM_ERR_WORKSPACE = -3,  /* workspace too small                      */
+  CSM_ERR_NO_DEVICE = -4   /* no usable sm_100 device                  */
+};
+
+/* Library version string and last error message (thread-local). */
+const char* csm_version(void);
+const char* csm_last_error(void);
+
+/* Bytes of device workspace csm_cos_sin / csm_wave / the *_core calls need
+ * for `batch` matrices of order n (independent of precision). */
+size_t csm_workspace_size(int dtype, int64_t batch, int n);
+
+/* ---- K0: norm + selection ------------------------------------------------
+ * csm_norm1: norms[b] = max_j sum_i |a_bij|, each column summed
+ * sequentially in row order in the input dtype, exactly as numpy's
+ * np.abs(a).sum(axis=0).max() (matcore.py:100-104).  status[b] is set to
+ * CSM_NONFINITE_INPUT for a non-finite entry (driver.py:101-105), else 0.
+ * norms: device double[batch]. */
+int csm_norm1(int dtype, const void* a, int64_t batch, int n, double* norms,
+              int32_t* status, void* stream);
+
+/* Selection of (k, s) from norms with a built-in theta table
+ * (select_scheme, driver.py:64-88; tables theta_tables.py:79-144).
+ * Host twin: all pointers are HOST pointers.  Returns per-norm status
+ * (0, CSM_NONFINITE_NORM, CSM_SELECT_OVERFLOW). */
+int csm_select_host(const double* norms, int64_t count, int family,
+                    int precision, int32_t* k, int32_t* s, int32_t* status);
+
+/* Device twin: norms, k, s, status are DEVICE pointers. */
+int csm_select_device(const double* norms, int64_t count, int family,
+                      int precision, int32_t* k, int32_t* s, int32_t* status,
+                      void* stream);
+
+/* Host selection over an arbitrary caller-supplied table (the reference's
+ * select_scheme(norm, table) with a user-built ThetaTable, driver.py:70-88):
+ * entries in table order, theta_eff[i] = min(theta_cos, theta_sin), cost =
+ * cost_num[i] / cost_den[i] (the Fraction ThetaEntry.cost).  Writes the
+ * chosen entry INDEX and s.  Host pointers. */
+int csm_select_table(const double* norms, int64_t count,
+                     const double* theta_eff, const int64_t* cost_num,
+                     const int64_t* cost_den, int n_entries,
+                     int32_t* entry_index, int32_t* s, int32_t* status);
+
+/* ---- Full pipelines ------------------------------------------------------
+ * csm_cos_sin: for every matrix b: validate, norm, select (k, s) with the
+ * Taylor table of `precision`, scale by 2^-s, run the k-product factored
+ * chain, double s times; cos_out[b] = cos(a_b), sin_out[b] = sin(a_b).
+ * Replaces cos_sin(a, precision) (driver.py:108-123) for a batch.
+ * dtype CSM_F32 reads/writes float32, CSM_F32_IN_F64_OUT reads float32 and
+ * writes float64; both compute in float64 and take the 1-norm in float32
+ * like numpy does for a float32 array. */
+int csm_cos_sin(int dtype, int precision, const void* a, void* cos_out,
+                void* sin_out, int64_t batch, int n, int32_t* k, int32_t* s,
+                int32_t* status, void* workspace, size_t ws_bytes,
+                void* stream);
+
+/* csm_wave: c_out[b] = c(t_b^2 A_b), s_out[b] = s(t_b, A_b), with selection
+ * on (t_b*t_b)*norm1(A_b) and the wave table, the chain at t_b/2^s and s
+ * doubling steps.  Replaces wave_cos_sin(a, t, precision)
+ * (driver.py:126-146).  t: DEVICE double[batch]. */
+int csm_wave(int dtype, int precision, const void* a, const double* t,
+             void* c_out, void* s_out, int64_t batch, int n, int32_t* k,
+             int32_t* s, int32_t* status, void* workspace, size_t ws_bytes,
+             void* stream);
+
+/* ---- Fixed-scheme cores (no selection, no doubling) ----------------------
+ * csm_taylor_core: taylor_cos_sin(a, SchemeId(COS_SIN_TAYLOR, k), ledger)
+ * (schemes.py:376-395), k in {3,4,6,7}, for every matrix of the batch.
+ * csm_wave_core: wave_kernels(a, t, SchemeId(WAVE_KERNEL, k), ledger)
+ * (schemes.py:411-430), k in {3,4,5}; t: DEVICE double[batch].
+ * status: DEVICE int32[batch] (non-finite input is NOT checked here, as in
+ * the reference, whose scheme layer never validates finiteness). */
+int csm_taylor_core(int dtype, int k, const void* a, void* cos_out,
+                    void* sin_out, int64_t batch, int n, int32_t* status,
+                    void* workspace, size_t ws_bytes, void* stream);
+int csm_wave_core(int dtype, int k, const void* a, const double* t,
+                  void* c_out, void* s_out, int64_t batch, int n,
+                  int32_t* status, void* workspace, size_t ws_bytes,
+                  void* stream);
+
+/* Copy the built-in theta table of (family, precision) -- the reference's
+ * TAYLOR_TABLE / WAVE_TABLE (theta_tables.py:79-144) -- into host arrays of
+ * `capacity` entries; returns the entry count (or a negative error). */
+int csm_theta_table(int family, int precision, double* theta_cos,
+                    double* theta_sin, int32_t* k, int capacity);
+
+/* ---- Measurement helpers (not part of the reference surface) ------------
+ * csm_fp64_peak: time a DMMA (mma.sync m8n8k4 f64) throughput loop on the
+ * current device for ~`iters` iterations; returns TFLOP/s in *tflops.
+ * csm_last_launch_count: number of kernels the last pipeline call on this
+ * thread launched. */
+int csm_fp64_peak(int iters, double* tflops, void* stream);
+int64_t csm_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COSSIN_B200_H */

@@ -1,0 +1,71 @@
+"""B200-native matrix cosine/sine (arXiv 2010.00465), drop-in for `cossinm`.
+
+The public names of the reference's hot path (pkg/src/cossinm/__init__.py)
+with the same signatures, plus batched entry points.  Every computation
+runs in libcossin_b200.so (FP64 DMMA kernels for sm_100a) through the
+C-ABI in include/cossin_b200.h; importing this package fails if the library
+has not been built, and computing without a CUDA device raises.
+"""
+from .api import (
+    BatchReport,
+    cos_sin,
+    cos_sin_batched,
+    identity,
+    matrix_from_rows,
+    norm1,
+    select_batch,
+    select_scheme,
+    taylor_cos_sin,
+    wave_cos_sin,
+    wave_cos_sin_batched,
+    wave_kernels,
+)
+from .records import (
+    TAYLOR_TABLE,
+    UNIT_ROUNDOFF,
+    WAVE_TABLE,
+    ComputationReport,
+    CosSinResult,
+    CostLedger,
+    DenseMatrix,
+    MatrixInputError,
+    Precision,
+    SchemeFamily,
+    SchemeId,
+    ThetaEntry,
+    ThetaTable,
+    WaveResult,
+    table_for,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BatchReport",
+    "ComputationReport",
+    "CosSinResult",
+    "CostLedger",
+    "DenseMatrix",
+    "MatrixInputError",
+    "Precision",
+    "SchemeFamily",
+    "SchemeId",
+    "TAYLOR_TABLE",
+    "ThetaEntry",
+    "ThetaTable",
+    "UNIT_ROUNDOFF",
+    "WAVE_TABLE",
+    "WaveResult",
+    "cos_sin",
+    "cos_sin_batched",
+    "identity",
+    "matrix_from_rows",
+    "norm1",
+    "select_batch",
+    "select_scheme",
+    "table_for",
+    "taylor_cos_sin",
+    "wave_cos_sin",
+    "wave_cos_sin_batched",
+    "wave_kernels",
+]

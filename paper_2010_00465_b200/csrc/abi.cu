@@ -1,0 +1,385 @@
+// abi.cu -- the extern "C" boundary (include/cossin_b200.h).
+//
+// Each entry point validates its arguments the way the reference's Python
+// layer does (driver.py:101-105 shape/finiteness, driver.py:77-78 norm,
+// schemes.py:78-84 scheme id), then runs K0 (norm + selection) and either
+// the fused n <= 64 kernel (K1) or the tiled chain (K2-K4).  There is no
+// CPU fallback: without a device every compute call returns
+// CSM_ERR_NO_DEVICE.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/cossin_b200.h"
+#include "common.cuh"
+
+namespace csm {
+cudaError_t ensure_tables();
+cudaError_t launch_norm1(int dtype, const void* a, int64_t batch, int n,
+                         unsigned long long* normbits, int32_t* status, cudaStream_t stream);
+cudaError_t launch_select(const unsigned long long* normbits, const double* t, int64_t batch,
+                          int family, int precision, int32_t* K, int32_t* S, int32_t* status,
+                          double* norms_out, cudaStream_t stream);
+cudaError_t launch_select_norms(const double* norms, int64_t count, int family, int precision,
+                                int32_t* K, int32_t* S, int32_t* status, cudaStream_t stream);
+cudaError_t launch_fill_ks(int32_t* K, int32_t* S, int32_t* status, int64_t batch, int k,
+                           cudaStream_t stream);
+cudaError_t launch_fused64(int dtype, bool wave, const void* a, void* c, void* s,
+                           const double* t, const int32_t* k, const int32_t* sx,
+                           const int32_t* st, int64_t batch, int n, int* counter,
+                           cudaStream_t stream);
+size_t tiled_workspace_bytes(int64_t batch, int n);
+cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void* c_out,
+                      void* s_out, int64_t batch, int n, const int32_t* dK, const int32_t* dS,
+                      const int32_t* dStatus, void* ws, cudaStream_t stream, int64_t* launches);
+}  // namespace csm
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(CSM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct CommonWs {
+  unsigned long long* normbits;
+  int32_t* kbuf;
+  int32_t* sbuf;
+  int* counter;
+  void* tiled;
+};
+
+size_t common_bytes(int64_t batch) {
+  return align256(static_cast<size_t>(batch) * 8) + 2 * align256(static_cast<size_t>(batch) * 4) + 256;
+}
+
+CommonWs carve(void* ws, int64_t batch) {
+  char* p = static_cast<char*>(ws);
+  CommonWs w;
+  w.normbits = reinterpret_cast<unsigned long long*>(p);
+  p += align256(static_cast<size_t>(batch) * 8);
+  w.kbuf = reinterpret_cast<int32_t*>(p);
+  p += align256(static_cast<size_t>(batch) * 4);
+  w.sbuf = reinterpret_cast<int32_t*>(p);
+  p += align256(static_cast<size_t>(batch) * 4);
+  w.counter = reinterpret_cast<int*>(p);
+  p += 256;
+  w.tiled = p;
+  return w;
+}
+
+int check_device() {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) return fail(CSM_ERR_NO_DEVICE, "no CUDA device available");
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) return fail(CSM_ERR_NO_DEVICE, "kernels are built for sm_100a (B200) only");
+  e = csm::ensure_tables();
+  if (e != cudaSuccess) return cuda_fail(e, "constant tables");
+  return CSM_SUCCESS;
+}
+
+int check_common(int dtype, int64_t batch, int n, size_t ws_bytes) {
+  if (dtype != CSM_F64 && dtype != CSM_F32 && dtype != CSM_F32_IN_F64_OUT)
+    return fail(CSM_ERR_ARG, "dtype must be CSM_F64, CSM_F32 or CSM_F32_IN_F64_OUT");
+  if (batch < 0 || n < 0) return fail(CSM_ERR_ARG, "batch and n must be nonnegative");
+  if (batch > (int64_t(1) << 31) - 1) return fail(CSM_ERR_ARG, "batch too large");
+  if (ws_bytes < csm_workspace_size(dtype, batch, n))
+    return fail(CSM_ERR_WORKSPACE, "workspace smaller than csm_workspace_size()");
+  return CSM_SUCCESS;
+}
+
+// After K/S/status are on the device: run K1 or the tiled chain.
+int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, void* s,
+                int64_t batch, int n, const int32_t* K, const int32_t* S, const int32_t* st,
+                const CommonWs& w, cudaStream_t stream) {
+  if (n == 0 || batch == 0) return CSM_SUCCESS;
+  cudaError_t e;
+  if (n <= 64) {
+    e = cudaMemsetAsync(w.counter, 0, sizeof(int), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "memset counter");
+    e = csm::launch_fused64(dtype, wave, a, c, s, t, K, S, st, batch, n, w.counter, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "fused64 launch");
+    ++g_launches;
+  } else {
+    e = csm::run_tiled(dtype, wave, a, t, c, s, batch, n, K, S, st, w.tiled, stream, &g_launches);
+    if (e != cudaSuccess) return cuda_fail(e, "tiled chain");
+  }
+  return CSM_SUCCESS;
+}
+
+int pipeline(int dtype, int precision, bool wave, const void* a, const double* t, void* c,
+             void* s, int64_t batch, int n, int32_t* k, int32_t* sx, int32_t* status, void* ws,
+             size_t ws_bytes, void* stream_v) {
+  g_launches = 0;
+  int rc = check_common(dtype, batch, n, ws_bytes);
+  if (rc) return rc;
+  if (precision != CSM_PREC_DOUBLE && precision != CSM_PREC_SINGLE)
+    return fail(CSM_ERR_ARG, "precision must be CSM_PREC_DOUBLE or CSM_PREC_SINGLE");
+  if (batch == 0) return CSM_SUCCESS;
+  if (!k || !sx || !status || !ws || (n > 0 && (!a || !c || !s)) || (wave && !t))
+    return fail(CSM_ERR_ARG, "null pointer argument");
+  if ((rc = check_device())) return rc;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  CommonWs w = carve(ws, batch);
+  cudaError_t e = cudaMemsetAsync(w.normbits, 0, static_cast<size_t>(batch) * 8, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, static_cast<size_t>(batch) * 4, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  if (n > 0) {
+    e = csm::launch_norm1(dtype, a, batch, n, w.normbits, status, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "norm1 kernel");
+    ++g_launches;
+  }
+  e = csm::launch_select(w.normbits, t, batch, wave ? 1 : 0, precision, k, sx, status, nullptr,
+                         stream);
+  if (e != cudaSuccess) return cuda_fail(e, "select kernel");
+  ++g_launches;
+  return run_compute(dtype, wave, a, t, c, s, batch, n, k, sx, status, w, stream);
+}
+
+int core(int dtype, bool wave, int kval, const void* a, const double* t, void* c, void* s,
+         int64_t batch, int n, int32_t* status, void* ws, size_t ws_bytes, void* stream_v) {
+  g_launches = 0;
+  int rc = check_common(dtype, batch, n, ws_bytes);
+  if (rc) return rc;
+  const bool ok = wave ? (kval == 3 || kval == 4 || kval == 5)
+                       : (kval == 3 || kval == 4 || kval == 6 || kval == 7);
+  if (!ok) return fail(CSM_ERR_ARG, "k_products is not valid for this scheme family");
+  if (batch == 0) return CSM_SUCCESS;
+  if (!status || !ws || (n > 0 && (!a || !c || !s)) || (wave && !t))
+    return fail(CSM_ERR_ARG, "null pointer argument");
+  if ((rc = check_device())) return rc;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  CommonWs w = carve(ws, batch);
+  cudaError_t e = csm::launch_fill_ks(w.kbuf, w.sbuf, status, batch, kval, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
+  ++g_launches;
+  return run_compute(dtype, wave, a, t, c, s, batch, n, w.kbuf, w.sbuf, status, w, stream);
+}
+
+// ---- FP64 DMMA peak probe --------------------------------------------------
+__global__ void dmma_peak_kernel(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) csm::dmma(c[i], a, b);
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc += c[i][0] + c[i][1];
+  if (acc == 1234.5) out[0] = acc;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* csm_version(void) { return "cossin_b200 0.1.0 (sm_100a, FP64 DMMA)"; }
+
+const char* csm_last_error(void) { return g_err.c_str(); }
+
+int64_t csm_last_launch_count(void) { return g_launches; }
+
+size_t csm_workspace_size(int dtype, int64_t batch, int n) {
+  (void)dtype;
+  if (batch < 0 || n < 0) return 0;
+  size_t bytes = common_bytes(batch);
+  if (n > 64) bytes += csm::tiled_workspace_bytes(batch, n) + 256;
+  return bytes;
+}
+
+int csm_norm1(int dtype, const void* a, int64_t batch, int n, double* norms, int32_t* status,
+              void* stream_v) {
+  g_launches = 0;
+  if (dtype != CSM_F64 && dtype != CSM_F32 && dtype != CSM_F32_IN_F64_OUT)
+    return fail(CSM_ERR_ARG, "bad dtype");
+  if (batch < 0 || n < 0) return fail(CSM_ERR_ARG, "batch and n must be nonnegative");
+  if (batch == 0) return CSM_SUCCESS;
+  if (!norms || !status || (n > 0 && !a)) return fail(CSM_ERR_ARG, "null pointer argument");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  // norms doubles as the bit accumulator (same size, zero bits == 0.0)
+  auto* bits = reinterpret_cast<unsigned long long*>(norms);
+  cudaError_t e = cudaMemsetAsync(bits, 0, static_cast<size_t>(batch) * 8, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, static_cast<size_t>(batch) * 4, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  if (n > 0) {
+    e = csm::launch_norm1(dtype, a, batch, n, bits, status, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "norm1 kernel");
+    ++g_launches;
+  }
+  return CSM_SUCCESS;
+}
+
+int csm_select_host(const double* norms, int64_t count, int family, int precision, int32_t* k,
+                    int32_t* s, int32_t* status) {
+  if (family != CSM_FAMILY_TAYLOR && family != CSM_FAMILY_WAVE) return fail(CSM_ERR_ARG, "bad family");
+  if (precision != CSM_PREC_DOUBLE && precision != CSM_PREC_SINGLE)
+    return fail(CSM_ERR_ARG, "bad precision");
+  if (count < 0) return fail(CSM_ERR_ARG, "count must be nonnegative");
+  if (count > 0 && (!norms || !k || !s || !status)) return fail(CSM_ERR_ARG, "null pointer argument");
+  const csm::Tables& T = csm::host_tables();
+  for (int64_t i = 0; i < count; ++i) {
+    int kk = 0, ss = 0;
+    status[i] = csm::select_one(norms[i], T.theta[family][precision], T.kk[family][precision],
+                                T.nent[family], T.log2fix, &kk, &ss);
+    k[i] = kk;
+    s[i] = ss;
+  }
+  return CSM_SUCCESS;
+}
+
+int csm_select_device(const double* norms, int64_t count, int family, int precision, int32_t* k,
+                      int32_t* s, int32_t* status, void* stream) {
+  g_launches = 0;
+  if (family != CSM_FAMILY_TAYLOR && family != CSM_FAMILY_WAVE) return fail(CSM_ERR_ARG, "bad family");
+  if (precision != CSM_PREC_DOUBLE && precision != CSM_PREC_SINGLE)
+    return fail(CSM_ERR_ARG, "bad precision");
+  if (count < 0) return fail(CSM_ERR_ARG, "count must be nonnegative");
+  if (count == 0) return CSM_SUCCESS;
+  if (!norms || !k || !s || !status) return fail(CSM_ERR_ARG, "null pointer argument");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaError_t e = csm::launch_select_norms(norms, count, family, precision, k, s, status,
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "select kernel");
+  ++g_launches;
+  return CSM_SUCCESS;
+}
+
+int csm_select_table(const double* norms, int64_t count, const double* theta_eff,
+                     const int64_t* cost_num, const int64_t* cost_den, int n_entries,
+                     int32_t* entry_index, int32_t* s, int32_t* status) {
+  if (count < 0 || n_entries <= 0) return fail(CSM_ERR_ARG, "need count >= 0 and n_entries > 0");
+  if (count > 0 && (!norms || !theta_eff || !cost_num || !cost_den || !entry_index || !s || !status))
+    return fail(CSM_ERR_ARG, "null pointer argument");
+  for (int i = 0; i < n_entries; ++i)
+    if (cost_den[i] <= 0) return fail(CSM_ERR_ARG, "cost denominators must be positive");
+  const long long* fix = csm::host_tables().log2fix;
+  for (int64_t q = 0; q < count; ++q) {
+    const double norm = norms[q];
+    entry_index[q] = 0;
+    s[q] = 0;
+    if (!(norm >= 0.0) || !csm::finite_d(norm)) { status[q] = CSM_NONFINITE_NORM; continue; }
+    int chosen = -1;
+    for (int i = 0; i < n_entries; ++i)
+      if (norm <= theta_eff[i]) { chosen = i; break; }
+    if (chosen >= 0) { entry_index[q] = chosen; status[q] = CSM_OK; continue; }
+    int st = CSM_OK, best_i = -1, best_s = 0;
+    __int128 bnum = 0, bden = 1;
+    for (int i = 0; i < n_entries; ++i) {
+      int si = 0;
+      if (!(norm <= theta_eff[i])) {
+        const double qv = norm / theta_eff[i];
+        if (!csm::finite_d(qv)) { st = CSM_SELECT_OVERFLOW; break; }
+        si = std::max(0, csm::ceil_log2_ref(qv, fix));
+      }
+      const __int128 num = static_cast<__int128>(cost_num[i]) + 2 * static_cast<__int128>(si) * cost_den[i];
+      const __int128 den = cost_den[i];
+      bool better = best_i < 0;
+      if (!better) {
+        const __int128 lhs = num * bden, rhs = bnum * den;
+        better = lhs < rhs || (lhs == rhs && si < best_s);
+      }
+      if (better) { best_i = i; best_s = si; bnum = num; bden = den; }
+    }
+    status[q] = st;
+    if (st == CSM_OK) { entry_index[q] = best_i; s[q] = best_s; }
+  }
+  return CSM_SUCCESS;
+}
+
+int csm_cos_sin(int dtype, int precision, const void* a, void* cos_out, void* sin_out,
+                int64_t batch, int n, int32_t* k, int32_t* s, int32_t* status, void* workspace,
+                size_t ws_bytes, void* stream) {
+  return pipeline(dtype, precision, false, a, nullptr, cos_out, sin_out, batch, n, k, s, status,
+                  workspace, ws_bytes, stream);
+}
+
+int csm_wave(int dtype, int precision, const void* a, const double* t, void* c_out, void* s_out,
+             int64_t batch, int n, int32_t* k, int32_t* s, int32_t* status, void* workspace,
+             size_t ws_bytes, void* stream) {
+  return pipeline(dtype, precision, true, a, t, c_out, s_out, batch, n, k, s, status, workspace,
+                  ws_bytes, stream);
+}
+
+int csm_taylor_core(int dtype, int k, const void* a, void* cos_out, void* sin_out, int64_t batch,
+                    int n, int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
+  return core(dtype, false, k, a, nullptr, cos_out, sin_out, batch, n, status, workspace, ws_bytes,
+              stream);
+}
+
+int csm_wave_core(int dtype, int k, const void* a, const double* t, void* c_out, void* s_out,
+                  int64_t batch, int n, int32_t* status, void* workspace, size_t ws_bytes,
+                  void* stream) {
+  return core(dtype, true, k, a, t, c_out, s_out, batch, n, status, workspace, ws_bytes, stream);
+}
+
+int csm_theta_table(int family, int precision, double* theta_cos, double* theta_sin, int32_t* k,
+                    int capacity) {
+  if (family != CSM_FAMILY_TAYLOR && family != CSM_FAMILY_WAVE) return fail(CSM_ERR_ARG, "bad family");
+  if (precision != CSM_PREC_DOUBLE && precision != CSM_PREC_SINGLE)
+    return fail(CSM_ERR_ARG, "bad precision");
+  const double* tc[2][2] = {{kThetaCos_taylor_double, kThetaCos_taylor_single},
+                            {kThetaCos_wave_double, kThetaCos_wave_single}};
+  const double* ts[2][2] = {{kThetaSin_taylor_double, kThetaSin_taylor_single},
+                            {kThetaSin_wave_double, kThetaSin_wave_single}};
+  const int* kk[2][2] = {{kK_taylor_double, kK_taylor_single}, {kK_wave_double, kK_wave_single}};
+  const int count = family == CSM_FAMILY_TAYLOR ? 4 : 3;
+  if (capacity < count || !theta_cos || !theta_sin || !k) return fail(CSM_ERR_ARG, "capacity too small");
+  for (int i = 0; i < count; ++i) {
+    theta_cos[i] = tc[family][precision][i];
+    theta_sin[i] = ts[family][precision][i];
+    k[i] = kk[family][precision][i];
+  }
+  return count;
+}
+
+int csm_fp64_peak(int iters, double* tflops, void* stream_v) {
+  if (!tflops || iters <= 0) return fail(CSM_ERR_ARG, "bad arguments");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* scratch = nullptr;
+  cudaError_t e = cudaMalloc(&scratch, 8);
+  if (e != cudaSuccess) return cuda_fail(e, "malloc");
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int warps = 8;
+  dmma_peak_kernel<<<sms, 32 * warps, 0, stream>>>(scratch, iters / 8 + 1);  // warm-up
+  cudaEventRecord(e0, stream);
+  dmma_peak_kernel<<<sms, 32 * warps, 0, stream>>>(scratch, iters);
+  cudaEventRecord(e1, stream);
+  e = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(scratch);
+  if (e != cudaSuccess) return cuda_fail(e, "peak kernel");
+  const double flops = 2.0 * 256.0 * 8.0 * static_cast<double>(iters) * warps * sms;
+  *tflops = flops / (static_cast<double>(ms) * 1e-3) / 1e12;
+  return CSM_SUCCESS;
+}
+
+}  // extern "C"

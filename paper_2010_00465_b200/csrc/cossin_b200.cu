@@ -1,0 +1,6 @@
+// cossin_b200.cu -- unity translation unit: one .so, one copy of the
+// __constant__ tables shared by every kernel (no relocatable device code).
+#include "k0_select.cu"
+#include "fused64.cu"
+#include "tiled.cu"
+#include "abi.cu"

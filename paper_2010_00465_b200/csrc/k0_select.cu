@@ -1,0 +1,179 @@
+// k0_select.cu -- K0: per-matrix 1-norm, finiteness check and (k, s)
+// selection on the device, plus the constant tables.
+//
+// norm1 (matcore.py:100-104) is np.abs(a).sum(axis=0).max(): numpy reduces
+// axis 0 row by row, so each column sum is a SEQUENTIAL accumulation in row
+// order, in the input's dtype (float32 sums for float32 input).  One thread
+// per (matrix, column) reproduces exactly that order; loads are coalesced
+// across the columns of a row.  The max over columns is exact and
+// order-free, so an atomicMax on the (non-negative) double's bit pattern
+// finishes the norm.  Selection then runs one thread per matrix with the
+// bit-exact twin of select_scheme (common.cuh, driver.py:64-88).
+#include "common.cuh"
+
+namespace csm {
+
+// (dTables is defined in common.cuh)
+
+static Tables make_tables() {
+  Tables t{};
+  for (int i = 0; i < 4; ++i) {
+    t.theta[0][0][i] = kTheta_taylor_double[i];
+    t.theta[0][1][i] = kTheta_taylor_single[i];
+    t.kk[0][0][i] = kK_taylor_double[i];
+    t.kk[0][1][i] = kK_taylor_single[i];
+  }
+  for (int i = 0; i < 3; ++i) {
+    t.theta[1][0][i] = kTheta_wave_double[i];
+    t.theta[1][1][i] = kTheta_wave_single[i];
+    t.kk[1][0][i] = kK_wave_double[i];
+    t.kk[1][1][i] = kK_wave_single[i];
+  }
+  t.nent[0] = 4;
+  t.nent[1] = 3;
+  for (int i = 0; i < 1024; ++i) t.log2fix[i] = kLog2Fix[i];
+  for (int i = 0; i < 8; ++i) t.x8[i] = kXDeg8[i];
+  for (int i = 0; i < 9; ++i) t.z8[i] = kZDeg8[i];
+  for (int j = 0; j < 4; ++j)
+    for (int i = 0; i < 4; ++i) t.a12[j][i] = kADeg12[j * 4 + i];
+  for (int i = 0; i < 12; ++i) t.z12[i] = kZDeg12[i];
+  return t;
+}
+
+const Tables& host_tables() {
+  static const Tables t = make_tables();
+  return t;
+}
+
+// Upload the tables once per device (idempotent; cheap check afterwards).
+cudaError_t ensure_tables() {
+  static int done_mask = 0;  // bit per device ordinal (< 32)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 32 && (done_mask >> dev) & 1) return cudaSuccess;
+  e = cudaMemcpyToSymbol(dTables, &host_tables(), sizeof(Tables));
+  if (e == cudaSuccess && dev < 32) done_mask |= 1 << dev;
+  return e;
+}
+
+template <typename T>
+__global__ void norm1_kernel(const T* __restrict__ A, int64_t batch, int n,
+                             unsigned long long* __restrict__ normbits,
+                             int32_t* __restrict__ status) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= batch * n) return;
+  const int64_t b = idx / n;
+  const int j = static_cast<int>(idx - b * n);
+  const T* p = A + b * n * n + j;
+  T acc = T(0);
+  bool fin = true;
+#pragma unroll 8
+  for (int i = 0; i < n; ++i) {
+    const T x = p[static_cast<int64_t>(i) * n];
+    fin &= (x - x == T(0));
+    acc = acc + fabs(x);  // sequential in row order: no reassociation
+  }
+  if (!fin) status[b] = kNonfiniteInput;
+  const double d = static_cast<double>(acc);
+  atomicMax(normbits + b, static_cast<unsigned long long>(__double_as_longlong(d)));
+}
+
+// family 0 taylor / 1 wave; t may be null for taylor.
+__global__ void select_kernel(const unsigned long long* __restrict__ normbits,
+                              const double* __restrict__ t, int64_t batch,
+                              int family, int precision, int32_t* __restrict__ K,
+                              int32_t* __restrict__ S, int32_t* __restrict__ status,
+                              double* __restrict__ norms_out) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  double norm = __longlong_as_double(static_cast<long long>(normbits[b]));
+  if (norms_out) norms_out[b] = norm;
+  int st = status[b];
+  int k = 0, s = 0;
+  if (st == kOk) {
+    if (family == 1) {
+      const double tb = t[b];
+      norm = (tb * tb) * norm;  // driver.py:136, float(t)*float(t)*norm1(a)
+    }
+    st = select_one(norm, dTables.theta[family][precision],
+                    dTables.kk[family][precision], dTables.nent[family],
+                    dTables.log2fix, &k, &s);
+  }
+  K[b] = k;
+  S[b] = s;
+  status[b] = st;
+}
+
+__global__ void select_norms_kernel(const double* __restrict__ norms,
+                                    int64_t count, int family, int precision,
+                                    int32_t* __restrict__ K, int32_t* __restrict__ S,
+                                    int32_t* __restrict__ status) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= count) return;
+  int k = 0, s = 0;
+  int st = select_one(norms[b], dTables.theta[family][precision],
+                      dTables.kk[family][precision], dTables.nent[family],
+                      dTables.log2fix, &k, &s);
+  K[b] = k;
+  S[b] = s;
+  status[b] = st;
+}
+
+__global__ void fill_ks_kernel(int32_t* __restrict__ K, int32_t* __restrict__ S,
+                               int32_t* __restrict__ status, int64_t batch,
+                               int k) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  K[b] = k;
+  S[b] = 0;
+  status[b] = 0;
+}
+
+static inline unsigned blocks_for(int64_t work, int threads) {
+  return static_cast<unsigned>((work + threads - 1) / threads);
+}
+
+// norm + finiteness: status must be zeroed and normbits zeroed beforehand.
+cudaError_t launch_norm1(int dtype, const void* a, int64_t batch, int n,
+                         unsigned long long* normbits, int32_t* status,
+                         cudaStream_t stream) {
+  const int64_t work = batch * n;
+  if (work == 0) return cudaSuccess;
+  const int threads = 256;
+  if (dtype == 0)
+    norm1_kernel<double><<<blocks_for(work, threads), threads, 0, stream>>>(
+        static_cast<const double*>(a), batch, n, normbits, status);
+  else
+    norm1_kernel<float><<<blocks_for(work, threads), threads, 0, stream>>>(
+        static_cast<const float*>(a), batch, n, normbits, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select(const unsigned long long* normbits, const double* t,
+                          int64_t batch, int family, int precision, int32_t* K,
+                          int32_t* S, int32_t* status, double* norms_out,
+                          cudaStream_t stream) {
+  if (batch == 0) return cudaSuccess;
+  select_kernel<<<blocks_for(batch, 256), 256, 0, stream>>>(
+      normbits, t, batch, family, precision, K, S, status, norms_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_norms(const double* norms, int64_t count, int family,
+                                int precision, int32_t* K, int32_t* S,
+                                int32_t* status, cudaStream_t stream) {
+  if (count == 0) return cudaSuccess;
+  select_norms_kernel<<<blocks_for(count, 256), 256, 0, stream>>>(
+      norms, count, family, precision, K, S, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_ks(int32_t* K, int32_t* S, int32_t* status,
+                           int64_t batch, int k, cudaStream_t stream) {
+  if (batch == 0) return cudaSuccess;
+  fill_ks_kernel<<<blocks_for(batch, 256), 256, 0, stream>>>(K, S, status, batch, k);
+  return cudaGetLastError();
+}
+
+}  // namespace csm

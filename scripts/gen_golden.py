@@ -1,0 +1,182 @@
+"""Generate golden vectors by running the REFERENCE itself (build container only).
+
+Imports the read-only reference package from /root/reference/pkg/src and
+records its outputs on seeded inputs into tests/golden/*.npz.  The oracle
+(oracle/cossin_oracle.py) is pinned against these files by
+tests/test_oracle_golden.py; the GPU parity tests then use the oracle.
+
+Reference entry points exercised (paths under /root/reference):
+  select_scheme  pkg/src/cossinm/driver.py:70-88
+  cos_sin        pkg/src/cossinm/driver.py:108-123
+  wave_cos_sin   pkg/src/cossinm/driver.py:126-146
+  norm1          pkg/src/cossinm/matcore.py:100-104
+"""
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+
+sys.dont_write_bytecode = True
+sys.path.insert(0, os.environ.get("COSSIN_REF_SRC", "/root/reference/pkg/src"))
+
+import cossinm  # noqa: E402
+from cossinm import Precision  # noqa: E402
+from cossinm.theta_tables import TAYLOR_TABLE, WAVE_TABLE  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "tests", "golden")
+
+
+def selection_norms(table, rng) -> np.ndarray:
+    """Random norms plus the boundary traps of driver.py:67 (log2/ceil)."""
+    vals = list(10.0 ** rng.uniform(-6, 7, 3000))
+    vals += [0.0, 5e-324, 1e-300, 1e300]
+    for e in table.entries:
+        th = e.theta_eff
+        vals += [th, math.nextafter(th, 0), math.nextafter(th, math.inf)]
+        for p in range(0, 45):
+            base = math.ldexp(th, p)
+            for j in range(0, 40):
+                q = math.ldexp(1.0 + j * 2.0 ** -52, p)
+                vals.append(q * th)
+                vals.append(math.nextafter(base, 0))
+            for j in (-3, -2, -1, 1, 2, 3):
+                vals.append(base * (1.0 + j * 2.0 ** -52))
+    return np.unique(np.array(vals, dtype=np.float64))
+
+
+def gen_selection(rng):
+    out = {}
+    for fam, tabs in (("taylor", TAYLOR_TABLE), ("wave", WAVE_TABLE)):
+        for prec in (Precision.DOUBLE, Precision.SINGLE):
+            tab = tabs[prec]
+            norms = selection_norms(tab, rng)
+            ks, ss = [], []
+            for x in norms:
+                scheme, s = cossinm.select_scheme(float(x), tab)
+                ks.append(scheme.k_products)
+                ss.append(s)
+            key = f"{fam}_{prec.value}"
+            out[f"{key}_norm"] = norms
+            out[f"{key}_k"] = np.array(ks, dtype=np.int8)
+            out[f"{key}_s"] = np.array(ss, dtype=np.int16)
+    np.savez_compressed(os.path.join(OUT, "selection.npz"), **out)
+
+
+def trig_cases(rng):
+    cases = []
+    g = np.random.default_rng(0).standard_normal((64, 64))
+    cases.append(("cfg1", g * (2.0 / cossinm.norm1(g)), "double"))
+    for n, target in ((1, 2.7), (2, 0.004), (3, 0.07), (4, 0.5), (5, 2.0),
+                      (7, 9.0), (8, 50.0), (13, 1.3), (16, 0.9), (31, 3.3),
+                      (32, 20.0), (33, 0.02), (48, 7.0), (63, 100.0),
+                      (64, 0.3), (64, 31.0)):
+        m = rng.standard_normal((n, n))
+        cases.append((f"rand{n}_{target}", m * (target / cossinm.norm1(m)),
+                      "double"))
+    cases.append(("zero5", np.zeros((5, 5)), "double"))
+    cases.append(("pi_diag", np.diag([math.pi, math.pi]), "double"))
+    cases.append(("diag3", np.diag([0.1, -0.3, 0.55]), "double"))
+    cases.append(("invol_1e4", np.array([[1.0, 1e4], [0.0, -1.0]]), "double"))
+    nil = np.triu(rng.standard_normal((9, 9)), 1)
+    cases.append(("nilpotent9", nil * (40.0 / cossinm.norm1(nil)), "double"))
+    b = rng.standard_normal((8, 8))
+    sym = b + b.T
+    cases.append(("sym8_50", sym * (50.0 / cossinm.norm1(sym)), "double"))
+    for n, target in ((6, 0.5), (17, 4.0), (64, 20.0), (40, 45.0)):
+        m = rng.uniform(-1, 1, (n, n))
+        cases.append((f"single{n}_{target}",
+                      m * (target / cossinm.norm1(m)), "single"))
+    return cases
+
+
+def gen_trig(rng):
+    out = {}
+    names = []
+    for name, a, prec in trig_cases(rng):
+        rep = cossinm.cos_sin(a, Precision(prec))
+        out[f"{name}__a"] = a
+        out[f"{name}__cos"] = rep.result.cos_part
+        out[f"{name}__sin"] = rep.result.sin_part
+        out[f"{name}__ks"] = np.array([rep.scheme_used.k_products,
+                                       rep.scaling_exponent], dtype=np.int32)
+        names.append(f"{name}|{prec}")
+    # float32 inputs as the reference sees them (its own mixed precision)
+    for n, target in ((12, 3.0), (64, 25.0)):
+        m = rng.uniform(-1, 1, (n, n))
+        a32 = (m * (target / cossinm.norm1(m))).astype(np.float32)
+        rep = cossinm.cos_sin(a32, Precision.SINGLE)
+        name = f"f32in{n}_{target}"
+        out[f"{name}__a"] = a32
+        out[f"{name}__cos"] = rep.result.cos_part
+        out[f"{name}__sin"] = rep.result.sin_part
+        out[f"{name}__ks"] = np.array([rep.scheme_used.k_products,
+                                       rep.scaling_exponent], dtype=np.int32)
+        names.append(f"{name}|single")
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(OUT, "trig.npz"), **out)
+
+
+def gen_wave(rng):
+    out = {}
+    names = []
+    cases = []
+    for n, t in ((2, 2.0), (3, 1.3), (6, 0.05), (16, 0.7), (32, 0.01),
+                 (64, 0.002)):
+        b = rng.standard_normal((n, n))
+        a = b @ b.T + 0.5 * np.eye(n)
+        cases.append((f"spd{n}_{t}", a, t, "double"))
+    cases.append(("diag4_t2", np.diag([4.0, 4.0]), 2.0, "double"))
+    cases.append(("diag_small", np.diag([0.25, 0.01]), 1.0, "double"))
+    cases.append(("zero4", np.zeros((4, 4)), 0.7, "double"))
+    cases.append(("t0", rng.standard_normal((3, 3)), 0.0, "double"))
+    cases.append(("neg", np.diag([-0.49]), 1.0, "double"))
+    n = 48
+    lap = (np.diag(2.0 * np.ones(n)) - np.diag(np.ones(n - 1), 1)
+           - np.diag(np.ones(n - 1), -1)) * (n + 1) ** 2
+    cases.append(("lap48", lap + np.diag(rng.uniform(0, 10, n)), 3e-3,
+                  "double"))
+    cases.append(("lap48_single", lap + np.diag(rng.uniform(0, 10, n)), 1e-2,
+                  "single"))
+    for name, a, t, prec in cases:
+        rep = cossinm.wave_cos_sin(a, t, Precision(prec))
+        out[f"{name}__a"] = a
+        out[f"{name}__t"] = np.array(t)
+        out[f"{name}__c"] = rep.result.c_part
+        out[f"{name}__s"] = rep.result.s_part
+        out[f"{name}__ks"] = np.array([rep.scheme_used.k_products,
+                                       rep.scaling_exponent], dtype=np.int32)
+        names.append(f"{name}|{prec}")
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(OUT, "wave.npz"), **out)
+
+
+def gen_norms(rng):
+    """norm1 bits on shapes/dtypes whose column sums exercise the order."""
+    out = {}
+    for i, (n, dt) in enumerate(((3, np.float64), (64, np.float64),
+                                 (257, np.float64), (64, np.float32),
+                                 (300, np.float32))):
+        a = (rng.standard_normal((n, n)) * 10.0 ** rng.uniform(-3, 3, (n, n)))
+        a = a.astype(dt)
+        out[f"a{i}"] = a
+        out[f"n{i}"] = np.array(cossinm.norm1(a))
+    np.savez_compressed(os.path.join(OUT, "norm1.npz"), **out)
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    rng = np.random.default_rng(20100465)
+    gen_selection(rng)
+    gen_trig(rng)
+    gen_wave(rng)
+    gen_norms(rng)
+    for f in sorted(os.listdir(OUT)):
+        print(f, os.path.getsize(os.path.join(OUT, f)))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,64 @@
+"""The C-ABI library loads and exports exactly what include/cossin_b200.h
+declares (CPU-only: no compute calls)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2010_00465_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "cossin_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(csm_[a-z0-9_]+)\s*\(", text))
+
+
+def test_header_lists_the_bound_symbols():
+    assert header_functions() == set(_lib.SIGNATURES)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.lib()
+    for name in header_functions():
+        assert hasattr(lib, name), name
+        assert ctypes.cast(getattr(lib, name), ctypes.c_void_p).value
+
+
+def test_version_and_workspace_size():
+    lib = _lib.lib()
+    assert b"sm_100a" in lib.csm_version()
+    small = lib.csm_workspace_size(0, 16, 64)
+    big = lib.csm_workspace_size(0, 16, 256)
+    assert 0 < small < big
+    # tiled path: 9 float64 slots of 256^2 per matrix at least
+    assert big >= 16 * 9 * 256 * 256 * 8
+
+
+def test_argument_errors_without_device():
+    lib = _lib.lib()
+    rc = lib.csm_cos_sin(7, 0, None, None, None, 1, 4, None, None, None,
+                         None, 0, None)
+    assert rc == _lib.ERR_ARG
+    assert "dtype" in _lib.last_error()
+    rc = lib.csm_taylor_core(0, 5, None, None, None, 1, 4, None, None,
+                             1 << 20, None)
+    assert rc == _lib.ERR_ARG
+    rc = lib.csm_cos_sin(0, 0, None, None, None, 4, 8, None, None, None,
+                         None, 0, None)
+    assert rc == _lib.ERR_WORKSPACE
+
+
+def test_elf_is_sm100a():
+    """The .so carries sm_100a SASS (cuobjdump lists the arch)."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "--list-elf", _lib.lib_path()],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out

@@ -1,0 +1,271 @@
+"""GPU parity: the sm_100a path against the CPU oracle (pinned to the
+reference's golden vectors) on the same seeded inputs.
+
+Bars (BASELINE.json north_star): (k, s) bit-exact; relative 1-norm
+difference <= 1e-12 for float64 and <= 1e-5 for float32; the Pythagorean
+residual ||C^2 + S^2 - I||_1 is checked loosely (it is a float64 floor that
+grows with ||cos||), never as the parity gate.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_2010_00465_b200 as csm
+from oracle import cossin_oracle as orc
+from tests._util import cfg2_like, cfg3_like, laplacian_wave, rel1
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-12
+TOL32 = 1e-5
+
+
+def _golden(golden_dir, name):
+    return np.load(os.path.join(golden_dir, name))
+
+
+def test_cfg1_matrix(cuda):
+    """configs[0]: one 64x64 N(0,1) matrix rescaled to 1-norm 2."""
+    g = np.random.default_rng(0).standard_normal((64, 64))
+    a = g * (2.0 / orc.norm1(g))
+    rep = csm.cos_sin(a)
+    c, s, k, sc = orc.cos_sin(a)
+    assert (rep.scheme_used.k_products, rep.scaling_exponent) == (k, sc) == (7, 1)
+    assert rep.total_products == 9
+    assert rel1(rep.result.cos_part, c) <= TOL64
+    assert rel1(rep.result.sin_part, s) <= TOL64
+
+
+def test_golden_trig_cases(cuda, golden_dir):
+    g = _golden(golden_dir, "trig.npz")
+    for entry in g["names"]:
+        name, prec = str(entry).split("|")
+        a = g[f"{name}__a"]
+        rep = csm.cos_sin(a, csm.Precision(prec))
+        k, s = (int(v) for v in g[f"{name}__ks"])
+        assert (rep.scheme_used.k_products, rep.scaling_exponent) == (k, s), name
+        assert rep.total_products == k + 2 * s
+        tol = TOL64 if a.dtype == np.float64 else TOL32
+        assert rel1(rep.result.cos_part, g[f"{name}__cos"]) <= tol, name
+        ref_s = g[f"{name}__sin"]
+        if orc.norm1(ref_s) > 0:
+            assert rel1(rep.result.sin_part, ref_s) <= tol, name
+        else:
+            assert np.array_equal(rep.result.sin_part, ref_s), name
+
+
+def test_golden_wave_cases(cuda, golden_dir):
+    g = _golden(golden_dir, "wave.npz")
+    for entry in g["names"]:
+        name, prec = str(entry).split("|")
+        a, t = g[f"{name}__a"], float(g[f"{name}__t"])
+        rep = csm.wave_cos_sin(a, t, csm.Precision(prec))
+        k, s = (int(v) for v in g[f"{name}__ks"])
+        assert (rep.scheme_used.k_products, rep.scaling_exponent) == (k, s), name
+        assert rel1(rep.result.c_part, g[f"{name}__c"]) <= TOL64, name
+        ref_s = g[f"{name}__s"]
+        if orc.norm1(ref_s) > 0:
+            assert rel1(rep.result.s_part, ref_s) <= TOL64, name
+        else:
+            assert np.array_equal(rep.result.s_part, ref_s), name
+
+
+def test_bitwise_identities(cuda):
+    # pkg/tests/test_driver.py:89-94, test_schemes.py:69-110
+    rep = csm.cos_sin(np.zeros((3, 3)))
+    assert np.array_equal(rep.result.cos_part, np.eye(3))
+    assert np.array_equal(rep.result.sin_part, np.zeros((3, 3)))
+    assert rep.total_products == 3
+    rep = csm.wave_cos_sin(np.zeros((4, 4)), 0.7)
+    assert np.array_equal(rep.result.c_part, np.eye(4))
+    assert np.array_equal(rep.result.s_part, 0.7 * np.eye(4))
+    rng = np.random.default_rng(3)
+    for k in (3, 4, 5):
+        out = csm.wave_kernels(rng.standard_normal((3, 3)), 0.0,
+                               csm.SchemeId(csm.SchemeFamily.WAVE_KERNEL, k),
+                               csm.CostLedger())
+        assert np.array_equal(out.c_part, np.eye(3))
+        assert np.array_equal(out.s_part, np.zeros((3, 3)))
+    d = np.diag([0.1, -0.3, 0.55])
+    off = ~np.eye(3, dtype=bool)
+    for k in (3, 4, 6, 7):
+        out = csm.taylor_cos_sin(d, csm.SchemeId(csm.SchemeFamily.COS_SIN_TAYLOR, k),
+                                 csm.CostLedger())
+        assert np.all(out.cos_part[off] == 0.0) and np.all(out.sin_part[off] == 0.0)
+        if k >= 6:
+            for i, x in enumerate(np.diag(d)):
+                assert out.cos_part[i, i] == pytest.approx(math.cos(x), abs=1e-15)
+                assert out.sin_part[i, i] == pytest.approx(math.sin(x), abs=1e-15)
+
+
+def test_scheme_cores_match_oracle(cuda, rng):
+    """taylor_cos_sin / wave_kernels per k, fixed scheme, no scaling."""
+    for n in (5, 64, 100):
+        a = rng.standard_normal((n, n))
+        a *= 0.8 / orc.norm1(a)
+        for k in (3, 4, 6, 7):
+            led = csm.CostLedger()
+            out = csm.taylor_cos_sin(a, csm.SchemeId(csm.SchemeFamily.COS_SIN_TAYLOR, k), led)
+            c, s = orc.taylor_core(a, k)
+            assert led.total_cost == k
+            assert rel1(out.cos_part, c) <= TOL64, (n, k)
+            assert rel1(out.sin_part, s) <= TOL64, (n, k)
+        for k in (3, 4, 5):
+            led = csm.CostLedger()
+            out = csm.wave_kernels(a, 0.9, csm.SchemeId(csm.SchemeFamily.WAVE_KERNEL, k), led)
+            c, s = orc.wave_core(a, 0.9, k)
+            assert led.total_cost == k
+            assert rel1(out.c_part, c) <= TOL64, (n, k)
+            assert rel1(out.s_part, s) <= TOL64, (n, k)
+
+
+def test_batched_cfg2_distribution(cuda):
+    """configs[1] distribution (64x64, norms 1e-3..1e2), 512 matrices."""
+    rng = np.random.default_rng(11)
+    a = cfg2_like(rng, 512)
+    rep = csm.cos_sin_batched(a)
+    worst = 0.0
+    for i in range(a.shape[0]):
+        c, s, k, sc = orc.cos_sin(a[i])
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc), i
+        worst = max(worst, rel1(rep.cos_part[i], c), rel1(rep.sin_part[i], s))
+    assert worst <= TOL64, worst
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 16, 17, 33, 63])
+def test_batched_small_orders(cuda, n):
+    rng = np.random.default_rng(100 + n)
+    a = cfg2_like(rng, 24, n=n, lo=-3, hi=1.5)
+    rep = csm.cos_sin_batched(a)
+    for i in range(a.shape[0]):
+        c, s, k, sc = orc.cos_sin(a[i])
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc)
+        assert rel1(rep.cos_part[i], c) <= TOL64
+        assert rel1(rep.sin_part[i], s) <= TOL64
+
+
+@pytest.mark.parametrize("n", [65, 96, 128, 200, 256])
+def test_batched_tiled_orders(cuda, n):
+    rng = np.random.default_rng(200 + n)
+    a = cfg2_like(rng, 12, n=n, lo=-3, hi=1.7)
+    rep = csm.cos_sin_batched(a)
+    for i in range(a.shape[0]):
+        c, s, k, sc = orc.cos_sin(a[i])
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc)
+        assert rel1(rep.cos_part[i], c) <= TOL64, (n, i)
+        assert rel1(rep.sin_part[i], s) <= TOL64, (n, i)
+
+
+@pytest.mark.parametrize("n", [64, 256])
+def test_batched_float32(cuda, n):
+    """configs[2] variant: float32 storage, float64 compute, SINGLE table."""
+    rng = np.random.default_rng(300 + n)
+    a32 = cfg3_like(rng, 16, n=n)
+    rep = csm.cos_sin_batched(a32, csm.Precision.SINGLE)
+    assert rep.cos_part.dtype == np.float32
+    for i in range(a32.shape[0]):
+        c, s, k, sc = orc.cos_sin(a32[i], "single")           # reference as-is
+        c64, s64, _, _ = orc.cos_sin(a32[i].astype(np.float64), "single")
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc)
+        assert rel1(rep.cos_part[i], c) <= TOL32
+        assert rel1(rep.sin_part[i], s) <= TOL32
+        assert rel1(rep.cos_part[i], c64) <= TOL32
+        assert rel1(rep.sin_part[i], s64) <= TOL32
+
+
+@pytest.mark.parametrize("n", [48, 130])
+def test_batched_wave_laplacian(cuda, n):
+    """configs[3] family (SPD Laplacian + potential), smaller n."""
+    rng = np.random.default_rng(400 + n)
+    a, t = laplacian_wave(rng, 8, n)
+    rep = csm.wave_cos_sin_batched(a, t)
+    for i in range(a.shape[0]):
+        c, s, k, sc = orc.wave_cos_sin(a[i], t[i])
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc)
+        assert rel1(rep.cos_part[i], c) <= TOL64, (n, i, sc)
+        assert rel1(rep.sin_part[i], s) <= TOL64, (n, i, sc)
+
+
+def test_device_tensors_in_and_out(cuda):
+    import torch
+    rng = np.random.default_rng(5)
+    a = cfg2_like(rng, 8)
+    ad = torch.from_numpy(a).to(cuda)
+    rep = csm.cos_sin_batched(ad)
+    assert rep.cos_part.is_cuda and rep.k.is_cuda
+    ref = csm.cos_sin_batched(a)
+    assert np.array_equal(rep.cos_part.cpu().numpy(), ref.cos_part)
+    assert np.array_equal(rep.sin_part.cpu().numpy(), ref.sin_part)
+
+
+def test_input_errors(cuda):
+    with pytest.raises(csm.MatrixInputError):
+        csm.cos_sin(np.zeros((2, 3)))
+    with pytest.raises(csm.MatrixInputError):
+        csm.cos_sin(np.array([[math.inf, 0.0], [0.0, 0.0]]))
+    with pytest.raises(csm.MatrixInputError):
+        csm.wave_cos_sin(np.array([[math.nan]]), 1.0)
+    with pytest.raises(ValueError):  # column sum overflows to inf
+        csm.cos_sin(np.full((2, 2), 1e308))
+    with pytest.raises(OverflowError):  # norm / theta overflows
+        csm.cos_sin(np.diag([1.7e308, 0.0]))
+    a = np.stack([np.eye(3), np.eye(3)])
+    a[1, 0, 0] = math.nan
+    rep = csm.cos_sin_batched(a, raise_on_error=False)
+    assert list(rep.status) == [0, 1]
+    assert np.all(np.isnan(rep.cos_part[1]))
+
+
+def test_empty_inputs(cuda):
+    rep = csm.cos_sin(np.zeros((0, 0)))
+    assert rep.result.cos_part.shape == (0, 0)
+    assert rep.total_products == 3
+    rep = csm.cos_sin_batched(np.zeros((0, 4, 4)))
+    assert rep.cos_part.shape == (0, 4, 4)
+
+
+def test_device_selection_matches_host(cuda):
+    import ctypes
+
+    import torch
+    from paper_2010_00465_b200 import _lib
+    rng = np.random.default_rng(77)
+    norms = np.concatenate([10.0 ** rng.uniform(-8, 12, 1_000_000),
+                            rng.uniform(0, 40, 200_000)])
+    extra = []
+    for tab in (csm.TAYLOR_TABLE, csm.WAVE_TABLE):
+        for p in csm.Precision:
+            for e in tab[p].entries:
+                for q in range(0, 50):
+                    x = math.ldexp(e.theta_eff, q)
+                    for _ in range(40):
+                        extra.append(x)
+                        x = math.nextafter(x, math.inf)
+    norms = np.concatenate([norms, np.array(extra)])
+    nd = torch.from_numpy(norms).to(cuda)
+    for fam_code, fam in ((0, csm.SchemeFamily.COS_SIN_TAYLOR),
+                          (1, csm.SchemeFamily.WAVE_KERNEL)):
+        for p in csm.Precision:
+            k = torch.empty(norms.size, dtype=torch.int32, device=cuda)
+            s, st = torch.empty_like(k), torch.empty_like(k)
+            rc = _lib.lib().csm_select_device(
+                ctypes.c_void_p(nd.data_ptr()), norms.size, fam_code,
+                0 if p is csm.Precision.DOUBLE else 1,
+                ctypes.c_void_p(k.data_ptr()), ctypes.c_void_p(s.data_ptr()),
+                ctypes.c_void_p(st.data_ptr()),
+                ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+            assert rc == 0
+            hk, hs, hst = csm.select_batch(norms, fam, p)
+            assert np.array_equal(k.cpu().numpy(), hk)
+            assert np.array_equal(s.cpu().numpy(), hs)
+            assert np.array_equal(st.cpu().numpy(), hst)
+
+
+def test_device_norm1_bits(cuda, golden_dir):
+    g = _golden(golden_dir, "norm1.npz")
+    i = 0
+    while f"a{i}" in g:
+        assert csm.norm1(g[f"a{i}"]) == float(g[f"n{i}"]), i
+        i += 1

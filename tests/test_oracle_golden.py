@@ -1,0 +1,126 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself.
+
+tests/golden/*.npz come from scripts/gen_golden.py, which imports the
+reference package (pkg/src/cossinm) in the build container and records its
+select_scheme / cos_sin / wave_cos_sin / norm1 outputs.  The oracle must
+reproduce (k, s) and norm1 bit for bit, and the matrix outputs to within
+a few ulps of BLAS reordering (it runs the same numpy calls, so on the
+same machine it is normally bit-exact).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import cossin_oracle as orc
+
+
+def _load(golden_dir, name):
+    return np.load(os.path.join(golden_dir, name), allow_pickle=False)
+
+
+def rel1(x, ref):
+    d = orc.norm1(x - ref)
+    r = orc.norm1(ref)
+    return d / r if r > 0 else d
+
+
+def test_constants_match_reference_bits(golden_dir):
+    doc = json.load(open(os.path.join(golden_dir, "constants.json")))
+    for i in range(1, 9):
+        assert orc.X8[i] == float.fromhex(doc["x_deg8"][str(i)]), i
+    for i in range(9):
+        assert orc.Z8[i] == float.fromhex(doc["z_deg8"][str(i)]), i
+    for j in (1, 2, 3, 4):
+        for i in range(4):
+            assert orc.A12[j][i] == float.fromhex(doc["a_deg12"][f"{i},{j}"])
+    for i in range(12):
+        assert orc.Z12[i] == float.fromhex(doc["z_deg12"][str(i)]), i
+    for key, ents in doc["tables"].items():
+        fam, prec = key.split("_")
+        mine = orc.THETA[(fam, prec)]
+        assert [k for k, _ in mine] == [e["k"] for e in ents]
+        assert [th for _, th in mine] == [float.fromhex(e["theta_eff"])
+                                          for e in ents]
+
+
+def test_log2_fix_table_matches_libm(golden_dir):
+    """The fix-up table the device uses reproduces math.log2 + ceil."""
+    doc = json.load(open(os.path.join(golden_dir, "constants.json")))
+    fix = doc["log2_fix"]
+    rng = np.random.default_rng(5)
+    for e in list(range(0, 80)) + list(rng.integers(80, 1023, 40)):
+        e = int(e)
+        J = fix[e]
+        for j in sorted({0, 1, 2, J, J + 1, J + 2, max(J - 1, 0)}):
+            q = math.ldexp(1.0 + j * 2.0 ** -52, e)
+            want = math.ceil(math.log2(q))
+            got = e if (j == 0 or j <= J) else e + 1
+            assert got == want, (e, j, J)
+
+
+def test_selection_matches_reference(golden_dir):
+    g = _load(golden_dir, "selection.npz")
+    for fam in ("taylor", "wave"):
+        for prec in ("double", "single"):
+            key = f"{fam}_{prec}"
+            norms, ks, ss = g[f"{key}_norm"], g[f"{key}_k"], g[f"{key}_s"]
+            for x, k, s in zip(norms, ks, ss):
+                assert orc.select(float(x), fam, prec) == (int(k), int(s)), x
+
+
+def test_select_known_answers():
+    # pkg/tests/test_driver.py:27-40, :97-104
+    assert orc.select(0.005) == (3, 0)
+    assert orc.select(0.0) == (3, 0)
+    assert orc.select(10.0) == (7, 3)
+    assert orc.select(math.pi) == (7, 1)
+    for bad in (-1.0, math.inf, math.nan):
+        with pytest.raises(ValueError):
+            orc.select(bad)
+
+
+def test_norm1_bits(golden_dir):
+    g = _load(golden_dir, "norm1.npz")
+    i = 0
+    while f"a{i}" in g:
+        a = g[f"a{i}"]
+        assert orc.norm1(a) == float(g[f"n{i}"])
+        assert orc.norm1_sequential(a) == float(g[f"n{i}"])
+        i += 1
+
+
+def test_trig_outputs_match_reference(golden_dir):
+    g = _load(golden_dir, "trig.npz")
+    for entry in g["names"]:
+        name, prec = str(entry).split("|")
+        a = g[f"{name}__a"]
+        c, s, k, sc = orc.cos_sin(a, prec)
+        assert (k, sc) == tuple(int(v) for v in g[f"{name}__ks"]), name
+        assert rel1(c, g[f"{name}__cos"]) <= 1e-14, name
+        assert rel1(s, g[f"{name}__sin"]) <= 1e-14 or orc.norm1(s) < 1e-300
+
+
+def test_wave_outputs_match_reference(golden_dir):
+    g = _load(golden_dir, "wave.npz")
+    for entry in g["names"]:
+        name, prec = str(entry).split("|")
+        a, t = g[f"{name}__a"], float(g[f"{name}__t"])
+        c, s, k, sc = orc.wave_cos_sin(a, t, prec)
+        assert (k, sc) == tuple(int(v) for v in g[f"{name}__ks"]), name
+        assert rel1(c, g[f"{name}__c"]) <= 1e-14, name
+        assert rel1(s, g[f"{name}__s"]) <= 1e-14 or orc.norm1(s) < 1e-300
+
+
+def test_bitwise_identities():
+    # pkg/tests/test_schemes.py:69-110 restated through the driver
+    c, s, k, sc = orc.cos_sin(np.zeros((3, 3)))
+    assert np.array_equal(c, np.eye(3)) and np.array_equal(s, np.zeros((3, 3)))
+    c, s, _, _ = orc.wave_cos_sin(np.zeros((4, 4)), 0.7)
+    assert np.array_equal(c, np.eye(4)) and np.array_equal(s, 0.7 * np.eye(4))
+    d = np.diag([0.1, -0.3, 0.55])
+    c, s, _, _ = orc.cos_sin(d)
+    off = ~np.eye(3, dtype=bool)
+    assert np.all(c[off] == 0.0) and np.all(s[off] == 0.0)
