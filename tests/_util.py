@@ -13,6 +13,20 @@ def rel1(x, ref):
     return float(d / r) if r > 0 else float(d)
 
 
+def pair_close(x, ref, partner_ref, tol):
+    """Parity test for one output of a (cos, sin) pair: relative 1-norm
+    difference <= tol, or -- when the reference output is itself pure
+    cancellation residue (sin(pi I) ~ 1e-16) -- difference <= tol on the
+    pair's scale ||partner||_1.  Returns (ok, measured)."""
+    r = rel1(x, ref)
+    if r <= tol:
+        return True, r
+    x = np.asarray(x, dtype=np.float64)
+    d = float(np.abs(x - ref).sum(axis=-2).max()) if x.size else 0.0
+    scale = float(np.abs(np.asarray(partner_ref, dtype=np.float64)).sum(axis=-2).max())
+    return d <= tol * scale, r
+
+
 def pythagorean_residual(c, s):
     """||C^2 + S^2 - I||_1 (reported beside the parity numbers)."""
     c = np.asarray(c, dtype=np.float64)
