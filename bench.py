@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 cos/sin hot path (BASELINE.json metric).
+
+Default workload (configs[1]): a batch of 16384 float64 64x64 matrices,
+N(0,1) entries rescaled to 1-norm log-uniform in [1e-3, 1e2], cos+sin in the
+fused shared-memory kernel.  One step = one pass of the whole pipeline
+(norm, (k, s) selection, chain, doubling) over the batch.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config cfg2|cfg1|cfg3|cfg4|cfg5|sweep64..1024]
+
+N > 1 runs under torchrun, one rank per GPU: every rank owns its own
+16384-matrix shard (weak scaling, no collective on the data path); the step
+time is the max over ranks.  --impl reference times the reference algorithm
+(the oracle port, oracle/cossin_oracle.py) on the host cores with a process
+pool, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("matrices/sec and FP64 TFLOP/s (fraction of DMMA peak) for batched "
+          "cos+sin at n=64-1024")
+
+CONFIGS = {
+    # name: (kind, batch, n, dtype, precision, description)
+    "cfg1": ("cfg1", 1, 64, "f64", "double",
+             "single 64x64 f64, N(0,1) seed 0, 1-norm 2.0"),
+    "cfg2": ("cfg2", 16384, 64, "f64", "double",
+             "16384 x 64x64 f64, N(0,1), 1-norm log-uniform [1e-3, 1e2]"),
+    "cfg3": ("cfg3", 4096, 256, "f32", "single",
+             "4096 x 256x256 f32, U(-1,1), 1-norm log-uniform [1e-2, 50]"),
+    "cfg4": ("cfg4", 512, 512, "f64", "double",
+             "wave pair, 512 x 512x512 SPD Laplacian*(n+1)^2 + diag U(0,10),"
+             " t log-uniform [1e-4, 1e-1]"),
+    "cfg5": ("cfg5", 1, 8192, "f64", "double",
+             "one 8192x8192 f64 symmetric 20*(G+G^T)/(2 sqrt n)"),
+}
+for _n in (64, 128, 256, 512, 1024):
+    _b = max(1, (1 << 30) // (_n * _n * 8))
+    CONFIGS[f"sweep{_n}"] = ("cfg2", _b, _n, "f64", "double",
+                             f"{_b} x {_n}x{_n} f64, cfg2 distribution "
+                             "(~1 GiB input)")
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# Inputs (seeded synthetic data with the configs' shapes and distributions).
+
+def make_inputs(kind: str, batch: int, n: int, seed: int):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    t = None
+    if kind == "cfg1":
+        g = np.random.default_rng(0).standard_normal((64, 64))
+        a = (g * (2.0 / np.abs(g).sum(axis=0).max()))[None]
+    elif kind == "cfg5":
+        g = np.random.default_rng(seed).standard_normal((n, n))
+        a = (20.0 * (g + g.T) / (2.0 * math.sqrt(n)))[None]
+    else:
+        from oracle.cpu_pool import _gen  # same generator as the CPU leg
+        a, t = _gen(kind, seed, batch, n)
+    return a, t
+
+
+# ---------------------------------------------------------------------------
+# Clock sampling during the timed region.
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}",
+                     f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._th = threading.Thread(target=self._loop, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
+                    "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        pw = [float(r[2]) for r in self.rows
+              if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows),
+                "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------------
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline_leg(kind, n, seconds):
+    from oracle.cpu_pool import run_pool
+    per_worker = {"cfg2": 256, "cfg3": 8, "cfg4": 2}.get(kind, 64)
+    rate, workers, done, secs = run_pool(kind, n, per_worker,
+                                         min_seconds=seconds)
+    return rate, workers, done, secs, per_worker
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference algorithm (oracle port) on the host
+    cores, K timed steps after W warm-up steps, each a bounded sample."""
+    world, rank, _ = dist_setup(args)
+    kind, batch, n, dt, prec, desc = cfg
+    if rank != 0:
+        return
+    if kind in ("cfg1", "cfg5"):
+        from oracle import cossin_oracle as orc
+        a, _ = make_inputs(kind, batch, n, 0)
+        times = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            orc.cos_sin(a[0])
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        rate = 1.0 / statistics.mean(times)
+        cores, sample = os.cpu_count(), f"{args.steps} full calls"
+    else:
+        per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))
+        rates = []
+        for i in range(args.warmup + args.steps):
+            rate_i, workers, done, secs, pw = cpu_baseline_leg(kind, n, per_step)
+            if i >= args.warmup:
+                rates.append(rate_i)
+        rate = statistics.mean(rates)
+        cores = workers
+        sample = (f"{workers} processes x 1 BLAS thread, each re-running "
+                  f"{pw} seeded {desc.split(',')[0]} matrices for >= "
+                  f"{per_step:.1f} s per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate,
+        "unit": "matrices/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64" if dt == "f64" else "f32->f64", "data": "synthetic",
+        "config": {"workload": args.config, "description": desc},
+        "cpu_baseline": {"value": rate, "unit": "matrices/s", "cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": "matrices/s",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+
+    import paper_2010_00465_b200 as csm
+    from paper_2010_00465_b200 import _lib
+    from paper_2010_00465_b200.plan import BatchPlan
+
+    world, rank, local = dist_setup(args)
+    kind, batch, n, dt, prec, desc = cfg
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if pg is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if pg is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.SUM)
+        return float(t.item())
+
+    a_np, t_np = make_inputs(kind, batch, n, seed=rank)
+    tdtype = torch.float32 if dt == "f32" else torch.float64
+    a_np = a_np.astype(np.float32 if dt == "f32" else np.float64)
+    precision = csm.Precision.SINGLE if prec == "single" else csm.Precision.DOUBLE
+    wave = kind == "cfg4"
+    plan = BatchPlan(batch, n, tdtype, precision=precision, wave=wave,
+                     device=dev)
+    a_dev = torch.from_numpy(a_np).to(dev)
+    t_dev = torch.from_numpy(t_np).to(dev) if wave else None
+
+    # correctness spot check against the oracle (outside the timed region)
+    plan.run(a_dev, t_dev)
+    torch.cuda.synchronize()
+    st = plan.status.cpu().numpy()
+    assert not st.any(), "non-zero status in bench inputs"
+    ks = plan.k.cpu().numpy().astype(np.int64)
+    ss = plan.s.cpu().numpy().astype(np.int64)
+    from oracle import cossin_oracle as orc
+    for i in range(min(4, batch) if n >= 512 else min(8, batch)):
+        if wave:
+            c, s, k, sc = orc.wave_cos_sin(a_np[i], float(t_np[i]), prec)
+        else:
+            c, s, k, sc = orc.cos_sin(a_np[i].astype(np.float64), prec)
+        assert (int(ks[i]), int(ss[i])) == (k, sc), (i, ks[i], ss[i], k, sc)
+        cg = plan.cos[i].double().cpu().numpy()
+        err = np.abs(cg - c).sum(0).max() / max(np.abs(c).sum(0).max(), 1e-300)
+        assert err <= (1e-5 if dt == "f32" else 1e-10), (i, err)
+    flops_step = float((2.0 * n ** 3 * (ks + 2 * ss)).sum())
+
+    # warm-up, then K timed steps between barriers + synchronize
+    for _ in range(args.warmup):
+        plan.run(a_dev, t_dev)
+    torch.cuda.synchronize()
+    L = _lib.lib()
+    L.csm_profile_enable(1)
+    plan.launches = 0
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            plan.run(a_dev, t_dev)
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = e0.elapsed_time(e1)
+    kern_ms = ctypes_collect(L)
+    L.csm_profile_enable(0)
+    launches = plan.launches
+    ms_step = max_over_ranks(ms_total / args.steps)
+    units = sum_over_ranks(float(batch))
+    value = units / (ms_step * 1e-3)
+    tflops = sum_over_ranks(flops_step) / (ms_step * 1e-3) / 1e12
+
+    # e2e through the public plan API from pinned host memory
+    a_host = torch.from_numpy(a_np).pin_memory()
+    c_host = torch.empty(a_host.shape, dtype=tdtype).pin_memory()
+    s_host = torch.empty_like(c_host).pin_memory()
+    t_host = torch.from_numpy(t_np).pin_memory() if wave else None
+    e2e_steps = max(1, min(args.steps, 10))
+    for _ in range(2):
+        plan.run_host(a_host, c_host, s_host, t_host)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record()
+    for _ in range(e2e_steps):
+        plan.run_host(a_host, c_host, s_host, t_host)
+        _ = float(c_host[batch - 1, n - 1, n - 1])  # host read of the result
+    e3.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e2.elapsed_time(e3) / e2e_steps)
+    assert np.allclose(c_host[0].double().numpy(),
+                       plan.cos[0].double().cpu().numpy())
+    esz = 4 if dt == "f32" else 8
+    h2d = batch * n * n * esz + (batch * 8 if wave else 0)
+    d2h = 2 * batch * n * n * esz
+
+    peak = None
+    if rank == 0:
+        pk = ctypes.c_double(0.0)
+        if L.csm_fp64_peak(20000, ctypes.byref(pk), None) == 0:
+            peak = pk.value
+    kern_avg_ms = kern_ms[0] / max(kern_ms[1], 1)
+    achieved = flops_step / (kern_avg_ms * 1e-3) / 1e12 if kern_avg_ms > 0 else None
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof_json):
+        try:
+            traffic = json.load(open(prof_json)).get(args.config)
+        except Exception:
+            traffic = None
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline and kind not in ("cfg1", "cfg5"):
+        rate, workers, done, secs, pw = cpu_baseline_leg(kind, n, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "matrices/s", "cores": workers,
+               "kind": "port",
+               "sample": (f"oracle port of cos_sin/wave_cos_sin on {done} "
+                          f"matrices ({workers} processes x {pw} seeded "
+                          f"{desc.split(',')[0]} inputs, 1 BLAS thread each, "
+                          f"{secs:.1f} s)")}
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "matrices/s",
+        "tflops": tflops,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64" if dt == "f64" else "f32 storage, f64 compute",
+        "data": "synthetic (seeded; per-rank shard seed = rank)",
+        "config": {"workload": args.config, "description": desc,
+                   "batch_per_gpu": batch, "n": n, "precision_table": prec,
+                   "mean_products": float((ks + 2 * ss).mean()),
+                   "l2": "inputs larger than L2 (no flush needed)"
+                   if batch * n * n * esz > 2 * 126e6 else
+                   "input fits L2; steps reuse it (no flush)",
+                   "parallelism": f"batch shard x{world} (no collective)"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if (achieved and peak) else None,
+                     "traffic": traffic,
+                     "kernel": "fused64_kernel" if n <= 64 else "gemm_epi_kernel",
+                     "peak_source": "csm_fp64_peak: DMMA m8n8k4 loop on this "
+                                    "GPU in this run (MEASURED_PEAKS.json has "
+                                    "no FP64 entry)",
+                     "flops_per_step": flops_step,
+                     "kernel_ms_per_step": kern_avg_ms},
+        "e2e": {"value": batch * world / (e2e_ms * 1e-3), "unit": "matrices/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_ms},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+import ctypes  # noqa: E402
+
+
+def ctypes_collect(L):
+    tot = ctypes.c_double(0.0)
+    cnt = ctypes.c_int64(0)
+    L.csm_profile_collect(ctypes.byref(tot), ctypes.byref(cnt))
+    return tot.value, cnt.value
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warm-up raised to 3 (timing rule)")
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -145,6 +145,15 @@ int csm_theta_table(int family, int precision, double* theta_cos,
 int csm_fp64_peak(int iters, double* tflops, void* stream);
 int64_t csm_last_launch_count(void);
 
+/* Live timing of the dominant kernel: while enabled, every pipeline call on
+ * this thread records a CUDA event pair on its stream around the dominant
+ * kernel (the fused n <= 64 kernel, or the tiled GEMM launches).
+ * csm_profile_collect synchronises those events, returns the summed
+ * milliseconds and the number of intervals, and clears them.
+ * csm_profile_enable(0/1) also clears. */
+int csm_profile_enable(int on);
+int csm_profile_collect(double* total_ms, int64_t* intervals);
+
 #ifdef __cplusplus
 }
 #endif

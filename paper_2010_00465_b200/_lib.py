@@ -47,6 +47,8 @@ SIGNATURES = {
     "csm_theta_table": (_i32, [_i32, _i32, _vp, _vp, _vp, _i32]),
     "csm_fp64_peak": (_i32, [_i32, _vp, _vp]),
     "csm_last_launch_count": (_i64, []),
+    "csm_profile_enable": (_i32, [_i32]),
+    "csm_profile_collect": (_i32, [_vp, _vp]),
 }
 
 _LOCK = threading.Lock()

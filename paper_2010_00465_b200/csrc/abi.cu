@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/cossin_b200.h"
 #include "common.cuh"
@@ -36,6 +38,36 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
 }  // namespace csm
 
 namespace {
+thread_local bool g_prof = false;
+thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_ev;
+thread_local cudaEvent_t g_prof_open = nullptr;
+}  // namespace
+
+namespace csm {
+void prof_begin(cudaStream_t stream) {
+  if (!g_prof) return;
+  if (cudaEventCreate(&g_prof_open) != cudaSuccess) { g_prof_open = nullptr; return; }
+  cudaEventRecord(g_prof_open, stream);
+}
+void prof_end(cudaStream_t stream) {
+  if (!g_prof || !g_prof_open) return;
+  cudaEvent_t e1;
+  if (cudaEventCreate(&e1) != cudaSuccess) return;
+  cudaEventRecord(e1, stream);
+  g_prof_ev.emplace_back(g_prof_open, e1);
+  g_prof_open = nullptr;
+}
+}  // namespace csm
+
+namespace {
+
+void prof_clear() {
+  for (auto& p : g_prof_ev) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
+  g_prof_ev.clear();
+}
 
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
@@ -110,7 +142,9 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
   if (n <= 64) {
     e = cudaMemsetAsync(w.counter, 0, sizeof(int), stream);
     if (e != cudaSuccess) return cuda_fail(e, "memset counter");
+    csm::prof_begin(stream);
     e = csm::launch_fused64(dtype, wave, a, c, s, t, K, S, st, batch, n, w.counter, stream);
+    csm::prof_end(stream);
     if (e != cudaSuccess) return cuda_fail(e, "fused64 launch");
     ++g_launches;
   } else {
@@ -349,6 +383,28 @@ int csm_theta_table(int family, int precision, double* theta_cos, double* theta_
     k[i] = kk[family][precision][i];
   }
   return count;
+}
+
+int csm_profile_enable(int on) {
+  prof_clear();
+  g_prof = on != 0;
+  return CSM_SUCCESS;
+}
+
+int csm_profile_collect(double* total_ms, int64_t* intervals) {
+  if (!total_ms || !intervals) return fail(CSM_ERR_ARG, "null pointer argument");
+  double sum = 0.0;
+  for (auto& p : g_prof_ev) {
+    cudaError_t e = cudaEventSynchronize(p.second);
+    if (e != cudaSuccess) return cuda_fail(e, "profile events");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.first, p.second);
+    sum += ms;
+  }
+  *total_ms = sum;
+  *intervals = static_cast<int64_t>(g_prof_ev.size());
+  prof_clear();
+  return CSM_SUCCESS;
 }
 
 int csm_fp64_peak(int iters, double* tflops, void* stream_v) {

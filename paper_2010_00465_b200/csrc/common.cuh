@@ -95,4 +95,8 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// Live-timing hooks (abi.cu): no-ops unless csm_profile_enable(1).
+void prof_begin(cudaStream_t stream);
+void prof_end(cudaStream_t stream);
+
 }  // namespace csm

@@ -569,6 +569,7 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     attr_done = true;
   }
   const unsigned tiles = static_cast<unsigned>((NP / tk::BM) * (NP / tk::BN));
+  prof_begin(stream);
   for (const Launch& L : launches_v) {
     for (size_t done = 0; done < L.cnt; done += 65535) {
       const size_t cnt = std::min<size_t>(65535, L.cnt - done);
@@ -580,6 +581,7 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
   }
+  prof_end(stream);
 
   {
     const size_t nn = static_cast<size_t>(n) * n;

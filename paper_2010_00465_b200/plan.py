@@ -1,0 +1,144 @@
+"""Planned batched pipeline: buffers allocated once, stream-ordered runs.
+
+``BatchPlan`` is the serving/benchmark form of cos_sin_batched /
+wave_cos_sin_batched: it owns the device outputs, the (k, s, status) arrays
+and the C-ABI workspace, so a run is one C call with no allocation and no
+host synchronisation (n <= 64).  ``run_host`` streams a batch from pinned
+host memory through the device and back in chunks on three CUDA streams
+(H2D, compute, D2H), so the two PCIe directions and the kernels overlap.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from .records import _PREC_CODE, Precision
+
+
+def _vp(x: int) -> ctypes.c_void_p:
+    return ctypes.c_void_p(x)
+
+
+class BatchPlan:
+    """Pre-allocated pipeline for `batch` matrices of order n.
+
+    dtype: torch.float64 or torch.float32 (float32 computes in float64 and
+    stores float32).  wave=True plans the wave pair c(t^2 A), s(t, A)."""
+
+    def __init__(self, batch: int, n: int, dtype=None, *,
+                 precision: Precision = Precision.DOUBLE, wave: bool = False,
+                 device=None, chunk: int | None = None):
+        import torch
+        self.torch = torch
+        self.batch, self.n = int(batch), int(n)
+        self.dtype = dtype or torch.float64
+        self.code = _lib.F64 if self.dtype == torch.float64 else _lib.F32
+        self.precision = precision
+        self.wave = wave
+        self.device = torch.device(device or "cuda")
+        dev = self.device
+        shape = (self.batch, self.n, self.n)
+        self.cos = torch.empty(shape, dtype=self.dtype, device=dev)
+        self.sin = torch.empty_like(self.cos)
+        self.k = torch.empty(self.batch, dtype=torch.int32, device=dev)
+        self.s = torch.empty_like(self.k)
+        self.status = torch.empty_like(self.k)
+        self.chunk = int(chunk or self.batch) or 1
+        L = _lib.lib()
+        self.ws_bytes = int(L.csm_workspace_size(self.code, self.chunk, self.n))
+        self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8,
+                              device=dev)
+        self._a_dev = None
+        self._t_dev = None
+        self._streams = None
+        self.launches = 0
+
+    # -- one C-ABI call on a contiguous slice [lo, hi) -----------------------
+    def _call(self, a_ptr: int, lo: int, hi: int, stream_handle: int,
+              t_ptr: int | None) -> None:
+        L = _lib.lib()
+        esz = self.cos.element_size()
+        nn = self.n * self.n
+        cnt = hi - lo
+        out = [_vp(self.cos.data_ptr() + lo * nn * esz),
+               _vp(self.sin.data_ptr() + lo * nn * esz), cnt, self.n,
+               _vp(self.k.data_ptr() + 4 * lo), _vp(self.s.data_ptr() + 4 * lo),
+               _vp(self.status.data_ptr() + 4 * lo), _vp(self.ws.data_ptr()),
+               self.ws_bytes, _vp(stream_handle)]
+        if self.wave:
+            rc = L.csm_wave(self.code, _PREC_CODE[self.precision], _vp(a_ptr),
+                            _vp(t_ptr), *out)
+        else:
+            rc = L.csm_cos_sin(self.code, _PREC_CODE[self.precision],
+                               _vp(a_ptr), *out)
+        _lib.check(rc, "csm_wave" if self.wave else "csm_cos_sin")
+        self.launches += int(L.csm_last_launch_count())
+
+    def run(self, a, t=None, stream=None):
+        """Device-resident run on the whole batch (a: CUDA tensor, C-order).
+        Returns (cos, sin, k, s, status) device tensors; no host sync."""
+        torch = self.torch
+        if a.shape != (self.batch, self.n, self.n) or a.dtype != self.dtype:
+            raise ValueError("input does not match the plan")
+        a = a.contiguous()
+        st = stream or torch.cuda.current_stream()
+        h = int(st.cuda_stream)
+        tp = None
+        if self.wave:
+            tp = t.contiguous().data_ptr()
+        esz = a.element_size()
+        nn = self.n * self.n
+        tsz = 8
+        for lo in range(0, self.batch, self.chunk):
+            hi = min(self.batch, lo + self.chunk)
+            self._call(a.data_ptr() + lo * nn * esz, lo, hi, h,
+                       None if tp is None else tp + lo * tsz)
+        return self.cos, self.sin, self.k, self.s, self.status
+
+    def run_host(self, a_host, cos_host, sin_host, t_host=None,
+                 chunks: int = 8) -> None:
+        """Host->device->host run: pinned CPU tensors in and out, chunked
+        over H2D / compute / D2H streams.  Ends with the current stream
+        waiting on the last D2H copy (call synchronize to read results)."""
+        torch = self.torch
+        if self._a_dev is None:
+            self._a_dev = torch.empty((self.batch, self.n, self.n),
+                                      dtype=self.dtype, device=self.device)
+            if self.wave:
+                self._t_dev = torch.empty(self.batch, dtype=torch.float64,
+                                          device=self.device)
+            self._streams = [torch.cuda.Stream(device=self.device)
+                             for _ in range(3)]
+        if self.chunk < (self.batch + chunks - 1) // chunks:
+            chunks = (self.batch + self.chunk - 1) // self.chunk
+        s_h2d, s_cmp, s_d2h = self._streams
+        cur = torch.cuda.current_stream()
+        for s in self._streams:
+            s.wait_stream(cur)
+        step = (self.batch + chunks - 1) // chunks
+        nn = self.n * self.n
+        esz = self._a_dev.element_size()
+        for lo in range(0, self.batch, step):
+            hi = min(self.batch, lo + step)
+            with torch.cuda.stream(s_h2d):
+                self._a_dev[lo:hi].copy_(a_host[lo:hi], non_blocking=True)
+                if self.wave:
+                    self._t_dev[lo:hi].copy_(t_host[lo:hi], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_h2d)
+            s_cmp.wait_event(ev_in)
+            for clo in range(lo, hi, self.chunk):
+                chi = min(hi, clo + self.chunk)
+                self._call(self._a_dev.data_ptr() + clo * nn * esz, clo, chi,
+                           int(s_cmp.cuda_stream),
+                           None if not self.wave
+                           else self._t_dev.data_ptr() + 8 * clo)
+            ev_out = torch.cuda.Event()
+            ev_out.record(s_cmp)
+            s_d2h.wait_event(ev_out)
+            with torch.cuda.stream(s_d2h):
+                cos_host[lo:hi].copy_(self.cos[lo:hi], non_blocking=True)
+                sin_host[lo:hi].copy_(self.sin[lo:hi], non_blocking=True)
+        cur.wait_stream(s_d2h)
+        cur.wait_stream(s_cmp)
+        cur.wait_stream(s_h2d)
