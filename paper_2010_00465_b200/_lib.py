@@ -56,7 +56,8 @@ _LIB: ctypes.CDLL | None = None
 
 
 def lib_path() -> str:
-    return _build.LIB
+    """The in-tree library, or $CSM_LIB_PATH (e.g. an instrumented build)."""
+    return os.environ.get("CSM_LIB_PATH") or _build.LIB
 
 
 def lib() -> ctypes.CDLL:

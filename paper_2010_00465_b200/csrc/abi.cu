@@ -29,8 +29,12 @@ cudaError_t launch_fill_ks(int32_t* K, int32_t* S, int32_t* status, int64_t batc
                            cudaStream_t stream);
 cudaError_t launch_fused64(int dtype, bool wave, const void* a, void* c, void* s,
                            const double* t, const int32_t* k, const int32_t* sx,
-                           const int32_t* st, int64_t batch, int n, int* counter,
+                           const int32_t* st, const int32_t* order, int64_t batch, int n,
                            cudaStream_t stream);
+size_t schedule_ws_bytes();
+cudaError_t launch_schedule(const int32_t* K, const int32_t* S, const int32_t* status,
+                            int64_t batch, int* bins, int32_t* order, cudaStream_t stream,
+                            int64_t* launches);
 size_t tiled_workspace_bytes(int64_t batch, int n);
 cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void* c_out,
                       void* s_out, int64_t batch, int n, const int32_t* dK, const int32_t* dS,
@@ -87,12 +91,14 @@ struct CommonWs {
   unsigned long long* normbits;
   int32_t* kbuf;
   int32_t* sbuf;
-  int* counter;
+  int32_t* order;  // cost-sorted schedule of the fused kernel
+  int* bins;       // counting-sort scratch
   void* tiled;
 };
 
 size_t common_bytes(int64_t batch) {
-  return align256(static_cast<size_t>(batch) * 8) + 2 * align256(static_cast<size_t>(batch) * 4) + 256;
+  return align256(static_cast<size_t>(batch) * 8) + 3 * align256(static_cast<size_t>(batch) * 4) +
+         align256(csm::schedule_ws_bytes());
 }
 
 CommonWs carve(void* ws, int64_t batch) {
@@ -104,8 +110,10 @@ CommonWs carve(void* ws, int64_t batch) {
   p += align256(static_cast<size_t>(batch) * 4);
   w.sbuf = reinterpret_cast<int32_t*>(p);
   p += align256(static_cast<size_t>(batch) * 4);
-  w.counter = reinterpret_cast<int*>(p);
-  p += 256;
+  w.order = reinterpret_cast<int32_t*>(p);
+  p += align256(static_cast<size_t>(batch) * 4);
+  w.bins = reinterpret_cast<int*>(p);
+  p += align256(csm::schedule_ws_bytes());
   w.tiled = p;
   return w;
 }
@@ -140,10 +148,10 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
   if (n == 0 || batch == 0) return CSM_SUCCESS;
   cudaError_t e;
   if (n <= 64) {
-    e = cudaMemsetAsync(w.counter, 0, sizeof(int), stream);
-    if (e != cudaSuccess) return cuda_fail(e, "memset counter");
+    e = csm::launch_schedule(K, S, st, batch, w.bins, w.order, stream, &g_launches);
+    if (e != cudaSuccess) return cuda_fail(e, "schedule kernels");
     csm::prof_begin(stream);
-    e = csm::launch_fused64(dtype, wave, a, c, s, t, K, S, st, batch, n, w.counter, stream);
+    e = csm::launch_fused64(dtype, wave, a, c, s, t, K, S, st, w.order, batch, n, stream);
     csm::prof_end(stream);
     if (e != cudaSuccess) return cuda_fail(e, "fused64 launch");
     ++g_launches;
@@ -384,6 +392,19 @@ int csm_theta_table(int family, int precision, double* theta_cos, double* theta_
   }
   return count;
 }
+
+#ifdef CSM_TRACE
+int csm_trace_dump(unsigned long long* out, int cap) {
+  int n = 0;
+  cudaMemcpyFromSymbol(&n, csm::f64k::g_trace_n, sizeof(int));
+  if (n > cap) n = cap;
+  if (n > (1 << 16)) n = 1 << 16;
+  cudaMemcpyFromSymbol(out, csm::f64k::g_trace, sizeof(unsigned long long) * n);
+  int zero = 0;
+  cudaMemcpyToSymbol(csm::f64k::g_trace_n, &zero, sizeof(int));
+  return n;
+}
+#endif
 
 int csm_profile_enable(int on) {
   prof_clear();

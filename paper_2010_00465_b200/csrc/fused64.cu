@@ -1,20 +1,32 @@
 // fused64.cu -- K1: the whole cos/sin (or wave) pipeline for n <= 64 with
 // every intermediate resident in shared memory.
 //
-// One persistent CTA per SM (256 threads, 8 warps) pulls matrices from an
-// atomic work counter.  A matrix is zero-padded to 64x64 (block-diagonal
-// padding is exact: the padded block evolves as p(0) I and never touches
-// the real block).  Seven 32 KiB slots: six hold the chain's live set
-// (peak six for the degree-12 chain) and the
-// seventh receives the NEXT matrix by cp.async while this one computes.
+// One persistent CTA per SM (256 threads, 8 warps) walks a static snake
+// schedule over the matrices sorted by cost k + 2s (K0 builds it), so the
+// CTAs finish together without a shared work queue.  A matrix is
+// zero-padded to 64x64 (block-diagonal padding is exact: the padded block
+// evolves as p(0) I and never touches the real block).  Seven 32 KiB
+// slots: the input A (slot 0), five work slots and slot 6, which receives
+// the NEXT matrix's input by one TMA bulk copy as soon as the current chain
+// no longer needs it as a work slot.
 //
-// Every product is a 64x64x64 FP64 GEMM on the DMMA pipe (mma.sync
-// m8n8k4): warp w owns rows [16(w/2), +16) x cols [32(w%2), +32) = 2x4
-// DMMA tiles; doubling steps and the wave k=3 sine are DUAL products that
-// share the right operand and reuse its fragments.  Linear combinations
-// run in the GEMM epilogue on the accumulator registers (never a separate
-// pass).  Slots use an XOR swizzle on 32-byte chunks so both DMMA fragment
-// loads are bank-conflict free.
+// The chain of scheme k is a short PROGRAM of steps (kChains below): each
+// step is one 64x64x64 FP64 product on the DMMA pipe (mma.sync m8n8k4; or a
+// dual product sharing its right operand) followed by an epilogue that
+// forms the scheme's linear combinations from the accumulator registers and
+// writes them to slots that are not operands of the step, then one barrier.
+// So the GEMM code exists once, every lincomb is fused, and there is one
+// __syncthreads per product.
+//
+// Layout: slot element (r, c) lives at r*64 + 2*((c/2) ^ f(r)) + (c&1) with
+// f(r) = ((r&1)<<2) | (r&2): an XOR swizzle on 16-byte pairs that makes the
+// DMMA A/B fragment loads (LDS.64) and the epilogue's 16-byte accesses in
+// accumulator layout all bank-conflict free.
+//
+// Scaling is folded: Taylor never uses A elementwise, so y = 2^-2s (A A)
+// and sin = 2^-s (A sc) are exact power-of-two rescalings of the
+// accumulators (driver.py:115); the wave family materialises y = (t')^2 A
+// (schemes.py:424) in place.
 //
 // Reference mapping: chains schemes.py:264-361, trig use :376-395, wave use
 // :411-430, scaling driver.py:115/:139, doubling driver.py:91-98.
@@ -24,18 +36,166 @@ namespace csm {
 
 namespace f64k {
 
+// Optional phase trace (build with -DCSM_TRACE; tools/trace_fused.py): CTA 0,
+// thread 0 logs (clock64 << 8 | tag) at phase boundaries.
+#ifdef CSM_TRACE
+__device__ unsigned long long g_trace[1 << 16];
+__device__ int g_trace_n;
+__device__ __forceinline__ int& trace_count() {
+  __shared__ int n;  // only thread 0 of CTA 0 touches it
+  return n;
+}
+#define CSM_TRACE_EV(tag, val)                                                    \
+  do {                                                                            \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                    \
+      const int i_ = trace_count()++;                                             \
+      if (i_ < (1 << 16)) g_trace[i_] = ((val) << 8) | (tag);                     \
+      g_trace_n = i_ + 1;                                                         \
+    }                                                                             \
+  } while (0)
+#else
+#define CSM_TRACE_EV(tag, val) do { } while (0)
+#endif
+#define TRACE_T(tag) CSM_TRACE_EV(tag, static_cast<unsigned long long>(clock64()))
+
 constexpr int NP = 64;
 constexpr int SLOT = NP * NP;  // doubles per slot
 constexpr int NSLOTS = 7;
 constexpr int THREADS = 256;
 
+__host__ __device__ constexpr int swz_f(int r) { return ((r & 1) << 2) | (r & 2); }
 __device__ __forceinline__ int swz(int r, int c) {
-  return r * NP + ((((c >> 2) ^ (r & 7))) << 2) + (c & 3);
+  return r * NP + 2 * ((c >> 1) ^ swz_f(r)) + (c & 1);
 }
+
+// ---------------------------------------------------------------------------
+// Chain programs.
+
+enum Epi : int8_t {
+  E_SCALED,    // o0 = scale * acc
+  E_DEG2,      // o0 = I - y/2 + acc/24 ; o1 = I - y/6 + acc/120            (y=i0)
+  E_DEG4A,     // o0 = acc ; o1 = -y/720 + acc/40320                        (y=i0)
+  E_DEG4B,     // o0 = I - y/2 + y2/24 + acc ; o1 = I - y/6 + y2/120 + acc/7 (y,y2)
+  E_DEG4W1,    // o0 = acc ; o1 = -y/720 + acc/40320 ; o2 = -y/5040 + acc/9! (y)
+  E_DEG4W2,    // dual: o0 = I - y/2 + y2/24 + q ; o1 = tp (I - y/6 + y2/120 + q9)
+  E_DEG8A,     // o0 = acc ; o1 = x1 y + x2 acc                             (y)
+  E_DEG8B,     // o0 = acc ; o1 = x3 y2 + acc ; o2 = x4 I + x5 y + x6 y2 + x7 acc
+  E_DEG8C,     // o0 = cos ; o1 = inner ; keep = sin base     (y, y2, p8)
+  E_KEEP,      // o0 = scale * (keep + acc)
+  E_DEG12B,    // o0 = acc ; o1 = c4                                        (y, y2)
+  E_DEG12C,    // o0 = mid = c3 + acc ; o1 = c2 + mid                       (y, y2, y3)
+  E_DEG12D,    // o0 = cos = c1 + acc ; o1 = inner ; keep = sin base (y,y2,y3,mid)
+};
+
+enum Scale : int8_t { SC_ONE = 0, SC_F = 1, SC_F2 = 2, SC_TP = 3 };
+
+struct __align__(16) Step {
+  int8_t dual;            // 0: acc = L1 R ; 1: acc = L1 R, acc2 = L2 R
+  int8_t l1, l2, r;       // operand slots
+  int8_t epi, scale;
+  int8_t o0, o1, o2;      // output slots (-1 unused)
+  int8_t i0, i1, i2, i3;  // elementwise input slots (-1 unused)
+  int8_t pad[3];
+};
+static_assert(sizeof(Step) == 16, "one 128-bit load per step");
+
+struct __align__(16) Chain {
+  int8_t nsteps;
+  int8_t cos_slot, sin_slot, free1, free2;  // final pair and two free slots
+  int8_t pf_after;  // the next matrix's input may land in slot 6 after this step
+  int8_t cos_step, cos_out, sin_step, sin_out;  // producers of the final pair
+  int8_t pad[6];
+  Step step[7];
+};
+static_assert(sizeof(Chain) == 128, "chain table layout");
+
+// Slot ids: 0 = this matrix's input (A, or y for the wave family), 1..6 =
+// work slots; slot 6 doubles as the landing buffer of the next matrix's
+// input, so a chain may use it only up to step pf_after.
+#define S_(d, l1, l2, r, e, sc, o0, o1, o2, i0, i1, i2, i3) \
+  {d, l1, l2, r, e, sc, o0, o1, o2, i0, i1, i2, i3, {0, 0, 0}}
+#define H_(ns, cs, ss, f1, f2, pf, cst, co, sst, so) \
+  ns, cs, ss, f1, f2, pf, cst, co, sst, so, {0, 0, 0, 0, 0, 0}
+constexpr int8_t X = -1;
+
+__constant__ Chain kChains[7] = {
+    // [0] Taylor k=3: chain_deg2 (schemes.py:264-272); sin = A sc (:394)
+    {H_(3, 2, 4, 1, 3, 0, 1, 0, 2, 0),
+     {S_(0, 0, X, 0, E_SCALED, SC_F2, 1, X, X, X, X, X, X),     // y = A A
+      S_(0, 1, X, 1, E_DEG2, SC_ONE, 2, 3, X, 1, X, X, X),       // cos, sc
+      S_(0, 0, X, 3, E_SCALED, SC_F, 4, X, X, X, X, X, X)}},     // sin = A sc
+    // [1] Taylor k=4: chain_deg4(exact_sine=False) (:275-299)
+    {H_(4, 4, 1, 2, 3, 0, 2, 0, 3, 0),
+     {S_(0, 0, X, 0, E_SCALED, SC_F2, 1, X, X, X, X, X, X),     // y
+      S_(0, 1, X, 1, E_DEG4A, SC_ONE, 2, 3, X, 1, X, X, X),      // y2, L
+      S_(0, 2, X, 3, E_DEG4B, SC_ONE, 4, 5, X, 1, 2, X, X),      // cos, sc
+      S_(0, 0, X, 5, E_SCALED, SC_F, 1, X, X, X, X, X, X)}},     // sin
+    // [2] Taylor k=6: chain_deg8 (:302-326)
+    {H_(6, 3, 5, 1, 2, 3, 3, 0, 5, 0),
+     {S_(0, 0, X, 0, E_SCALED, SC_F2, 1, X, X, X, X, X, X),     // y
+      S_(0, 1, X, 1, E_DEG8A, SC_ONE, 2, 3, X, 1, X, X, X),      // y2, L
+      S_(0, 2, X, 3, E_DEG8B, SC_ONE, 4, 5, 6, 1, 2, X, X),      // p8, L2, R2
+      S_(0, 5, X, 6, E_DEG8C, SC_ONE, 3, 1, X, 1, 2, 4, X),      // cos, inner
+      S_(0, 1, X, 4, E_KEEP, SC_ONE, 2, X, X, X, X, X, X),       // sc
+      S_(0, 0, X, 2, E_SCALED, SC_F, 5, X, X, X, X, X, X)}},     // sin = A sc
+    // [3] Taylor k=7: chain_deg12 (:329-361)
+    {H_(7, 4, 5, 1, 2, 4, 4, 0, 6, 0),
+     {S_(0, 0, X, 0, E_SCALED, SC_F2, 1, X, X, X, X, X, X),     // y
+      S_(0, 1, X, 1, E_SCALED, SC_ONE, 2, X, X, X, X, X, X),     // y2
+      S_(0, 2, X, 1, E_DEG12B, SC_ONE, 3, 4, X, 1, 2, X, X),     // y3, c4
+      S_(0, 4, X, 4, E_DEG12C, SC_ONE, 5, 6, X, 1, 2, 3, X),     // mid, L
+      S_(0, 6, X, 5, E_DEG12D, SC_ONE, 4, 1, X, 1, 2, 3, 5),     // cos, inner
+      S_(0, 1, X, 4, E_KEEP, SC_ONE, 2, X, X, X, X, X, X),       // sc
+      S_(0, 0, X, 2, E_SCALED, SC_F, 5, X, X, X, X, X, X)}},     // sin = A sc
+    // [4] wave k=3: chain_deg4(exact_sine=True) on y (slot 0), :426-427
+    {H_(2, 4, 5, 1, 2, 0, 1, 0, 1, 1),
+     {S_(0, 0, X, 0, E_DEG4W1, SC_ONE, 1, 2, 3, 0, X, X, X),     // y2, L, L9
+      S_(1, 2, 3, 1, E_DEG4W2, SC_TP, 4, 5, X, 0, 1, X, X)}},    // cos, s
+    // [5] wave k=4: chain_deg8 on y
+    {H_(4, 2, 4, 1, 3, 0, 2, 0, 3, 0),
+     {S_(0, 0, X, 0, E_DEG8A, SC_ONE, 1, 2, X, 0, X, X, X),      // y2, L
+      S_(0, 1, X, 2, E_DEG8B, SC_ONE, 3, 4, 5, 0, 1, X, X),      // p8, L2, R2
+      S_(0, 4, X, 5, E_DEG8C, SC_ONE, 2, 1, X, 0, 1, 3, X),      // cos, inner
+      S_(0, 1, X, 3, E_KEEP, SC_TP, 4, X, X, X, X, X, X)}},      // s
+    // [6] wave k=5: chain_deg12 on y
+    {H_(5, 3, 2, 1, 4, 0, 3, 0, 4, 0),
+     {S_(0, 0, X, 0, E_SCALED, SC_ONE, 1, X, X, X, X, X, X),     // y2
+      S_(0, 1, X, 0, E_DEG12B, SC_ONE, 2, 3, X, 0, 1, X, X),     // y3, c4
+      S_(0, 3, X, 3, E_DEG12C, SC_ONE, 4, 5, X, 0, 1, 2, X),     // mid, L
+      S_(0, 5, X, 4, E_DEG12D, SC_ONE, 3, 1, X, 0, 1, 2, 4),     // cos, inner
+      S_(0, 1, X, 3, E_KEEP, SC_TP, 2, X, X, X, X, X, X)}},      // s
+};
+#undef H_
+#undef S_
+
+// ---------------------------------------------------------------------------
+// Per-thread geometry: warp w owns rows [16(w/2), +16) x cols [32(w%2), +32)
+// = 2 x 4 DMMA tiles; lane = 4g + t.
 
 struct Lane {
   int rb, cb, g, t;
+  int aoff[2][4];  // A-fragment element offsets: row mi, chunk q (+16 m)
+  int boff[4];     // B-fragment element offsets for tile ni (+64 kk)
 };
+
+__device__ __forceinline__ void make_lane(Lane& ln) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ln.rb = (warp >> 1) * 16;
+  ln.cb = (warp & 1) * 32;
+  ln.g = lane >> 2;
+  ln.t = lane & 3;
+  // A: element (r = rb + 8 mi + g, c = 4 j + t), j = 4 m + q
+  //    -> r*64 + 4 ((j) ^ h) + t with h = f(g)/2 (affects the low 2 bits of j)
+  const int h = swz_f(ln.g) >> 1;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      ln.aoff[mi][q] = (ln.rb + mi * 8 + ln.g) * NP + 4 * (q ^ h) + ln.t;
+  // B: element (r = kk + t, c = cb + 8 ni + g) -> kk*64 + swz(t, c) (f(r) = f(t))
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni) ln.boff[ni] = swz(ln.t, ln.cb + ni * 8 + ln.g);
+}
 
 typedef double Acc[2][4][2];
 
@@ -46,65 +206,33 @@ __device__ __forceinline__ void zero(Acc& a) {
     for (int j = 0; j < 4; ++j) a[i][j][0] = a[i][j][1] = 0.0;
 }
 
-// acc = L * R over the full 64-deep contraction.
-__device__ __forceinline__ void gemm1(const double* __restrict__ L,
-                                      const double* __restrict__ R, Acc& acc,
-                                      const Lane& ln) {
+// acc = L * R (and acc2 = L2 * R when DUAL), full 64-deep contraction.
+template <bool DUAL>
+__device__ __forceinline__ void gemm(const double* __restrict__ L,
+                                     const double* __restrict__ L2,
+                                     const double* __restrict__ R, Acc& acc,
+                                     Acc& acc2, const Lane& ln) {
   zero(acc);
+  if (DUAL) zero(acc2);
 #pragma unroll
   for (int kk = 0; kk < NP; kk += 4) {
-    double a[2], b[4];
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi) a[mi] = L[swz(ln.rb + mi * 8 + ln.g, kk + ln.t)];
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) b[ni] = R[swz(kk + ln.t, ln.cb + ni * 8 + ln.g)];
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
-  }
-}
-
-// acc1 = L1 * R, acc2 = L2 * R (shared right-operand fragments).
-__device__ __forceinline__ void gemm2(const double* __restrict__ L1,
-                                      const double* __restrict__ L2,
-                                      const double* __restrict__ R, Acc& acc1,
-                                      Acc& acc2, const Lane& ln) {
-  zero(acc1);
-  zero(acc2);
-#pragma unroll
-  for (int kk = 0; kk < NP; kk += 4) {
-    double a1[2], a2[2], b[4];
+    const int j = kk >> 2, m = j >> 2, q = j & 3;
+    double a[2], a2[2], b[4];
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi) {
-      a1[mi] = L1[swz(ln.rb + mi * 8 + ln.g, kk + ln.t)];
-      a2[mi] = L2[swz(ln.rb + mi * 8 + ln.g, kk + ln.t)];
+      a[mi] = L[ln.aoff[mi][q] + 16 * m];
+      if (DUAL) a2[mi] = L2[ln.aoff[mi][q] + 16 * m];
     }
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) b[ni] = R[swz(kk + ln.t, ln.cb + ni * 8 + ln.g)];
+    for (int ni = 0; ni < 4; ++ni) b[ni] = R[ln.boff[ni] + NP * kk];
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) {
-        dmma(acc1[mi][ni], a1[mi], b[ni]);
-        dmma(acc2[mi][ni], a2[mi], b[ni]);
+        dmma(acc[mi][ni], a[mi], b[ni]);
+        if (DUAL) dmma(acc2[mi][ni], a2[mi], b[ni]);
       }
   }
-}
-
-// Visit the 8 element pairs this thread owns (its accumulator positions).
-// f(mi, ni, off, i0, i1): off = swizzled offset of the pair, i0/i1 = 1.0
-// where the pair's first/second element lies on the diagonal, else 0.0.
-template <class F>
-__device__ __forceinline__ void owned(const Lane& ln, F&& f) {
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int r = ln.rb + mi * 8 + ln.g;
-      const int c = ln.cb + ni * 8 + 2 * ln.t;
-      f(mi, ni, swz(r, c), r == c ? 1.0 : 0.0, r == c + 1 ? 1.0 : 0.0);
-    }
 }
 
 __device__ __forceinline__ double2 ld2(const double* p, int off) {
@@ -114,268 +242,229 @@ __device__ __forceinline__ void st2(double* p, int off, double x, double y) {
   *reinterpret_cast<double2*>(p + off) = make_double2(x, y);
 }
 
-// Store one result pair: acc values in, slot out.
-__device__ __forceinline__ void store_acc(double* dst, const Acc& acc,
-                                          const Lane& ln) {
-  owned(ln, [&](int mi, int ni, int off, double, double) {
-    st2(dst, off, acc[mi][ni][0], acc[mi][ni][1]);
-  });
-}
-
 // ---------------------------------------------------------------------------
-// Chains.  Each leaves cos / sin slot pointers in *pc / *ps.  `Y` is the even
-// variable's slot for the wave family (y = t^2 A) and A for Taylor.
-// Between a product and its epilogue there is a barrier, so an epilogue may
-// overwrite the product's own operands; elementwise reads and writes happen
-// only at the thread's own positions.
+// Epilogue: one formula per Epi, evaluated on the thread's 8 owned pairs.
 
-// Taylor k=3 -- chain_deg2 (schemes.py:264-272) + sin = A sc (:394).
-__device__ void taylor3(double* A, double* const* W, const Lane& ln,
-                        double** pc, double** ps) {
-  Acc acc;
-  gemm1(A, A, acc, ln);
-  store_acc(W[0], acc, ln);  // y
-  __syncthreads();
-  gemm1(W[0], W[0], acc, ln);  // y2
-  owned(ln, [&](int mi, int ni, int off, double i0, double i1) {
-    double2 y = ld2(W[0], off);
-    const double* a = acc[mi][ni];
-    double c0 = fma(1.0 / 24.0, a[0], fma(-0.5, y.x, i0));
-    double c1 = fma(1.0 / 24.0, a[1], fma(-0.5, y.y, i1));
-    double s0 = fma(1.0 / 120.0, a[0], fma(-1.0 / 6.0, y.x, i0));
-    double s1 = fma(1.0 / 120.0, a[1], fma(-1.0 / 6.0, y.y, i1));
-    st2(W[1], off, c0, c1);
-    st2(W[2], off, s0, s1);
-  });
-  __syncthreads();
-  gemm1(A, W[2], acc, ln);
-  store_acc(W[3], acc, ln);
-  __syncthreads();
-  *pc = W[1];
-  *ps = W[3];
-}
+template <typename TOut>
+struct EpiArgs {
+  double* o[3];        // shared-memory outputs
+  TOut* g[3];          // optional global outputs (final cos / sin when s == 0)
+  const double* in[4];
+  double scale;
+  int n;
+};
 
-// Taylor k=4 -- chain_deg4(exact_sine=False) (schemes.py:275-299).
-__device__ void taylor4(double* A, double* const* W, const Lane& ln,
-                        double** pc, double** ps) {
-  Acc acc;
-  gemm1(A, A, acc, ln);
-  store_acc(W[0], acc, ln);  // y
-  __syncthreads();
-  gemm1(W[0], W[0], acc, ln);  // y2
-  owned(ln, [&](int mi, int ni, int off, double, double) {
-    double2 y = ld2(W[0], off);
-    const double* a = acc[mi][ni];
-    st2(W[1], off, a[0], a[1]);
-    st2(W[2], off, fma(1.0 / 40320.0, a[0], (-1.0 / 720.0) * y.x),
-        fma(1.0 / 40320.0, a[1], (-1.0 / 720.0) * y.y));
-  });
-  __syncthreads();
-  gemm1(W[1], W[2], acc, ln);  // q = y2 (-y/720 + y2/40320)
-  owned(ln, [&](int mi, int ni, int off, double i0, double i1) {
-    double2 y = ld2(W[0], off), y2 = ld2(W[1], off);
-    const double* q = acc[mi][ni];
-    double c0 = q[0] + fma(1.0 / 24.0, y2.x, fma(-0.5, y.x, i0));
-    double c1 = q[1] + fma(1.0 / 24.0, y2.y, fma(-0.5, y.y, i1));
-    double s0 = fma(720.0 / 5040.0, q[0], fma(1.0 / 120.0, y2.x, fma(-1.0 / 6.0, y.x, i0)));
-    double s1 = fma(720.0 / 5040.0, q[1], fma(1.0 / 120.0, y2.y, fma(-1.0 / 6.0, y.y, i1)));
-    st2(W[3], off, c0, c1);
-    st2(W[4], off, s0, s1);
-  });
-  __syncthreads();
-  gemm1(A, W[4], acc, ln);
-  store_acc(W[0], acc, ln);  // sin (y is dead)
-  __syncthreads();
-  *pc = W[3];
-  *ps = W[0];
-}
-
-// Degree-8 core (schemes.py:302-326) on even variable in slot Y; y2 is
-// computed first.  Taylor k=6 (sin = A sc) and wave k=4 (s = tp sc).
-template <bool WAVE>
-__device__ void deg8(double* A, double* Y, double* const* W, double tp,
-                     const Lane& ln, double** pc, double** ps) {
-  const double* x = dTables.x8;  // x[0] = x1
-  const double* z = dTables.z8;
-  Acc acc;
-  // W slots (4): y2/sc, L/R2/inner/sin, p8, L2/cos
-  double *sY2 = W[0], *sL = W[1], *sP8 = W[2], *sL2 = W[3], *sR2 = W[1];
-  gemm1(Y, Y, acc, ln);  // y2
-  owned(ln, [&](int mi, int ni, int off, double, double) {
-    double2 y = ld2(Y, off);
-    const double* a = acc[mi][ni];
-    st2(sY2, off, a[0], a[1]);
-    st2(sL, off, fma(x[1], a[0], x[0] * y.x), fma(x[1], a[1], x[0] * y.y));
-  });
-  __syncthreads();
-  gemm1(sY2, sL, acc, ln);  // p8 = y2 (x1 y + x2 y2)
-  __syncthreads();           // sR2 overwrites sL
-  owned(ln, [&](int mi, int ni, int off, double i0, double i1) {
-    double2 y = ld2(Y, off), y2 = ld2(sY2, off);
-    const double* p = acc[mi][ni];
-    st2(sP8, off, p[0], p[1]);
-    st2(sL2, off, fma(x[2], y2.x, p[0]), fma(x[2], y2.y, p[1]));
-    st2(sR2, off, fma(x[6], p[0], fma(x[5], y2.x, fma(x[4], y.x, x[3] * i0))),
-        fma(x[6], p[1], fma(x[5], y2.y, fma(x[4], y.y, x[3] * i1))));
-  });
-  __syncthreads();
-  gemm1(sL2, sR2, acc, ln);  // p16
-  __syncthreads();            // cos overwrites L2, inner overwrites R2
-  double sb[2][4][2];
-  double *sCos = sL2, *sInner = sR2;
-  owned(ln, [&](int mi, int ni, int off, double i0, double i1) {
-    double2 y = ld2(Y, off), y2 = ld2(sY2, off), p8 = ld2(sP8, off);
-    const double* p = acc[mi][ni];
-    double c0 = p[0] + fma(x[7], y2.x, fma(-0.5, y.x, i0));
-    double c1 = p[1] + fma(x[7], y2.y, fma(-0.5, y.y, i1));
-    // inner = z5 I + z5 y + z6 y2 + z7 p8 + z8 cos
-    double n0 = fma(z[8], c0, fma(z[7], p8.x, fma(z[6], y2.x, fma(z[5], y.x, z[5] * i0))));
-    double n1 = fma(z[8], c1, fma(z[7], p8.y, fma(z[6], y2.y, fma(z[5], y.y, z[5] * i1))));
-    // sin base = z0 I + z1 y + z2 y2 + z3 p8 + z4 cos
-    sb[mi][ni][0] = fma(z[4], c0, fma(z[3], p8.x, fma(z[2], y2.x, fma(z[1], y.x, z[0] * i0))));
-    sb[mi][ni][1] = fma(z[4], c1, fma(z[3], p8.y, fma(z[2], y2.y, fma(z[1], y.y, z[0] * i1))));
-    st2(sCos, off, c0, c1);
-    st2(sInner, off, n0, n1);
-  });
-  __syncthreads();
-  gemm1(sInner, sP8, acc, ln);  // tail
-  double* sSc = sY2;             // y2 dead after the p16 epilogue
-  owned(ln, [&](int mi, int ni, int off, double, double) {
-    double v0 = sb[mi][ni][0] + acc[mi][ni][0];
-    double v1 = sb[mi][ni][1] + acc[mi][ni][1];
-    if (WAVE) { v0 *= tp; v1 *= tp; }
-    st2(sSc, off, v0, v1);
-  });
-  __syncthreads();
-  *pc = sCos;
-  if (WAVE) {
-    *ps = sSc;
-  } else {
-    gemm1(A, sSc, acc, ln);
-    store_acc(sInner, acc, ln);  // sin (inner dead)
-    __syncthreads();
-    *ps = sInner;
+// Store one accumulator-layout pair (r, c), (r, c+1) of an n x n result.
+template <typename TOut>
+__device__ __forceinline__ void gstore(TOut* __restrict__ dst, int n, int r, int c,
+                                       double v0, double v1) {
+#ifdef CSM_NO_STORE
+  if (v0 != 12345.678) return;  // experiment: measure without output traffic
+#endif
+  if (n == NP) {
+    if constexpr (sizeof(TOut) == 8)
+      *reinterpret_cast<double2*>(reinterpret_cast<double*>(dst) + r * NP + c) =
+          make_double2(v0, v1);
+    else
+      *reinterpret_cast<float2*>(reinterpret_cast<float*>(dst) + r * NP + c) =
+          make_float2(static_cast<float>(v0), static_cast<float>(v1));
+  } else if (r < n) {
+    if (c < n) dst[r * n + c] = static_cast<TOut>(v0);
+    if (c + 1 < n) dst[r * n + c + 1] = static_cast<TOut>(v1);
   }
 }
 
-// Degree-12 core (schemes.py:329-361) on even variable in slot Y.
-// Taylor k=7 (sin = A sc) and wave k=5 (s = tp sc).
-template <bool WAVE>
-__device__ void deg12(double* A, double* Y, double* const* W, double tp,
-                      const Lane& ln, double** pc, double** ps) {
+template <typename TOut>
+__device__ __forceinline__ void put(const EpiArgs<TOut>& E, int q, int r, int c, int off,
+                                    double v0, double v1) {
+  st2(E.o[q], off, v0, v1);
+  if (E.g[q]) gstore(E.g[q], E.n, r, c, v0, v1);
+}
+
+// Run BODY on each of the thread's 8 owned pairs (accumulator layout) with
+// r, c, off (swizzled), I0/I1 (identity entries) and p0/p1 (accumulator).
+#define FOR_PAIRS(...)                                                        \
+  _Pragma("unroll") for (int mi = 0; mi < 2; ++mi) {                          \
+    _Pragma("unroll") for (int ni = 0; ni < 4; ++ni) {                        \
+      const int r = ln.rb + mi * 8 + ln.g;                                    \
+      const int c = ln.cb + ni * 8 + 2 * ln.t;                                \
+      const int off = swz(r, c);                                              \
+      const double I0 = (r == c) ? 1.0 : 0.0, I1 = (r == c + 1) ? 1.0 : 0.0;  \
+      const double p0 = acc[mi][ni][0], p1 = acc[mi][ni][1];                  \
+      (void)I0; (void)I1; (void)off;                                          \
+      __VA_ARGS__                                                             \
+    }                                                                         \
+  }
+
+template <typename TOut>
+__device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const Acc& acc,
+                                         const Acc& acc2, Acc& keep, const Lane& ln) {
+  const double* x = dTables.x8;  // x[0] = x1
+  const double* z8 = dTables.z8;
   const double(*a)[4] = dTables.a12;  // a[j-1][i]
   const double* z = dTables.z12;
-  Acc acc;
-  double *sY2 = W[0], *sY3 = W[1], *sC4 = W[2], *sMid = W[3];
-  gemm1(Y, Y, acc, ln);  // y2
-  store_acc(sY2, acc, ln);
-  __syncthreads();
-  gemm1(sY2, Y, acc, ln);  // y3
-  owned(ln, [&](int mi, int ni, int off, double i0, double i1) {
-    double2 y = ld2(Y, off), y2 = ld2(sY2, off);
-    const double* p = acc[mi][ni];
-    st2(sY3, off, p[0], p[1]);
-    st2(sC4, off, fma(a[3][3], p[0], fma(a[3][2], y2.x, fma(a[3][1], y.x, a[3][0] * i0))),
-        fma(a[3][3], p[1], fma(a[3][2], y2.y, fma(a[3][1], y.y, a[3][0] * i1))));
-  });
-  __syncthreads();
-  gemm1(sC4, sC4, acc, ln);  // c4^2
-  __syncthreads();            // L overwrites c4
-  double* sL = sC4;
-  owned(ln, [&](int mi, int ni, int off, double i0, double i1) {
-    double2 y = ld2(Y, off), y2 = ld2(sY2, off), y3 = ld2(sY3, off);
-    const double* p = acc[mi][ni];
-    double m0 = fma(a[2][3], y3.x, fma(a[2][2], y2.x, fma(a[2][1], y.x, a[2][0] * i0))) + p[0];
-    double m1 = fma(a[2][3], y3.y, fma(a[2][2], y2.y, fma(a[2][1], y.y, a[2][0] * i1))) + p[1];
-    double l0 = fma(a[1][3], y3.x, fma(a[1][2], y2.x, fma(a[1][1], y.x, a[1][0] * i0))) + m0;
-    double l1 = fma(a[1][3], y3.y, fma(a[1][2], y2.y, fma(a[1][1], y.y, a[1][0] * i1))) + m1;
-    st2(sMid, off, m0, m1);
-    st2(sL, off, l0, l1);
-  });
-  __syncthreads();
-  gemm1(sL, sMid, acc, ln);  // (c2 + mid) mid
-  __syncthreads();            // cos overwrites L, inner overwrites mid
-  double sb[2][4][2];
-  double *sCos = sL, *sInner = sMid;
-  owned(ln, [&](int mi, int ni, int off, double i0, double i1) {
-    double2 y = ld2(Y, off), y2 = ld2(sY2, off), y3 = ld2(sY3, off),
-            md = ld2(sMid, off);
-    const double* p = acc[mi][ni];
-    double c0 = fma(a[0][3], y3.x, fma(a[0][2], y2.x, fma(a[0][1], y.x, a[0][0] * i0))) + p[0];
-    double c1 = fma(a[0][3], y3.y, fma(a[0][2], y2.y, fma(a[0][1], y.y, a[0][0] * i1))) + p[1];
-    double n0 = fma(z[11], c0, fma(z[10], md.x, fma(z[9], y3.x, fma(z[8], y2.x, fma(z[7], y.x, z[6] * i0)))));
-    double n1 = fma(z[11], c1, fma(z[10], md.y, fma(z[9], y3.y, fma(z[8], y2.y, fma(z[7], y.y, z[6] * i1)))));
-    sb[mi][ni][0] = fma(z[5], c0, fma(z[4], md.x, fma(z[3], y3.x, fma(z[2], y2.x, fma(z[1], y.x, z[0] * i0)))));
-    sb[mi][ni][1] = fma(z[5], c1, fma(z[4], md.y, fma(z[3], y3.y, fma(z[2], y2.y, fma(z[1], y.y, z[0] * i1)))));
-    st2(sCos, off, c0, c1);
-    st2(sInner, off, n0, n1);
-  });
-  __syncthreads();
-  gemm1(sInner, sCos, acc, ln);  // tail
-  double* sSc = sY2;             // y2 dead
-  owned(ln, [&](int mi, int ni, int off, double, double) {
-    double v0 = sb[mi][ni][0] + acc[mi][ni][0];
-    double v1 = sb[mi][ni][1] + acc[mi][ni][1];
-    if (WAVE) { v0 *= tp; v1 *= tp; }
-    st2(sSc, off, v0, v1);
-  });
-  __syncthreads();
-  *pc = sCos;
-  if (WAVE) {
-    *ps = sSc;
-  } else {
-    gemm1(A, sSc, acc, ln);
-    store_acc(sY3, acc, ln);  // sin (y3 dead)
-    __syncthreads();
-    *ps = sY3;
+  switch (epi) {
+    case E_SCALED:
+      FOR_PAIRS(put(E, 0, r, c, off, E.scale * p0, E.scale * p1);)
+      break;
+    case E_DEG2:
+      FOR_PAIRS({
+          const double2 y = ld2(E.in[0], off);
+          put(E, 0, r, c, off, fma(1.0 / 24.0, p0, fma(-0.5, y.x, I0)),
+              fma(1.0 / 24.0, p1, fma(-0.5, y.y, I1)));
+          put(E, 1, r, c, off, fma(1.0 / 120.0, p0, fma(-1.0 / 6.0, y.x, I0)),
+              fma(1.0 / 120.0, p1, fma(-1.0 / 6.0, y.y, I1)));
+        })
+      break;
+    case E_DEG4A:
+      FOR_PAIRS({
+          const double2 y = ld2(E.in[0], off);
+          put(E, 0, r, c, off, p0, p1);
+          put(E, 1, r, c, off, fma(1.0 / 40320.0, p0, (-1.0 / 720.0) * y.x),
+              fma(1.0 / 40320.0, p1, (-1.0 / 720.0) * y.y));
+        })
+      break;
+    case E_DEG4B:
+      FOR_PAIRS({
+          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
+          put(E, 0, r, c, off, p0 + fma(1.0 / 24.0, y2.x, fma(-0.5, y.x, I0)),
+              p1 + fma(1.0 / 24.0, y2.y, fma(-0.5, y.y, I1)));
+          put(E, 1, r, c, off,
+              fma(720.0 / 5040.0, p0, fma(1.0 / 120.0, y2.x, fma(-1.0 / 6.0, y.x, I0))),
+              fma(720.0 / 5040.0, p1, fma(1.0 / 120.0, y2.y, fma(-1.0 / 6.0, y.y, I1))));
+        })
+      break;
+    case E_DEG4W1:
+      FOR_PAIRS({
+          const double2 y = ld2(E.in[0], off);
+          put(E, 0, r, c, off, p0, p1);
+          put(E, 1, r, c, off, fma(1.0 / 40320.0, p0, (-1.0 / 720.0) * y.x),
+              fma(1.0 / 40320.0, p1, (-1.0 / 720.0) * y.y));
+          put(E, 2, r, c, off, fma(1.0 / 362880.0, p0, (-1.0 / 5040.0) * y.x),
+              fma(1.0 / 362880.0, p1, (-1.0 / 5040.0) * y.y));
+        })
+      break;
+    case E_DEG4W2:
+      FOR_PAIRS({
+          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
+          const double q0 = acc2[mi][ni][0], q1 = acc2[mi][ni][1];
+          put(E, 0, r, c, off, p0 + fma(1.0 / 24.0, y2.x, fma(-0.5, y.x, I0)),
+              p1 + fma(1.0 / 24.0, y2.y, fma(-0.5, y.y, I1)));
+          put(E, 1, r, c, off,
+              E.scale * (q0 + fma(1.0 / 120.0, y2.x, fma(-1.0 / 6.0, y.x, I0))),
+              E.scale * (q1 + fma(1.0 / 120.0, y2.y, fma(-1.0 / 6.0, y.y, I1))));
+        })
+      break;
+    case E_DEG8A:
+      FOR_PAIRS({
+          const double2 y = ld2(E.in[0], off);
+          put(E, 0, r, c, off, p0, p1);
+          put(E, 1, r, c, off, fma(x[1], p0, x[0] * y.x), fma(x[1], p1, x[0] * y.y));
+        })
+      break;
+    case E_DEG8B:
+      FOR_PAIRS({
+          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
+          put(E, 0, r, c, off, p0, p1);
+          put(E, 1, r, c, off, fma(x[2], y2.x, p0), fma(x[2], y2.y, p1));
+          put(E, 2, r, c, off, fma(x[6], p0, fma(x[5], y2.x, fma(x[4], y.x, x[3] * I0))),
+              fma(x[6], p1, fma(x[5], y2.y, fma(x[4], y.y, x[3] * I1))));
+        })
+      break;
+    case E_DEG8C:
+      FOR_PAIRS({
+          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off),
+                        p8 = ld2(E.in[2], off);
+          const double c0 = p0 + fma(x[7], y2.x, fma(-0.5, y.x, I0));
+          const double c1 = p1 + fma(x[7], y2.y, fma(-0.5, y.y, I1));
+          // inner = z5 I + z5 y + z6 y2 + z7 p8 + z8 cos
+          const double n0 = fma(z8[8], c0, fma(z8[7], p8.x, fma(z8[6], y2.x, fma(z8[5], y.x, z8[5] * I0))));
+          const double n1 = fma(z8[8], c1, fma(z8[7], p8.y, fma(z8[6], y2.y, fma(z8[5], y.y, z8[5] * I1))));
+          // sin base = z0 I + z1 y + z2 y2 + z3 p8 + z4 cos
+          keep[mi][ni][0] = fma(z8[4], c0, fma(z8[3], p8.x, fma(z8[2], y2.x, fma(z8[1], y.x, z8[0] * I0))));
+          keep[mi][ni][1] = fma(z8[4], c1, fma(z8[3], p8.y, fma(z8[2], y2.y, fma(z8[1], y.y, z8[0] * I1))));
+          put(E, 0, r, c, off, c0, c1);
+          put(E, 1, r, c, off, n0, n1);  // may overwrite y at this thread's own pair
+        })
+      break;
+    case E_KEEP:
+      FOR_PAIRS(put(E, 0, r, c, off, E.scale * (keep[mi][ni][0] + p0), E.scale * (keep[mi][ni][1] + p1));)
+      break;
+    case E_DEG12B:
+      FOR_PAIRS({
+          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
+          put(E, 0, r, c, off, p0, p1);
+          put(E, 1, r, c, off, fma(a[3][3], p0, fma(a[3][2], y2.x, fma(a[3][1], y.x, a[3][0] * I0))),
+              fma(a[3][3], p1, fma(a[3][2], y2.y, fma(a[3][1], y.y, a[3][0] * I1))));
+        })
+      break;
+    case E_DEG12C:
+      FOR_PAIRS({
+          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off),
+                        y3 = ld2(E.in[2], off);
+          const double m0 = fma(a[2][3], y3.x, fma(a[2][2], y2.x, fma(a[2][1], y.x, a[2][0] * I0))) + p0;
+          const double m1 = fma(a[2][3], y3.y, fma(a[2][2], y2.y, fma(a[2][1], y.y, a[2][0] * I1))) + p1;
+          const double l0 = fma(a[1][3], y3.x, fma(a[1][2], y2.x, fma(a[1][1], y.x, a[1][0] * I0))) + m0;
+          const double l1 = fma(a[1][3], y3.y, fma(a[1][2], y2.y, fma(a[1][1], y.y, a[1][0] * I1))) + m1;
+          put(E, 0, r, c, off, m0, m1);
+          put(E, 1, r, c, off, l0, l1);
+        })
+      break;
+    case E_DEG12D:
+      FOR_PAIRS({
+          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off),
+                        y3 = ld2(E.in[2], off), md = ld2(E.in[3], off);
+          const double c0 = fma(a[0][3], y3.x, fma(a[0][2], y2.x, fma(a[0][1], y.x, a[0][0] * I0))) + p0;
+          const double c1 = fma(a[0][3], y3.y, fma(a[0][2], y2.y, fma(a[0][1], y.y, a[0][0] * I1))) + p1;
+          const double n0 = fma(z[11], c0, fma(z[10], md.x, fma(z[9], y3.x, fma(z[8], y2.x, fma(z[7], y.x, z[6] * I0)))));
+          const double n1 = fma(z[11], c1, fma(z[10], md.y, fma(z[9], y3.y, fma(z[8], y2.y, fma(z[7], y.y, z[6] * I1)))));
+          keep[mi][ni][0] = fma(z[5], c0, fma(z[4], md.x, fma(z[3], y3.x, fma(z[2], y2.x, fma(z[1], y.x, z[0] * I0)))));
+          keep[mi][ni][1] = fma(z[5], c1, fma(z[4], md.y, fma(z[3], y3.y, fma(z[2], y2.y, fma(z[1], y.y, z[0] * I1)))));
+          put(E, 0, r, c, off, c0, c1);
+          put(E, 1, r, c, off, n0, n1);  // may overwrite y at this thread's own pair
+        })
+      break;
+    default:
+      break;
   }
 }
 
-// Wave k=3 -- chain_deg4(exact_sine=True) on y (schemes.py:275-299, :426-427).
-// q and q9 share their y2 factor: one dual product L*y2, L9*y2.
-__device__ void wave3(double* Y, double* const* W, double tp, const Lane& ln,
-                      double** pc, double** ps) {
-  Acc acc, acc2;
-  gemm1(Y, Y, acc, ln);  // y2
-  owned(ln, [&](int mi, int ni, int off, double, double) {
-    double2 y = ld2(Y, off);
-    const double* p = acc[mi][ni];
-    st2(W[0], off, p[0], p[1]);
-    st2(W[1], off, fma(1.0 / 40320.0, p[0], (-1.0 / 720.0) * y.x),
-        fma(1.0 / 40320.0, p[1], (-1.0 / 720.0) * y.y));
-    st2(W[2], off, fma(1.0 / 362880.0, p[0], (-1.0 / 5040.0) * y.x),
-        fma(1.0 / 362880.0, p[1], (-1.0 / 5040.0) * y.y));
-  });
-  __syncthreads();
-  gemm2(W[1], W[2], W[0], acc, acc2, ln);  // q, q9
-  owned(ln, [&](int mi, int ni, int off, double i0, double i1) {
-    double2 y = ld2(Y, off), y2 = ld2(W[0], off);
-    const double* q = acc[mi][ni];
-    const double* q9 = acc2[mi][ni];
-    double c0 = q[0] + fma(1.0 / 24.0, y2.x, fma(-0.5, y.x, i0));
-    double c1 = q[1] + fma(1.0 / 24.0, y2.y, fma(-0.5, y.y, i1));
-    double s0 = tp * (q9[0] + fma(1.0 / 120.0, y2.x, fma(-1.0 / 6.0, y.x, i0)));
-    double s1 = tp * (q9[1] + fma(1.0 / 120.0, y2.y, fma(-1.0 / 6.0, y.y, i1)));
-    st2(W[3], off, c0, c1);
-    st2(W[4], off, s0, s1);
-  });
-  __syncthreads();
-  *pc = W[3];
-  *ps = W[4];
-}
-
-// s doubling steps (driver.py:91-98): S <- 2 S C (old C), C <- 2 C C - I,
-// as one dual product [S; C] * C, written back in place after a barrier.
-__device__ void doubling(double* C, double* S, int steps, const Lane& ln) {
+// s doubling steps (driver.py:91-98): S <- 2 S C (old C), C <- 2 C C - I as
+// one dual product [S; C] * C into the two free slots, then swap; the last
+// step writes the results straight from registers to global memory.
+template <typename TOut>
+__device__ __forceinline__ void doubling(double*& C, double*& S, double*& F1,
+                                         double*& F2, int steps, const Lane& ln,
+                                         TOut* cdst, TOut* sdst, int n) {
   Acc sc, cc;
   for (int it = 0; it < steps; ++it) {
-    gemm2(S, C, C, sc, cc, ln);
-    __syncthreads();
-    owned(ln, [&](int mi, int ni, int off, double i0, double i1) {
-      st2(S, off, 2.0 * sc[mi][ni][0], 2.0 * sc[mi][ni][1]);
-      st2(C, off, fma(2.0, cc[mi][ni][0], -i0), fma(2.0, cc[mi][ni][1], -i1));
-    });
-    __syncthreads();
+    TRACE_T(6);
+    gemm<true>(S, C, C, sc, cc, ln);
+    const bool last = it == steps - 1;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int r = ln.rb + mi * 8 + ln.g;
+        const int c = ln.cb + ni * 8 + 2 * ln.t;
+        const double s0 = 2.0 * sc[mi][ni][0], s1 = 2.0 * sc[mi][ni][1];
+        const double c0 = fma(2.0, cc[mi][ni][0], (r == c) ? -1.0 : 0.0);
+        const double c1 = fma(2.0, cc[mi][ni][1], (r == c + 1) ? -1.0 : 0.0);
+        if (last) {
+          gstore(sdst, n, r, c, s0, s1);
+          gstore(cdst, n, r, c, c0, c1);
+        } else {
+          const int off = swz(r, c);
+          st2(F1, off, s0, s1);
+          st2(F2, off, c0, c1);
+        }
+      }
+    TRACE_T(7);
+    if (!last) {
+      __syncthreads();
+      double* t = S; S = F1; F1 = t;
+      t = C; C = F2; F2 = t;
+    }
   }
 }
 
@@ -390,6 +479,14 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src));
 }
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src));
+}
+__device__ __forceinline__ void cp_async8v(void* dst, const void* src) {
+  unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src));
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" ::);
 }
@@ -397,49 +494,64 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
-// Issue the load of matrix b into slot dst (async for fp64 input).
+// Load matrix (n x n, row-major) into slot dst: async for fp64 input.  For
+// n < 64 the padding is rewritten with zeros (the slot may hold a previous
+// chain's intermediate).
 template <typename TIn>
 __device__ __forceinline__ void load_matrix(double* dst, const TIn* __restrict__ src,
                                             int n) {
   const int tid = threadIdx.x;
+  if (n < NP) {
+    for (int p = tid; p < SLOT; p += THREADS) {
+      const int r = p >> 6, c = p & 63;
+      if (r >= n || c >= n) dst[swz(r, c)] = 0.0;
+    }
+  }
   if constexpr (sizeof(TIn) == 8) {
     const double* s = reinterpret_cast<const double*>(src);
-    if ((n & 1) == 0) {
+    if (n == NP) {
+#pragma unroll
+      for (int i = 0; i < (NP * NP / 2) / THREADS; ++i) {
+        const int p = tid + i * THREADS;
+        const int r = p >> 5, c = (p & 31) * 2;
+        cp_async16(dst + swz(r, c), s + r * NP + c);
+      }
+    } else if ((n & 1) == 0) {
       const int half = n >> 1;
       for (int p = tid; p < n * half; p += THREADS) {
-        int r = p / half, c = (p - r * half) * 2;
+        const int r = p / half, c = (p - r * half) * 2;
         cp_async16(dst + swz(r, c), s + static_cast<size_t>(r) * n + c);
       }
     } else {
       for (int p = tid; p < n * n; p += THREADS) {
-        int r = p / n, c = p - r * n;
+        const int r = p / n, c = p - r * n;
         cp_async8(dst + swz(r, c), s + p);
       }
     }
     cp_async_commit();
   } else {
     for (int p = tid; p < n * n; p += THREADS) {
-      int r = p / n, c = p - r * n;
+      const int r = p / n, c = p - r * n;
       dst[swz(r, c)] = static_cast<double>(src[p]);
     }
   }
 }
 
 template <typename TOut>
-__device__ __forceinline__ void store_matrix(TOut* __restrict__ dst,
-                                             const double* src, int n) {
+__device__ __forceinline__ void store_matrix(TOut* __restrict__ dst, const double* src,
+                                             int n) {
   const int tid = threadIdx.x;
-  if (sizeof(TOut) == 8 && (n & 1) == 0) {
-    const int half = n >> 1;
-    for (int p = tid; p < n * half; p += THREADS) {
-      int r = p / half, c = (p - r * half) * 2;
-      double2 v = *reinterpret_cast<const double2*>(src + swz(r, c));
-      *reinterpret_cast<double2*>(reinterpret_cast<double*>(dst) +
-                                  static_cast<size_t>(r) * n + c) = v;
+  if (sizeof(TOut) == 8 && n == NP) {
+#pragma unroll
+    for (int i = 0; i < (NP * NP / 2) / THREADS; ++i) {
+      const int p = tid + i * THREADS;
+      const int r = p >> 5, c = (p & 31) * 2;
+      *reinterpret_cast<double2*>(reinterpret_cast<double*>(dst) + r * NP + c) =
+          ld2(src, swz(r, c));
     }
   } else {
     for (int p = tid; p < n * n; p += THREADS) {
-      int r = p / n, c = p - r * n;
+      const int r = p / n, c = p - r * n;
       dst[p] = static_cast<TOut>(src[swz(r, c)]);
     }
   }
@@ -453,93 +565,196 @@ __device__ __forceinline__ void store_nan(TOut* __restrict__ dst, int n) {
 
 // ---------------------------------------------------------------------------
 
+// ---------------------------------------------------------------------------
+// Input staging: the next matrix lands, in its natural row-major layout, in
+// slot 6 through ONE TMA bulk copy (cp.async.bulk + mbarrier complete_tx)
+// issued by thread 0 -- no LSU traffic -- and is converted to the swizzled
+// layout (with the wave family's y = (t')^2 A scaling folded in) at the top
+// of its turn.  Odd n (not 16-byte aligned rows) falls back to a
+// cooperative synchronous copy.
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                            uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 template <typename TIn, typename TOut, bool WAVE>
 __global__ void __launch_bounds__(THREADS, 1)
 fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
                TOut* __restrict__ Sout, const double* __restrict__ T,
                const int32_t* __restrict__ K, const int32_t* __restrict__ Sx,
-               const int32_t* __restrict__ ST, int64_t batch, int n,
-               int* __restrict__ counter) {
-  extern __shared__ __align__(16) double smem[];
-  __shared__ long long sh_next;
-  double* slot[NSLOTS];
-#pragma unroll
-  for (int i = 0; i < NSLOTS; ++i) slot[i] = smem + i * SLOT;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+               const int32_t* __restrict__ ST, const int32_t* __restrict__ order,
+               int64_t batch, int n, int tma) {
+  extern __shared__ __align__(128) double smem[];
+  // Static schedule: CTA c takes order[] positions c, 2G-1-c, 2G+c, ... (a
+  // snake over the cost-sorted list).  Thread 0 stages the matrix ids two
+  // turns ahead and the next matrix's (k, s, status, t) by 4/8-byte
+  // cp.async into small rings, so no global latency is ever exposed.
+  __shared__ int sh_b[4];
+  __shared__ int sh_meta[2][4];
+  __shared__ double sh_t[2];
+  __shared__ __align__(8) uint64_t sh_bar;
+  __shared__ Chain sh_chain[7];
+  const int tid = threadIdx.x;
+  const int G = gridDim.x, cta = blockIdx.x;
   Lane ln;
-  ln.rb = (warp >> 1) * 16;
-  ln.cb = (warp & 1) * 32;
-  ln.g = lane >> 2;
-  ln.t = lane & 3;
+  make_lane(ln);
   const size_t nn = static_cast<size_t>(n) * n;
+  double* const land = smem + 6 * SLOT;
+  const unsigned in_bytes = static_cast<unsigned>(nn * sizeof(TIn));
+  auto posof = [&](int i) -> long long {
+    return static_cast<long long>(i) * G + ((i & 1) ? (G - 1 - cta) : cta);
+  };
+  auto prefetch = [&](int b) {  // thread 0 only: next input -> slot 6
+    if (tma && b >= 0) tma_load_1d(land, Ain + static_cast<size_t>(b) * nn, in_bytes, &sh_bar);
+  };
 
-  // Both A slots start zero so the padding outside n x n stays exact zero.
-  if (n < NP) {
-    for (int p = tid; p < SLOT; p += THREADS) slot[0][p] = slot[6][p] = 0.0;
+#ifdef CSM_TRACE
+  if (tid == 0) trace_count() = 0;
+#endif
+  for (int i = tid; i < static_cast<int>(sizeof(kChains) / 4); i += THREADS)
+    reinterpret_cast<int*>(sh_chain)[i] = reinterpret_cast<const int*>(kChains)[i];
+  if (tid == 0) {
+    mbar_init(&sh_bar, 1);
+    const long long p0 = posof(0), p1 = posof(1);
+    const int b0 = p0 < batch ? order[p0] : -1;
+    sh_b[0] = b0;
+    sh_b[1] = p1 < batch ? order[p1] : -1;
+    if (b0 >= 0) {
+      sh_meta[0][0] = K[b0]; sh_meta[0][1] = Sx[b0]; sh_meta[0][2] = ST[b0];
+      sh_t[0] = WAVE ? T[b0] : 0.0;
+      prefetch(b0);
+    }
   }
-  if (tid == 0) sh_next = atomicAdd(counter, 1);
-  __syncthreads();
-  long long cur = sh_next;
-  double* Acur = slot[0];
-  double* Anext = slot[6];
-  constexpr bool kAsync = sizeof(TIn) == 8;
-  if (kAsync && cur < batch) load_matrix(Acur, Ain + cur * nn, n);
   __syncthreads();
 
-  while (cur < batch) {
-    if (tid == 0) sh_next = atomicAdd(counter, 1);
-    if (!kAsync) load_matrix(Acur, Ain + cur * nn, n);
-    cp_async_wait_all();
+  Acc acc, acc2, keep;
+  for (int it = 0;; ++it) {
+    if (tid == 0) cp_async_wait_all();
     __syncthreads();
-    const long long nxt = sh_next;
-    if (kAsync && nxt < batch) load_matrix(Anext, Ain + nxt * nn, n);
-
-    TOut* cdst = Cout + cur * nn;
-    TOut* sdst = Sout + cur * nn;
-    const int st = ST[cur];
-    if (st != 0) {
+    const int b = sh_b[it & 3], bn = sh_b[(it + 1) & 3];
+    if (b < 0) break;
+    if (tma) mbar_wait(&sh_bar, it & 1);  // this matrix's input has landed
+    const int k = sh_meta[it & 1][0], s = sh_meta[it & 1][1], status = sh_meta[it & 1][2];
+    const double tcur = sh_t[it & 1];
+    TRACE_T(1);
+    CSM_TRACE_EV(9, static_cast<unsigned long long>(k * 16 + s));
+    if (tid == 0) {  // stage ids and metadata for the coming turns
+      const long long p2 = posof(it + 2);
+      if (p2 < batch) cp_async4(&sh_b[(it + 2) & 3], order + p2);
+      else sh_b[(it + 2) & 3] = -1;
+      if (bn >= 0) {
+        cp_async4(&sh_meta[(it + 1) & 1][0], K + bn);
+        cp_async4(&sh_meta[(it + 1) & 1][1], Sx + bn);
+        cp_async4(&sh_meta[(it + 1) & 1][2], ST + bn);
+        if (WAVE) cp_async8v(&sh_t[(it + 1) & 1], T + bn);
+      }
+      cp_async_commit();
+    }
+    const TIn* src = Ain + static_cast<size_t>(b) * nn;
+    if (!tma) {  // odd n: synchronous staging copy
+      for (int p = tid; p < static_cast<int>(nn); p += THREADS)
+        reinterpret_cast<TIn*>(land)[p] = src[p];
+      __syncthreads();
+    }
+    TOut* cdst = Cout + static_cast<size_t>(b) * nn;
+    TOut* sdst = Sout + static_cast<size_t>(b) * nn;
+    if (status != 0) {
       store_nan(cdst, n);
       store_nan(sdst, n);
-    } else {
-      const int k = K[cur], s = Sx[cur];
-      double tp = 0.0, f;
-      if (WAVE) {
-        tp = T[cur] / ldexp(1.0, s);  // driver.py:139, t / 2**s
-        f = tp * tp;                  // schemes.py:424, y = (t*t) a
-      } else {
-        f = ldexp(1.0, -s);  // driver.py:115, a * 2**-s
-      }
-      for (int p = tid; p < SLOT; p += THREADS) Acur[p] *= f;
       __syncthreads();
-      double* W[5] = {slot[1], slot[2], slot[3], slot[4], slot[5]};
-      double *pc, *ps;
-      if (!WAVE) {
-        if (k == 3) {
-          taylor3(Acur, W, ln, &pc, &ps);
-        } else if (k == 4) {
-          taylor4(Acur, W, ln, &pc, &ps);
-        } else {
-          Acc acc;
-          gemm1(Acur, Acur, acc, ln);  // y = A A  (schemes.py:388)
-          store_acc(W[0], acc, ln);
-          __syncthreads();
-          if (k == 6) deg8<false>(Acur, W[0], W + 1, 0.0, ln, &pc, &ps);
-          else deg12<false>(Acur, W[0], W + 1, 0.0, ln, &pc, &ps);
-        }
-      } else {
-        if (k == 3) wave3(Acur, W, tp, ln, &pc, &ps);
-        else if (k == 4) deg8<true>(nullptr, Acur, W, tp, ln, &pc, &ps);
-        else deg12<true>(nullptr, Acur, W, tp, ln, &pc, &ps);
-      }
-      doubling(pc, ps, s, ln);
-      store_matrix(cdst, pc, n);
-      store_matrix(sdst, ps, n);
+      if (tid == 0) prefetch(bn);
+      continue;
     }
-    double* tmp = Acur;
-    Acur = Anext;
-    Anext = tmp;
-    cur = nxt;
-    __syncthreads();  // sh_next consumed, slots free for the next matrix
+    double f, tp = 0.0;
+    if (WAVE) {
+      tp = tcur / ldexp(1.0, s);  // driver.py:139, t / 2**s
+      f = tp * tp;                // schemes.py:424, y = (t*t) a
+    } else {
+      f = ldexp(1.0, -s);  // driver.py:115, a * 2**-s (folded into P1/Pk)
+    }
+    {  // slot 6 (natural) -> slot 0 (swizzled, zero padded)
+      const double g = WAVE ? f : 1.0;
+      const TIn* nat = reinterpret_cast<const TIn*>(land);
+#pragma unroll 2
+      for (int p = tid; p < SLOT / 2; p += THREADS) {
+        const int r = p >> 5, c = (p & 31) * 2;
+        double v0 = 0.0, v1 = 0.0;
+        if (n == NP) {
+          v0 = static_cast<double>(nat[r * NP + c]);
+          v1 = static_cast<double>(nat[r * NP + c + 1]);
+        } else if (r < n) {
+          if (c < n) v0 = static_cast<double>(nat[r * n + c]);
+          if (c + 1 < n) v1 = static_cast<double>(nat[r * n + c + 1]);
+        }
+        st2(smem, swz(r, c), g * v0, g * v1);
+      }
+    }
+    __syncthreads();
+    auto slotp = [&](int i) -> double* { return smem + i * SLOT; };
+    const int ci = WAVE ? (k == 3 ? 4 : (k == 4 ? 5 : 6))
+                        : (k == 3 ? 0 : (k == 4 ? 1 : (k == 6 ? 2 : 3)));
+    const Chain& ch = sh_chain[ci];
+    const int nsteps = ch.nsteps, pf_after = ch.pf_after;
+    for (int i = 0; i < nsteps; ++i) {
+      const Step st = ch.step[i];
+      TRACE_T(2);
+      if (st.dual)
+        gemm<true>(slotp(st.l1), slotp(st.l2), slotp(st.r), acc, acc2, ln);
+      else
+        gemm<false>(slotp(st.l1), nullptr, slotp(st.r), acc, acc2, ln);
+      EpiArgs<TOut> E;
+      E.o[0] = slotp(st.o0);
+      E.o[1] = slotp(st.o1);
+      E.o[2] = slotp(st.o2);
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        E.g[q] = (s != 0) ? nullptr
+               : (i == ch.cos_step && q == ch.cos_out) ? cdst
+               : (i == ch.sin_step && q == ch.sin_out) ? sdst : nullptr;
+      E.in[0] = slotp(st.i0);
+      E.in[1] = slotp(st.i1);
+      E.in[2] = slotp(st.i2);
+      E.in[3] = slotp(st.i3);
+      E.scale = st.scale == SC_F ? f : st.scale == SC_F2 ? f * f
+              : st.scale == SC_TP ? tp : 1.0;
+      E.n = n;
+      epilogue(st.epi, E, acc, acc2, keep, ln);
+      TRACE_T(4);
+      __syncthreads();
+      TRACE_T(5);
+      if (i == pf_after && tid == 0) prefetch(bn);
+    }
+    double* C = slotp(ch.cos_slot);
+    double* S = slotp(ch.sin_slot);
+    double* F1 = slotp(ch.free1);
+    double* F2 = slotp(ch.free2);
+    doubling(C, S, F1, F2, s, ln, cdst, sdst, n);
   }
 }
 
@@ -552,40 +767,42 @@ size_t fused64_smem_bytes() {
 template <typename TIn, typename TOut, bool WAVE>
 static cudaError_t launch_one(const void* a, void* c, void* s, const double* t,
                               const int32_t* k, const int32_t* sx,
-                              const int32_t* st, int64_t batch, int n,
-                              int* counter, int grid, cudaStream_t stream) {
+                              const int32_t* st, const int32_t* order, int64_t batch,
+                              int n, int grid, cudaStream_t stream) {
   auto kern = f64k::fused64_kernel<TIn, TOut, WAVE>;
   const size_t smem = fused64_smem_bytes();
+  const size_t in_bytes = static_cast<size_t>(n) * n * sizeof(TIn);
+  const int tma = (in_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0) ? 1 : 0;
   cudaError_t e = cudaFuncSetAttribute(
       kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   kern<<<grid, f64k::THREADS, smem, stream>>>(
       static_cast<const TIn*>(a), static_cast<TOut*>(c), static_cast<TOut*>(s),
-      t, k, sx, st, batch, n, counter);
+      t, k, sx, st, order, batch, n, tma);
   return cudaGetLastError();
 }
 
-// Launch K1 for a batch of n <= 64 matrices whose (k, s, status) are already
-// on the device.  `counter` must be a zeroed device int.
+// Launch K1 for a batch of n <= 64 matrices whose (k, s, status) and
+// cost-sorted order[] are already on the device.
 cudaError_t launch_fused64(int dtype, bool wave, const void* a, void* c,
                            void* s, const double* t, const int32_t* k,
-                           const int32_t* sx, const int32_t* st, int64_t batch,
-                           int n, int* counter, cudaStream_t stream) {
+                           const int32_t* sx, const int32_t* st, const int32_t* order,
+                           int64_t batch, int n, cudaStream_t stream) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int grid = static_cast<int>(batch < sms ? batch : sms);
   if (grid < 1) return cudaSuccess;
   if (dtype == 0) {
-    return wave ? launch_one<double, double, true>(a, c, s, t, k, sx, st, batch, n, counter, grid, stream)
-                : launch_one<double, double, false>(a, c, s, t, k, sx, st, batch, n, counter, grid, stream);
+    return wave ? launch_one<double, double, true>(a, c, s, t, k, sx, st, order, batch, n, grid, stream)
+                : launch_one<double, double, false>(a, c, s, t, k, sx, st, order, batch, n, grid, stream);
   }
   if (dtype == 2) {
-    return wave ? launch_one<float, double, true>(a, c, s, t, k, sx, st, batch, n, counter, grid, stream)
-                : launch_one<float, double, false>(a, c, s, t, k, sx, st, batch, n, counter, grid, stream);
+    return wave ? launch_one<float, double, true>(a, c, s, t, k, sx, st, order, batch, n, grid, stream)
+                : launch_one<float, double, false>(a, c, s, t, k, sx, st, order, batch, n, grid, stream);
   }
-  return wave ? launch_one<float, float, true>(a, c, s, t, k, sx, st, batch, n, counter, grid, stream)
-              : launch_one<float, float, false>(a, c, s, t, k, sx, st, batch, n, counter, grid, stream);
+  return wave ? launch_one<float, float, true>(a, c, s, t, k, sx, st, order, batch, n, grid, stream)
+              : launch_one<float, float, false>(a, c, s, t, k, sx, st, order, batch, n, grid, stream);
 }
 
 }  // namespace csm

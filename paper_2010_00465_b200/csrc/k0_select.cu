@@ -176,4 +176,68 @@ cudaError_t launch_fill_ks(int32_t* K, int32_t* S, int32_t* status,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Cost-ordered schedule for the persistent fused kernel: order[] lists the
+// matrices by descending product count k + 2s (counting sort; failed
+// matrices last), so a snake assignment over the CTAs balances their work
+// without a shared atomic queue.
+
+constexpr int kCostBins = 2048;
+
+__global__ void cost_hist_kernel(const int32_t* __restrict__ K, const int32_t* __restrict__ S,
+                                 const int32_t* __restrict__ status, int64_t batch,
+                                 int* __restrict__ bins) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  int cost = status[b] == 0 ? K[b] + 2 * S[b] : 0;
+  cost = cost < kCostBins - 1 ? cost : kCostBins - 1;
+  atomicAdd(bins + (kCostBins - 1 - cost), 1);  // bin 0 = most expensive
+}
+
+// Exclusive scan of the bins in place (one block).
+__global__ void cost_scan_kernel(int* __restrict__ bins) {
+  __shared__ int part[1024];
+  const int t = threadIdx.x;  // 1024 threads, 2 bins each
+  const int a0 = bins[2 * t], a1 = bins[2 * t + 1];
+  part[t] = a0 + a1;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const int v = t >= off ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  const int excl = part[t] - (a0 + a1);
+  bins[2 * t] = excl;
+  bins[2 * t + 1] = excl + a0;
+}
+
+__global__ void cost_scatter_kernel(const int32_t* __restrict__ K, const int32_t* __restrict__ S,
+                                    const int32_t* __restrict__ status, int64_t batch,
+                                    int* __restrict__ bins, int32_t* __restrict__ order) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  int cost = status[b] == 0 ? K[b] + 2 * S[b] : 0;
+  cost = cost < kCostBins - 1 ? cost : kCostBins - 1;
+  const int pos = atomicAdd(bins + (kCostBins - 1 - cost), 1);
+  order[pos] = static_cast<int32_t>(b);
+}
+
+size_t schedule_ws_bytes() { return kCostBins * sizeof(int); }
+
+// bins: device scratch of schedule_ws_bytes(); order: device int32[batch].
+cudaError_t launch_schedule(const int32_t* K, const int32_t* S, const int32_t* status,
+                            int64_t batch, int* bins, int32_t* order, cudaStream_t stream,
+                            int64_t* launches) {
+  if (batch == 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(bins, 0, schedule_ws_bytes(), stream);
+  if (e != cudaSuccess) return e;
+  cost_hist_kernel<<<blocks_for(batch, 256), 256, 0, stream>>>(K, S, status, batch, bins);
+  cost_scan_kernel<<<1, 1024, 0, stream>>>(bins);
+  cost_scatter_kernel<<<blocks_for(batch, 256), 256, 0, stream>>>(K, S, status, batch, bins,
+                                                                  order);
+  *launches += 3;
+  return cudaGetLastError();
+}
+
 }  // namespace csm

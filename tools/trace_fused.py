@@ -1,0 +1,41 @@
+"""Phase trace of fused64 (CTA 0): build a -DCSM_TRACE copy of the library,
+run cfg2, print per-phase cycle statistics."""
+import ctypes, os, subprocess, sys
+from collections import defaultdict
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+so = os.path.join(ROOT, "tools", "libcossin_trace.so")
+if os.environ.get("TRACE_SO"):
+    so = os.path.join(ROOT, "tools", os.environ["TRACE_SO"])
+if "--build" in sys.argv:
+    extra = [a for a in sys.argv[1:] if a.startswith("-D")]
+    subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+                           "-Xcompiler", "-fPIC", "-shared", "-DCSM_TRACE", *extra, "-o", so,
+                           os.path.join(ROOT, "paper_2010_00465_b200/csrc/cossin_b200.cu")])
+    sys.exit(0)
+os.environ["CSM_LIB_PATH"] = so  # load the traced copy
+import numpy as np, torch
+from paper_2010_00465_b200 import _lib
+import paper_2010_00465_b200 as csm
+from tests._util import cfg2_like
+L = _lib.lib(); L.csm_trace_dump.restype = ctypes.c_int
+a = torch.from_numpy(cfg2_like(np.random.default_rng(0), 16384)).cuda()
+csm.cos_sin_batched(a); torch.cuda.synchronize()
+buf = (ctypes.c_ulonglong * 65536)(); L.csm_trace_dump(buf, 65536)
+csm.cos_sin_batched(a); torch.cuda.synchronize()
+n = L.csm_trace_dump(buf, 65536)
+ev = [(int(buf[i]) & 255, int(buf[i]) >> 8) for i in range(n)]
+# phases
+stats = defaultdict(list); last = None; mats = 0; ks = defaultdict(int)
+for tag, v in ev:
+    if tag == 9:
+        ks[(v >> 4, v & 15)] += 1; mats += 1; continue
+    if last is not None:
+        stats[(last[0], tag)].append(v - last[1])
+    last = (tag, v)
+t0 = ev[0][1]; t1 = ev[-1][1]
+print(f"events={n} matrices={mats} cycles={t1-t0} per-matrix={(t1-t0)/max(mats,1):.0f}")
+for key in sorted(stats, key=lambda k: -sum(stats[k])):
+    v = stats[key]
+    print(f"{key[0]}->{key[1]}: n={len(v):5d} mean={np.mean(v):8.1f} total={sum(v)/(t1-t0)*100:5.1f}%")
+print(sorted(ks.items()))
