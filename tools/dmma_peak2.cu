@@ -40,6 +40,11 @@ void run(const char* name, int warps) {
   cudaFree(d);
 }
 int main() {
+  run<4, 1>("distinct a,b", 16);
+  run<4, 1>("distinct a,b", 12);
+  run<8, 1>("distinct a,b", 12);
+  run<4, 1>("distinct a,b", 8);
+  run<2, 1>("distinct a,b", 16);
   run<8, 0>("shared a,b", 8);
   run<8, 1>("distinct a,b", 8);
   run<16, 1>("distinct a,b", 8);

@@ -39,3 +39,15 @@ for key in sorted(stats, key=lambda k: -sum(stats[k])):
     v = stats[key]
     print(f"{key[0]}->{key[1]}: n={len(v):5d} mean={np.mean(v):8.1f} total={sum(v)/(t1-t0)*100:5.1f}%")
 print(sorted(ks.items()))
+# per-epilogue-type breakdown: step index within chain -> (k, step)
+cur_k = None; step = 0; per = defaultdict(list); t2 = t3 = None
+for tag, v in ev:
+    if tag == 9:
+        cur_k = (v >> 4, v & 15); step = 0; continue
+    if tag == 2: t2 = v
+    if tag == 3: t3 = v
+    if tag == 4 and t2 is not None and t3 is not None:
+        per[(cur_k[0], step)].append((t3 - t2, v - t3)); step += 1
+for key in sorted(per):
+    a = np.array(per[key])
+    print(f"k={key[0]} step={key[1]}: n={len(a):4d} issue={a[:,0].mean():7.0f} drain+epi={a[:,1].mean():7.0f}")
