@@ -28,10 +28,11 @@ namespace csm {
 
 namespace tk {
 
-constexpr int BM = 64, BN = 64, BK = 32, STAGES = 3, THREADS = 128;
-constexpr int LDA = BK + 4, LDB = BN + 4;
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, THREADS = 128;
+constexpr int LDA = BK + 4, LDB = BN + 4, LDE = BN + 8;
 constexpr int A_STAGE = BM * LDA, B_STAGE = BK * LDB;
 constexpr size_t SMEM = static_cast<size_t>(STAGES) * (A_STAGE + B_STAGE) * sizeof(double);
+static_assert(BM * LDE <= STAGES * (A_STAGE + B_STAGE), "epilogue tile fits the pipeline buffers");
 constexpr int NSLOT = 9;
 constexpr int MAXT = 8;
 
@@ -62,23 +63,31 @@ __device__ __forceinline__ void wait_group() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-__global__ void __launch_bounds__(THREADS, 2)
+// One 64x64 output tile of one matrix: acc = L R over the full n-deep
+// contraction (3-stage cp.async pipeline, 4 warps of 32x32 = 4x4 DMMA
+// tiles), then the scheme's linear combinations: the accumulator tile is
+// staged in shared memory and every output element is formed by a compact
+// term loop with row-contiguous (coalesced) global reads and writes.
+__global__ void __launch_bounds__(THREADS, 4)
 gemm_epi_kernel(double* __restrict__ ws, int NP, size_t mat_stride,
                 const int32_t* __restrict__ idx, const Op* __restrict__ ops,
                 const double* __restrict__ tsc) {
   extern __shared__ __align__(16) double sm[];
+  __shared__ Op op;
   double* As = sm;
   double* Bs = sm + STAGES * A_STAGE;
-  const Op& op = ops[blockIdx.z];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < static_cast<int>(sizeof(Op) / 4); i += THREADS)
+    reinterpret_cast<int*>(&op)[i] = reinterpret_cast<const int*>(ops + blockIdx.z)[i];
   const int b = idx[blockIdx.y];
   const int tiles_n = NP / BN;
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x - tm * tiles_n;
   double* base = ws + static_cast<size_t>(b) * mat_stride;
   const size_t slotsz = static_cast<size_t>(NP) * NP;
+  __syncthreads();
   const double* L = base + op.lhs * slotsz + static_cast<size_t>(tm) * BM * NP;
   const double* R = base + op.rhs * slotsz + static_cast<size_t>(tn) * BN;
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
 
@@ -87,14 +96,14 @@ gemm_epi_kernel(double* __restrict__ ws, int NP, size_t mat_stride,
     double* bs = Bs + stage * B_STAGE;
 #pragma unroll
     for (int i = 0; i < (BM * BK / 2) / THREADS; ++i) {
-      int p = tid + i * THREADS;
-      int r = p / (BK / 2), c = (p - r * (BK / 2)) * 2;
+      const int p = tid + i * THREADS;
+      const int r = p / (BK / 2), c = (p - r * (BK / 2)) * 2;
       cp16(as + r * LDA + c, L + static_cast<size_t>(r) * NP + k0 + c);
     }
 #pragma unroll
     for (int i = 0; i < (BK * BN / 2) / THREADS; ++i) {
-      int p = tid + i * THREADS;
-      int r = p / (BN / 2), c = (p - r * (BN / 2)) * 2;
+      const int p = tid + i * THREADS;
+      const int r = p / (BN / 2), c = (p - r * (BN / 2)) * 2;
       cp16(bs + r * LDB + c, R + static_cast<size_t>(k0 + r) * NP + c);
     }
   };
@@ -115,7 +124,7 @@ gemm_epi_kernel(double* __restrict__ ws, int NP, size_t mat_stride,
     wait_group<STAGES - 2>();
     __syncthreads();
     {
-      int nxt = kt + STAGES - 1;
+      const int nxt = kt + STAGES - 1;
       if (nxt < nk) load_stage(nxt % STAGES, nxt * BK);
       commit();
     }
@@ -135,52 +144,54 @@ gemm_epi_kernel(double* __restrict__ ws, int NP, size_t mat_stride,
     }
   }
   wait_group<0>();
+  __syncthreads();  // pipeline buffers are free: stage the accumulator tile
 
-  // Epilogue: up to three outputs, each a sequential FMA sum of terms.
-  const int nout = op.nout;
+  double* E = sm;  // [BM][LDE]
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+      *reinterpret_cast<double2*>(E + (wm + mi * 8 + g) * LDE + wn + ni * 8 + 2 * t) =
+          make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+  __syncthreads();
+
   const double ts = tsc ? tsc[b] : 1.0;
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi) {
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-      const int r = tm * BM + wm + mi * 8 + g;
-      const int c = tn * BN + wn + ni * 8 + 2 * t;
-      const size_t off = static_cast<size_t>(r) * NP + c;
-      const double i0 = (r == c) ? 1.0 : 0.0, i1 = (r == c + 1) ? 1.0 : 0.0;
-      double o[3][2];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        o[q][0] = o[q][1] = 0.0;
-        if (q < nout) {
-          const OutSpec& os = op.out[q];
-          double v0 = 0.0, v1 = 0.0;
-#pragma unroll
-          for (int tt = 0; tt < MAXT; ++tt) {
-            if (tt < os.nterms) {
-              const int src = os.t[tt].src;
-              const double cf = os.t[tt].c;
-              double x0, x1;
-              if (src >= 0) {
-                double2 v = *reinterpret_cast<const double2*>(base + src * slotsz + off);
-                x0 = v.x; x1 = v.y;
-              } else if (src == SRC_ACC) {
-                x0 = acc[mi][ni][0]; x1 = acc[mi][ni][1];
-              } else if (src == SRC_I) {
-                x0 = i0; x1 = i1;
-              } else {
-                const int j = SRC_OUT0 - src;  // 0..q-1
-                x0 = (j == 0) ? o[0][0] : (j == 1) ? o[1][0] : o[2][0];
-                x1 = (j == 0) ? o[0][1] : (j == 1) ? o[1][1] : o[2][1];
-              }
-              v0 = fma(cf, x0, v0);
-              v1 = fma(cf, x1, v1);
-            }
-          }
-          if (os.tscale) { v0 *= ts; v1 *= ts; }
-          o[q][0] = v0; o[q][1] = v1;
-          *reinterpret_cast<double2*>(base + os.slot * slotsz + off) = make_double2(v0, v1);
+  const int nout = op.nout;
+  const int r0 = tm * BM, c0 = tn * BN;
+#pragma unroll 2
+  for (int p = tid; p < BM * BN / 2; p += THREADS) {
+    const int rr = p >> 5, cc = (p & 31) * 2;  // 32 pairs per tile row
+    const int r = r0 + rr, c = c0 + cc;
+    const size_t off = static_cast<size_t>(r) * NP + c;
+    const double2 av = *reinterpret_cast<const double2*>(E + rr * LDE + cc);
+    const double i0 = (r == c) ? 1.0 : 0.0, i1 = (r == c + 1) ? 1.0 : 0.0;
+    double o0[2] = {0.0, 0.0}, o1[2] = {0.0, 0.0};  // outputs 0 and 1 of this pair
+    for (int q = 0; q < nout; ++q) {
+      const OutSpec& os = op.out[q];
+      double v0 = 0.0, v1 = 0.0;
+      for (int tt = 0; tt < os.nterms; ++tt) {
+        const int src = os.t[tt].src;
+        const double cf = os.t[tt].c;
+        double x0, x1;
+        if (src >= 0) {
+          const double2 v = *reinterpret_cast<const double2*>(base + src * slotsz + off);
+          x0 = v.x; x1 = v.y;
+        } else if (src == SRC_ACC) {
+          x0 = av.x; x1 = av.y;
+        } else if (src == SRC_I) {
+          x0 = i0; x1 = i1;
+        } else if (src == SRC_OUT0) {
+          x0 = o0[0]; x1 = o0[1];
+        } else {
+          x0 = o1[0]; x1 = o1[1];
         }
+        v0 = fma(cf, x0, v0);
+        v1 = fma(cf, x1, v1);
       }
+      if (os.tscale) { v0 *= ts; v1 *= ts; }
+      if (q == 0) { o0[0] = v0; o0[1] = v1; }
+      if (q == 1) { o1[0] = v0; o1[1] = v1; }
+      *reinterpret_cast<double2*>(base + os.slot * slotsz + off) = make_double2(v0, v1);
     }
   }
 }
