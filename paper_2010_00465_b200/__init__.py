@@ -20,6 +20,8 @@ from .api import (
     wave_cos_sin_batched,
     wave_kernels,
 )
+from . import plan
+from .plan import BatchPlan
 from .records import (
     TAYLOR_TABLE,
     UNIT_ROUNDOFF,
@@ -41,6 +43,7 @@ from .records import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "BatchPlan",
     "BatchReport",
     "ComputationReport",
     "CosSinResult",
