@@ -81,30 +81,69 @@ def make_inputs(kind: str, batch: int, n: int, seed: int):
 # Clock sampling during the timed region.
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """Samples SM clock, power and throttle reasons during the timed region
+    (NVML at ~2 ms; nvidia-smi as a fallback)."""
+
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+             "sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, power_w, set(reasons))
         self._stop = threading.Event()
         self._th = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = None
+            try:  # match the torch device by PCI bus id (NVML ignores CUDA_VISIBLE_DEVICES)
+                import torch
+                pr = torch.cuda.get_device_properties(index)
+                bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+                self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        pw = nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        masks = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40,
+                 "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+        reasons = {k for k, m in masks.items() if bits & m}
+        self.rows.append((float(sm), float(self._max), pw, reasons))
+
+    def _sample_smi(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,"
+             "clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                              "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5).stdout.strip()
+        if out:
+            f = [x.strip() for x in out.split(",")]
+            reasons = {n for n, v in zip(self.NAMES, f[3:7]) if v.lower() == "active"}
+            self.rows.append((float(f[0]), float(f[1]), float(f[2]), reasons))
 
     def _loop(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}",
-                     f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                    capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                if self._nvml is not None:
+                    self._sample_nvml()
+                    self._stop.wait(0.002)
+                else:
+                    self._sample_smi()
+                    self._stop.wait(0.05)
             except Exception:
-                pass
-            self._stop.wait(0.1)
+                self._stop.wait(0.05)
 
     def __enter__(self):
         self._th = threading.Thread(target=self._loop, daemon=True)
@@ -120,21 +159,14 @@ class ClockSampler:
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
                     "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
-                 "sw_power_cap"]
         reasons = set()
         for r in self.rows:
-            for name, v in zip(names, r[4:8]):
-                if v.strip().lower() == "active":
-                    reasons.add(name)
-        pw = [float(r[2]) for r in self.rows
-              if r[2].replace(".", "").isdigit()]
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
+            reasons |= r[3]
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows),
+                "sm_max_mhz": max(r[1] for r in self.rows),
                 "reasons": sorted(reasons), "samples": len(self.rows),
-                "power_w_max": max(pw) if pw else None}
+                "power_w_max": max(r[2] for r in self.rows),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
