@@ -253,19 +253,13 @@ def run_ours(args, cfg):
         if pg is not None:
             pg.barrier()
 
+    from paper_2010_00465_b200 import dist as pdist
+
     def max_over_ranks(x: float) -> float:
-        if pg is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        return float(t.item())
+        return pdist.max_over_ranks(x, device=dev)
 
     def sum_over_ranks(x: float) -> float:
-        if pg is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.SUM)
-        return float(t.item())
+        return pdist.sum_over_ranks(x, device=dev)
 
     a_np, t_np = make_inputs(kind, batch, n, seed=rank)
     tdtype = torch.float32 if dt == "f32" else torch.float64
