@@ -269,3 +269,108 @@ def test_device_norm1_bits(cuda, golden_dir):
     while f"a{i}" in g:
         assert csm.norm1(g[f"a{i}"]) == float(g[f"n{i}"]), i
         i += 1
+
+
+# ---------------------------------------------------------------------------
+# Full-size configs: every matrix against the oracle (process pool), plus
+# size-independent properties.
+
+def _oracle_batch(args):
+    import numpy as _np
+    from oracle import cossin_oracle as _orc
+    kind, a, t, prec = args
+    out = []
+    for i in range(a.shape[0]):
+        if kind == "wave":
+            c, s, k, sc = _orc.wave_cos_sin(a[i], float(t[i]), prec)
+        else:
+            c, s, k, sc = _orc.cos_sin(a[i].astype(_np.float64) if a.dtype == _np.float32 else a[i], prec)
+        out.append((c, s, k, sc))
+    return out
+
+
+def _oracle_all(kind, a, t, prec, chunks=16):
+    import multiprocessing as mp
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    parts = np.array_split(np.arange(a.shape[0]), chunks)
+    jobs = [(kind, a[p], None if t is None else t[p], prec) for p in parts]
+    with mp.get_context("spawn").Pool(min(chunks, os.cpu_count() or 1)) as pool:
+        res = pool.map(_oracle_batch, jobs)
+    return [r for part in res for r in part]
+
+
+def _check_all(rep, ref, tol):
+    worst = 0.0
+    for i, (c, s, k, sc) in enumerate(ref):
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc), i
+        ok_c, rc = pair_close(rep.cos_part[i], c, s, tol)
+        ok_s, rs = pair_close(rep.sin_part[i], s, c, tol)
+        assert ok_c and ok_s, (i, rc, rs)
+        worst = max(worst, min(rc, 1.0), min(rs, 1.0))
+    return worst
+
+
+@pytest.mark.timeout(900)
+def test_full_cfg2_against_oracle(cuda):
+    """configs[1] at full size: all 16384 matrices, (k, s) exact, <= 1e-12."""
+    from oracle.cpu_pool import _gen
+    a, _ = _gen("cfg2", 0, 16384, 64)
+    rep = csm.cos_sin_batched(a)
+    _check_all(rep, _oracle_all("trig", a, None, "double"), TOL64)
+
+
+@pytest.mark.timeout(900)
+def test_full_cfg3_against_oracle(cuda):
+    """configs[2] at full size (4096 x 256^2 float32): (k, s) exact vs the
+    reference on the same float32 input, outputs within 1e-5."""
+    from oracle.cpu_pool import _gen
+    a, _ = _gen("cfg3", 0, 4096, 256)
+    rep = csm.cos_sin_batched(a, csm.Precision.SINGLE)
+    ref = _oracle_all("trig", a, None, "single")  # upcast oracle
+    for i, (c, s, k, sc) in enumerate(ref):
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc), i
+        assert rel1(rep.cos_part[i], c) <= TOL32, i
+        assert rel1(rep.sin_part[i], s) <= TOL32, i
+
+
+def test_negation_symmetry_bitwise(cuda):
+    """cos(-A) == cos(A) and sin(-A) == -sin(A) bit for bit (sign flips are
+    exact through every product), on the full cfg2 distribution."""
+    from oracle.cpu_pool import _gen
+    a, _ = _gen("cfg2", 3, 4096, 64)
+    p = csm.cos_sin_batched(a)
+    m = csm.cos_sin_batched(-a)
+    assert np.array_equal(p.k, m.k) and np.array_equal(p.s, m.s)
+    assert np.array_equal(p.cos_part, m.cos_part)
+    assert np.array_equal(p.sin_part, -m.sin_part)
+
+
+def test_batch_position_invariance(cuda):
+    """A matrix's result does not depend on its batch neighbours or position
+    (the schedule reorders by cost): subsets reproduce the full batch bits."""
+    from oracle.cpu_pool import _gen
+    a, _ = _gen("cfg2", 4, 3000, 64)
+    full = csm.cos_sin_batched(a)
+    idx = np.random.default_rng(1).permutation(3000)[:700]
+    sub = csm.cos_sin_batched(a[idx])
+    assert np.array_equal(sub.cos_part, full.cos_part[idx])
+    assert np.array_equal(sub.sin_part, full.sin_part[idx])
+    # tiled path too
+    b = cfg2_like(np.random.default_rng(5), 24, n=160)
+    fb = csm.cos_sin_batched(b)
+    sb = csm.cos_sin_batched(b[5:17])
+    assert np.array_equal(sb.cos_part, fb.cos_part[5:17])
+
+
+def test_pythagorean_full_cfg2(cuda):
+    """||C^2 + S^2 - I||_1 on the whole cfg2 batch, computed on the GPU in
+    float64; bounded by the float64 floor that grows with ||cos||."""
+    import torch
+    from oracle.cpu_pool import _gen
+    a, _ = _gen("cfg2", 0, 16384, 64)
+    rep = csm.cos_sin_batched(torch.from_numpy(a).to(cuda))
+    c, s = rep.cos_part, rep.sin_part
+    r = c @ c + s @ s - torch.eye(64, dtype=torch.float64, device=cuda)
+    res = r.abs().sum(dim=1).amax(dim=1)
+    cn = c.abs().sum(dim=1).amax(dim=1)
+    assert bool(torch.all(res <= 1e-13 * torch.clamp(cn * cn, min=1.0)))
