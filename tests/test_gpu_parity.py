@@ -374,3 +374,40 @@ def test_pythagorean_full_cfg2(cuda):
     res = r.abs().sum(dim=1).amax(dim=1)
     cn = c.abs().sum(dim=1).amax(dim=1)
     assert bool(torch.all(res <= 1e-13 * torch.clamp(cn * cn, min=1.0)))
+
+
+def _oracle_permuted(a):
+    """The oracle with every product evaluated in a different summation
+    order (K split in two halves): an estimate of the reference's own
+    rounding noise."""
+    from oracle import cossin_oracle as _o
+    import numpy as _np
+
+    class _T(_np.ndarray):
+        def __matmul__(self, other):
+            x, y = _np.asarray(self), _np.asarray(other)
+            h = x.shape[1] // 2 + 1
+            return (x[:, :h] @ y[:h] + x[:, h:] @ y[h:]).view(_T)
+
+    k, s = _o.select(_o.norm1(a))
+    c, sn = _o.taylor_core((a * 2.0 ** -s).view(_T), k)
+    c, sn = _o.double_angle(_np.asarray(c).view(_T), _np.asarray(sn).view(_T), s)
+    return _np.asarray(c), _np.asarray(sn)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("n", [1024])
+def test_large_symmetric_against_oracle_noise_floor(cuda, n):
+    """configs[4] analogue at n=1024 (20 (G+G^T)/(2 sqrt n), s=8): the 1e-12
+    gate sits below the reference's own rounding noise here,
+    so the gate is max(1e-12, 4 x the oracle-vs-permuted-oracle noise)."""
+    g = np.random.default_rng(0).standard_normal((n, n))
+    a = 20.0 * (g + g.T) / (2.0 * np.sqrt(n))
+    c, s, k, sc = orc.cos_sin(a)
+    cp, sp = _oracle_permuted(a)
+    noise = max(rel1(cp, c), rel1(sp, s))
+    rep = csm.cos_sin(a)
+    assert (rep.scheme_used.k_products, rep.scaling_exponent) == (k, sc)
+    gate = max(TOL64, 4.0 * noise)
+    assert rel1(rep.result.cos_part, c) <= gate, (rel1(rep.result.cos_part, c), noise)
+    assert rel1(rep.result.sin_part, s) <= gate, (rel1(rep.result.sin_part, s), noise)
