@@ -15,9 +15,11 @@
 //
 // GEMM: CTA tile 64x64, 4 warps of 32x32 (4x4 DMMA m8n8k4 tiles), K step 16
 // through a 3-stage cp.async pipeline, 4 CTAs per SM; padded smem rows
-// (20 / 68 doubles) make both fragment loads bank-conflict free.  The whole
-// chain (every k-group, every doubling step) is ONE persistent dataflow
-// launch over (task, tile) items with per-matrix completion counters.
+// (20 / 68 doubles) make both fragment loads bank-conflict free.  One launch
+// runs the same step index for every k-group (a work list of segments), and
+// each doubling step runs for all groups at once.  (A persistent dataflow
+// variant with per-matrix completion counters measured slower; see
+// tools/experiments/tiled_dataflow.cu.txt.)
 //
 // Reference mapping: schemes.py:264-361 (chains), :376-395 / :411-430
 // (trig / wave use), driver.py:91-98 (doubling), driver.py:115/:139
@@ -71,84 +73,56 @@ __device__ __forceinline__ void wait_group() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Persistent dataflow schedule: a task = one Op applied to one matrix (all
-// its 64x64 tiles); items = (task, tile) in topological order, handed out by
-// an atomic counter (so the items in flight stay a tight window and the
-// tiles of one product share its operand panels in L2).  Before an item a
-// CTA waits until its matrix has completed `need` tiles (all tiles of the
-// previous step); after the tile's epilogue it bumps the matrix's counter.
-// The lowest unfinished item always has its dependencies done and is held
-// by a resident CTA (the grid never exceeds the resident capacity), so the
-// schedule cannot deadlock; there are no per-step launches, no launch tails
-// and no host round trips between steps.
-struct Task {
-  int32_t b;         // matrix
-  int16_t op;        // op table index
-  int16_t dbl_step;  // -1 for chain ops, else doubling step
-  int32_t need;      // tiles of this matrix that must be complete first
-  int32_t pad;
+struct Seg {
+  int32_t op;       // op index into the op table
+  int32_t idx_off;  // offset of this segment's matrices in the index list
+  int32_t start;    // first work item (CTA row) of this segment
 };
 
-struct FlowArgs {
+struct LaunchArgs {
   double* ws;
-  const double* in0;   // slot-0 alias (float64 input, n == NP) or null
-  const Task* tasks;
-  const Op* ops;       // op table
-  const double* tsc;   // per-matrix t' (wave) or null
-  const int32_t* S;    // per-matrix s
-  int* done;           // per-matrix completed-tile counters (zeroed)
-  unsigned long long* next;  // work counter (zeroed)
-  void* cout;
+  const double* in0;    // slot-0 alias (float64 input, n == NP) or null
+  const int32_t* idx;   // index lists
+  const Op* ops;        // op table
+  const double* tsc;    // per-matrix t' (wave) or null
+  const int32_t* S;     // per-matrix s
+  void* cout;           // caller's outputs
   void* sout;
   size_t mat_stride;
-  long long items;
-  int NP, n, out_f32, tiles;
+  int NP, n, out_f32, dbl_step;  // dbl_step: -1 for chain ops, else i
+  int nseg, total, item_base, pad;
+  Seg seg[MAXSEG];
 };
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__global__ void __launch_bounds__(THREADS, 4) dataflow_kernel(const FlowArgs args) {
+// One 64x64 output tile of one matrix: acc = L R over the full NP-deep
+// contraction, then the op's linear combinations from the staged
+// accumulator tile with row-contiguous (coalesced) global reads and writes.
+__global__ void __launch_bounds__(THREADS, 4) gemm_epi_kernel(const LaunchArgs args) {
   extern __shared__ __align__(16) double sm[];
   __shared__ Op op;
-  __shared__ Task task;
-  __shared__ long long sh_item;
+  __shared__ int sh_b;
   double* As = sm;
   double* Bs = sm + STAGES * A_STAGE;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) sh_item = static_cast<long long>(atomicAdd(args.next, 1ull));
+  const int item = static_cast<int>(blockIdx.y) + args.item_base;
+  Seg sg = args.seg[0];
+#pragma unroll
+  for (int i = 1; i < MAXSEG; ++i)
+    if (i < args.nseg && item >= args.seg[i].start) sg = args.seg[i];
+  for (int i = tid; i < static_cast<int>(sizeof(Op) / 4); i += THREADS)
+    reinterpret_cast<int*>(&op)[i] = reinterpret_cast<const int*>(args.ops + sg.op)[i];
+  if (tid == 0) sh_b = args.idx[sg.idx_off + item - sg.start];
+  __syncthreads();
+  const int b = sh_b;
   const int NP = args.NP;
   const int tiles_n = NP / BN;
-  const size_t slotsz = static_cast<size_t>(NP) * NP;
+  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x - tm * tiles_n;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int n = args.n;
   const size_t nn = static_cast<size_t>(n) * n;
-
-  while (true) {
-    __syncthreads();  // previous item's smem (op, task, epilogue tile) is free
-    const long long item = sh_item;
-    if (item >= args.items) break;
-    const long long ti = item / args.tiles;
-    const int tile = static_cast<int>(item - ti * args.tiles);
-    unsigned long long nxt = 0;
-    if (tid == 0) {
-      nxt = atomicAdd(args.next, 1ull);  // next item, consumed after this one
-      task = args.tasks[ti];
-      if (task.need > 0) {
-        const int* cnt = args.done + task.b;
-        while (ld_acquire(cnt) < task.need) __nanosleep(64);
-      }
-    }
-    __syncthreads();
-    for (int i = tid; i < static_cast<int>(sizeof(Op) / 4); i += THREADS)
-      reinterpret_cast<int*>(&op)[i] = reinterpret_cast<const int*>(args.ops + task.op)[i];
-    __syncthreads();
-    const int b = task.b;
-    const int tm = tile / tiles_n, tn = tile - tm * tiles_n;
+  const size_t slotsz = static_cast<size_t>(NP) * NP;
+  {
     double* base = args.ws + static_cast<size_t>(b) * args.mat_stride;
     auto slot = [&](int sl) -> double* {
       if (sl == 0 && args.in0)
@@ -225,7 +199,7 @@ __global__ void __launch_bounds__(THREADS, 4) dataflow_kernel(const FlowArgs arg
     const int s_b = args.S[b];
     const double sc_tp = args.tsc ? args.tsc[b] : 1.0;
     const double sc_f = ldexp(1.0, -s_b), sc_f2 = ldexp(1.0, -2 * s_b);
-    const bool final_now = task.dbl_step < 0 ? (s_b == 0) : (s_b == task.dbl_step + 1);
+    const bool final_now = args.dbl_step < 0 ? (s_b == 0) : (s_b == args.dbl_step + 1);
     const int nout = op.nout;
     const int r0 = tm * BM, c0 = tn * BN;
 #pragma unroll 2
@@ -243,8 +217,8 @@ __global__ void __launch_bounds__(THREADS, 4) dataflow_kernel(const FlowArgs arg
           const int src = os.t[tt].src;
           const double cf = os.t[tt].c;
           double x0, x1;
-          if (src >= 0) {  // L2-coherent load: another SM wrote this slot
-            const double2 v = __ldcg(reinterpret_cast<const double2*>(slot(src) + off));
+          if (src >= 0) {
+            const double2 v = *reinterpret_cast<const double2*>(slot(src) + off);
             x0 = v.x; x1 = v.y;
           } else if (src == SRC_ACC) {
             x0 = av.x; x1 = av.y;
@@ -265,7 +239,7 @@ __global__ void __launch_bounds__(THREADS, 4) dataflow_kernel(const FlowArgs arg
         }
         if (q == 0) { o0[0] = v0; o0[1] = v1; }
         if (q == 1) { o1[0] = v0; o1[1] = v1; }
-        __stcg(reinterpret_cast<double2*>(base + os.slot * slotsz + off), make_double2(v0, v1));
+        *reinterpret_cast<double2*>(base + os.slot * slotsz + off) = make_double2(v0, v1);
         if (os.final != FIN_NONE && final_now && r < n) {
           void* dst = os.final == FIN_COS ? args.cout : args.sout;
           const size_t o = static_cast<size_t>(b) * nn + static_cast<size_t>(r) * n + c;
@@ -284,12 +258,6 @@ __global__ void __launch_bounds__(THREADS, 4) dataflow_kernel(const FlowArgs arg
           }
         }
       }
-    }
-    __syncthreads();  // every thread's slot stores precede the release
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(args.done + b, 1);
-      sh_item = static_cast<long long>(nxt);
     }
   }
 }
@@ -604,7 +572,13 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
 
   if (!order.empty()) {
     // op table: per group, its program ops then its two doubling op pairs
+    struct LaunchPlan {
+      std::vector<tk::Seg> seg;
+      int total;
+      int dbl_step;
+    };
     std::vector<Op> table;
+    std::vector<LaunchPlan> plans;
     std::vector<std::vector<size_t>> prog_off(groups.size());
     for (size_t gi = 0; gi < groups.size(); ++gi) {
       Group& G = groups[gi];
@@ -618,51 +592,44 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
       for (auto& op : doubling_ops(G.c1, G.s1, G.prog.cos_slot, G.prog.sin_slot)) table.push_back(op);
     }
     if (table.size() > 128) return cudaErrorInvalidValue;
-
-    // Task list in topological order: step j of every matrix before step
-    // j + 1 of any; need = tiles of the matrix's earlier steps.
-    const int T = (NP / tk::BM) * (NP / tk::BN);
-    std::vector<tk::Task> tasks;
-    std::vector<int32_t> done_ops(batch, 0);  // ops of earlier steps per matrix
-    for (int j = 0;; ++j) {
-      bool any = false;
+    // chain step j of every group in one launch
+    size_t max_steps = 0;
+    for (auto& G : groups) max_steps = std::max(max_steps, G.prog.steps.size());
+    for (size_t j = 0; j < max_steps; ++j) {
+      LaunchPlan L{{}, 0, -1};
       for (size_t gi = 0; gi < groups.size(); ++gi) {
         const Group& G = groups[gi];
-        const int nst = static_cast<int>(G.prog.steps.size());
-        for (size_t q = 0; q < G.cnt; ++q) {
-          const int32_t b = order[G.off + q];
-          if (j >= nst + hs[b]) continue;
-          any = true;
-          int first, nops, dbl;
-          if (j < nst) {
-            first = static_cast<int>(prog_off[gi][j]);
-            nops = static_cast<int>(G.prog.steps[j].size());
-            dbl = -1;
-          } else {
-            dbl = j - nst;
-            first = static_cast<int>(G.dbl_op[dbl & 1]);
-            nops = 2;
-          }
-          for (int o = 0; o < nops; ++o)
-            tasks.push_back({b, static_cast<int16_t>(first + o), static_cast<int16_t>(dbl),
-                             done_ops[b] * T, 0});
-          done_ops[b] += nops;
+        if (j >= G.prog.steps.size()) continue;
+        for (size_t o = 0; o < G.prog.steps[j].size(); ++o) {
+          L.seg.push_back({static_cast<int32_t>(prog_off[gi][j] + o),
+                           static_cast<int32_t>(G.off), L.total});
+          L.total += static_cast<int>(G.cnt);
         }
       }
-      if (!any) break;
+      plans.push_back(L);
     }
+    // doubling step i of every group in one launch
+    int max_s = 0;
+    for (auto& G : groups) max_s = std::max(max_s, G.max_s);
+    for (int i = 0; i < max_s; ++i) {
+      LaunchPlan L{{}, 0, i};
+      for (const Group& G : groups) {
+        int cnt = 0;
+        for (size_t j = 0; j < G.cnt; ++j)
+          if (hs[order[G.off + j]] > i) ++cnt;
+        if (!cnt) continue;
+        for (int o = 0; o < 2; ++o) {
+          L.seg.push_back({static_cast<int32_t>(G.dbl_op[i & 1] + o),
+                           static_cast<int32_t>(G.off), L.total});
+          L.total += cnt;
+        }
+      }
+      plans.push_back(L);
+    }
+    for (auto& L : plans)
+      if (L.seg.size() > static_cast<size_t>(tk::MAXSEG)) return cudaErrorInvalidValue;
 
-    tk::Task* d_tasks = nullptr;
-    int* d_done = nullptr;
-    e = cudaMallocAsync(reinterpret_cast<void**>(&d_tasks), tasks.size() * sizeof(tk::Task), stream);
-    if (e == cudaSuccess)
-      e = cudaMallocAsync(reinterpret_cast<void**>(&d_done),
-                          static_cast<size_t>(batch) * sizeof(int) + 16, stream);
-    if (e == cudaSuccess)
-      e = cudaMemsetAsync(d_done, 0, static_cast<size_t>(batch) * sizeof(int) + 16, stream);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(d_tasks, tasks.data(), tasks.size() * sizeof(tk::Task),
-                          cudaMemcpyHostToDevice, stream);
+    e = cudaMemcpyAsync(w.idx, order.data(), order.size() * 4, cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(w.ops, table.data(), table.size() * sizeof(Op), cudaMemcpyHostToDevice,
                           stream);
@@ -670,46 +637,42 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     if (e != cudaSuccess) return e;
 
     static bool attr_done = false;
-    static int resident = 0;
     if (!attr_done) {
-      e = cudaFuncSetAttribute(tk::dataflow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      e = cudaFuncSetAttribute(tk::gemm_epi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(tk::SMEM));
       if (e != cudaSuccess) return e;
-      int per_sm = 0, dev = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tk::dataflow_kernel, tk::THREADS,
-                                                    tk::SMEM);
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      resident = std::max(1, per_sm) * sms;
       attr_done = true;
     }
-    tk::FlowArgs A{};
+    const unsigned tiles = static_cast<unsigned>((NP / tk::BM) * (NP / tk::BN));
+    tk::LaunchArgs A{};
     A.ws = w.slots;
     A.in0 = fold ? static_cast<const double*>(a) : nullptr;
-    A.tasks = d_tasks;
+    A.idx = w.idx;
     A.ops = w.ops;
     A.tsc = wave ? w.tsc : nullptr;
     A.S = dS;
-    A.done = d_done;
-    A.next = reinterpret_cast<unsigned long long*>(
-        reinterpret_cast<char*>(d_done) + ((static_cast<size_t>(batch) * sizeof(int) + 7) & ~size_t(7)));
     A.cout = c_out;
     A.sout = s_out;
     A.mat_stride = mat_stride;
-    A.items = static_cast<long long>(tasks.size()) * T;
     A.NP = NP;
     A.n = n;
     A.out_f32 = out_f32;
-    A.tiles = T;
-    const long long grid = std::min<long long>(A.items, resident);
     prof_begin(stream);
-    tk::dataflow_kernel<<<static_cast<unsigned>(grid), tk::THREADS, tk::SMEM, stream>>>(A);
+    for (const LaunchPlan& L : plans) {
+      A.dbl_step = L.dbl_step;
+      A.nseg = static_cast<int>(L.seg.size());
+      for (size_t i = 0; i < L.seg.size(); ++i) A.seg[i] = L.seg[i];
+      A.total = L.total;
+      for (int done = 0; done < L.total; done += 65535) {
+        A.item_base = done;
+        const int cnt = std::min(65535, L.total - done);
+        dim3 grid(tiles, static_cast<unsigned>(cnt), 1);
+        tk::gemm_epi_kernel<<<grid, tk::THREADS, tk::SMEM, stream>>>(A);
+        ++*launches;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      }
+    }
     prof_end(stream);
-    ++*launches;
-    e = cudaGetLastError();
-    cudaFreeAsync(d_tasks, stream);
-    cudaFreeAsync(d_done, stream);
-    if (e != cudaSuccess) return e;
   }
 
   if (any_bad) {
