@@ -231,6 +231,90 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_cfg5(args, cfg):
+    """configs[4]: one 8192^2 matrix, block-row over the ranks with an NCCL
+    all-gather of the current right operand per product (distchain.py);
+    strong scaling (the total work is fixed)."""
+    import numpy as np
+    import torch
+
+    from paper_2010_00465_b200 import _lib, distchain
+    from paper_2010_00465_b200 import dist as pdist
+    world, rank, local = dist_setup(args)
+    kind, batch, n, dt, prec, desc = cfg
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    a_np, _ = make_inputs(kind, 1, n, seed=0)  # the same matrix on every rank
+    a_host = torch.from_numpy(np.ascontiguousarray(a_np[0])).pin_memory()
+    a = a_host.to(dev)
+    c, s_, st = distchain.cos_sin_distributed(a, gather_outputs=False)
+    torch.cuda.synchronize()
+    flops = 2.0 * n ** 3 * (st.k + 2 * st.s)
+    # correctness: symmetric input -> symmetric cos rows block vs its transpose
+    M, row0 = n // world, rank * (n // world)
+    blk = c[:, row0:row0 + M]
+    assert float((blk - blk.T).abs().max() / blk.abs().max()) <= 1e-10
+    for _ in range(args.warmup):
+        distchain.cos_sin_distributed(a, gather_outputs=False)
+    L = _lib.lib()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            distchain.cos_sin_distributed(a, gather_outputs=False)
+        e1.record()
+        torch.cuda.synchronize()
+    ms_step = pdist.max_over_ranks(e0.elapsed_time(e1) / args.steps, device=dev)
+    # e2e: H2D of A on every rank, compute, D2H of each rank's output rows
+    c_host = torch.empty((M, n), dtype=torch.float64).pin_memory()
+    s_host = torch.empty_like(c_host).pin_memory()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e2.record()
+    for _ in range(max(1, min(args.steps, 3))):
+        ad = a_host.to(dev, non_blocking=True)
+        cr, sr, _ = distchain.cos_sin_distributed(ad, gather_outputs=False)
+        c_host.copy_(cr, non_blocking=True)
+        s_host.copy_(sr, non_blocking=True)
+    e3.record()
+    torch.cuda.synchronize()
+    e2e_ms = pdist.max_over_ranks(e2.elapsed_time(e3) / max(1, min(args.steps, 3)), device=dev)
+    peak = None
+    if rank == 0:
+        pk = ctypes.c_double(0.0)
+        if L.csm_fp64_peak(20000, ctypes.byref(pk), None) == 0:
+            peak = pk.value
+    if rank == 0:
+        tfl = flops / (ms_step * 1e-3) / 1e12
+        line = {
+            "metric": METRIC, "value": 1.0 / (ms_step * 1e-3), "unit": "matrices/s",
+            "tflops": tfl, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+            "config": {"workload": args.config, "description": desc, "n": n,
+                       "k": st.k, "s": st.s, "gathers_per_step": st.gathers,
+                       "parallelism": f"block-row x{world}, NCCL all-gather per product"},
+            "roofline": {"bound": "tensor", "achieved": tfl, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (tfl / peak) if peak else None, "traffic": None,
+                         "kernel": "gemm_epi_kernel (slab mode) + all-gathers",
+                         "peak_source": "csm_fp64_peak on this GPU in this run"},
+            "e2e": {"value": 1.0 / (e2e_ms * 1e-3), "unit": "matrices/s",
+                    "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": 2 * M * n * 8,
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": (st.k + 2 * st.s) * args.steps,
+            "clocks": clk.summary(), "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def run_ours(args, cfg):
     import numpy as np
     import torch
@@ -455,6 +539,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif cfg[0] == "cfg5":
+        run_cfg5(args, cfg)
     else:
         run_ours(args, cfg)
 

@@ -137,6 +137,37 @@ int csm_wave_core(int dtype, int k, const void* a, const double* t,
 int csm_theta_table(int family, int precision, double* theta_cos,
                     double* theta_sin, int32_t* k, int capacity);
 
+/* ---- Block-row (slab) primitives of the distributed chain ----------------
+ * One very large matrix (configs[4], 8192^2) is split by rows over the
+ * ranks; every product is  out_rows = L_rows * R_full  with R_full the
+ * all-gathered right operand (the gather is the caller's: NCCL through
+ * torch.distributed in paper_2010_00465_b200/distchain.py).  The chain
+ * programs are exported as opaque op descriptors (csm_op_bytes() each) so
+ * the driver can interleave gathers and products step by step.
+ *   csm_chain_program: ops of scheme (family, k) in step order (fold = 1:
+ *     slot 0 is the raw input and 2^-s is folded into the products); returns
+ *     the step count, step_nops[i] = ops in step i, and the slots that hold
+ *     cos / sin after the chain (schemes.py:264-430).
+ *   csm_doubling_program: the two ops of one doubling step from (c0, s0)
+ *     into (c1, s1) (driver.py:91-98).
+ *   csm_slab_op: run one op on a slab of CSM_SLAB_SLOTS x M x NP float64
+ *     (M rows from global row row0, M and NP multiples of 64).  in0 = the
+ *     input rows (slot 0 alias), s / tp = the matrix's s and t', dbl_step =
+ *     -1 for chain ops or the doubling index; outputs that are final are
+ *     also written to cos_out / sin_out (the caller's M x NP rows).
+ *     scratch: device buffer of csm_slab_scratch_bytes(). */
+#define CSM_SLAB_SLOTS 9
+size_t csm_op_bytes(void);
+size_t csm_slab_scratch_bytes(void);
+int csm_chain_program(int family, int k, int fold, void* ops_out, int max_ops,
+                      int32_t* step_nops, int max_steps, int32_t* cos_slot,
+                      int32_t* sin_slot);
+int csm_doubling_program(int c0, int s0, int c1, int s1, void* ops_out);
+int csm_slab_op(const void* op, double* slab, int M, int NP, int row0,
+                const double* rhs_full, const double* in0, int s, double tp,
+                int dbl_step, void* cos_out, void* sin_out, int out_f32,
+                void* scratch, void* stream);
+
 /* ---- Measurement helpers (not part of the reference surface) ------------
  * csm_fp64_peak: time a DMMA (mma.sync m8n8k4 f64) throughput loop on the
  * current device for ~`iters` iterations; returns TFLOP/s in *tflops.

@@ -47,6 +47,12 @@ SIGNATURES = {
     "csm_theta_table": (_i32, [_i32, _i32, _vp, _vp, _vp, _i32]),
     "csm_fp64_peak": (_i32, [_i32, _vp, _vp]),
     "csm_last_launch_count": (_i64, []),
+    "csm_op_bytes": (_sz, []),
+    "csm_slab_scratch_bytes": (_sz, []),
+    "csm_chain_program": (_i32, [_i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _vp]),
+    "csm_doubling_program": (_i32, [_i32, _i32, _i32, _i32, _vp]),
+    "csm_slab_op": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _dp, _i32, _vp, _vp,
+                           _i32, _vp, _vp]),
     "csm_profile_enable": (_i32, [_i32]),
     "csm_profile_collect": (_i32, [_vp, _vp]),
 }

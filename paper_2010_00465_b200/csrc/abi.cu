@@ -36,6 +36,15 @@ cudaError_t launch_schedule(const int32_t* K, const int32_t* S, const int32_t* s
                             int64_t batch, int* bins, int32_t* order, cudaStream_t stream,
                             int64_t* launches);
 size_t tiled_workspace_bytes(int64_t batch, int n);
+size_t op_bytes();
+int chain_program(bool wave, int k, bool fold, void* ops_out, int max_ops, int32_t* step_nops,
+                  int max_steps, int32_t* cos_slot, int32_t* sin_slot);
+void doubling_program(int c0, int s0, int c1, int s1, void* ops_out);
+size_t slab_scratch_bytes();
+cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
+                    const double* rhs_full, const double* in0, int s, double tp, int dbl_step,
+                    void* cout, void* sout, int out_f32, void* scratch, cudaStream_t stream,
+                    int64_t* launches);
 cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void* c_out,
                       void* s_out, int64_t batch, int n, const int32_t* dK, const int32_t* dS,
                       const int32_t* dStatus, void* ws, cudaStream_t stream, int64_t* launches);
@@ -405,6 +414,48 @@ int csm_trace_dump(unsigned long long* out, int cap) {
   return n;
 }
 #endif
+
+size_t csm_op_bytes(void) { return csm::op_bytes(); }
+
+size_t csm_slab_scratch_bytes(void) { return csm::slab_scratch_bytes(); }
+
+int csm_chain_program(int family, int k, int fold, void* ops_out, int max_ops, int32_t* step_nops,
+                      int max_steps, int32_t* cos_slot, int32_t* sin_slot) {
+  if (family != CSM_FAMILY_TAYLOR && family != CSM_FAMILY_WAVE) return fail(CSM_ERR_ARG, "bad family");
+  const bool wave = family == CSM_FAMILY_WAVE;
+  const bool ok = wave ? (k == 3 || k == 4 || k == 5) : (k == 3 || k == 4 || k == 6 || k == 7);
+  if (!ok) return fail(CSM_ERR_ARG, "k_products is not valid for this scheme family");
+  if (!ops_out || !step_nops || !cos_slot || !sin_slot) return fail(CSM_ERR_ARG, "null pointer argument");
+  const int r = csm::chain_program(wave, k, fold != 0 && !wave, ops_out, max_ops, step_nops,
+                                   max_steps, cos_slot, sin_slot);
+  if (r < 0) return fail(CSM_ERR_ARG, "output arrays too small");
+  return r;
+}
+
+int csm_doubling_program(int c0, int s0, int c1, int s1, void* ops_out) {
+  if (!ops_out) return fail(CSM_ERR_ARG, "null pointer argument");
+  const int v[4] = {c0, s0, c1, s1};
+  for (int i = 0; i < 4; ++i)
+    if (v[i] < 1 || v[i] >= CSM_SLAB_SLOTS) return fail(CSM_ERR_ARG, "slot out of range");
+  csm::doubling_program(c0, s0, c1, s1, ops_out);
+  return CSM_SUCCESS;
+}
+
+int csm_slab_op(const void* op, double* slab, int M, int NP, int row0, const double* rhs_full,
+                const double* in0, int s, double tp, int dbl_step, void* cos_out, void* sin_out,
+                int out_f32, void* scratch, void* stream) {
+  g_launches = 0;
+  if (!op || !slab || !rhs_full || !scratch) return fail(CSM_ERR_ARG, "null pointer argument");
+  if (M <= 0 || NP <= 0 || M % 64 || NP % 64 || row0 < 0 || row0 + M > NP)
+    return fail(CSM_ERR_ARG, "slab shape must be M x NP with M, NP multiples of 64");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaError_t e = csm::slab_op(op, slab, M, NP, row0, rhs_full, in0, s, tp, dbl_step, cos_out,
+                               sin_out, out_f32, scratch, static_cast<cudaStream_t>(stream),
+                               &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "slab op");
+  return CSM_SUCCESS;
+}
 
 int csm_profile_enable(int on) {
   prof_clear();

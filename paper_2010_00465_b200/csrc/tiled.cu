@@ -25,6 +25,7 @@
 // (trig / wave use), driver.py:91-98 (doubling), driver.py:115/:139
 // (scaling), matcore.py:107-121 (linear combinations, fused here).
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -92,6 +93,12 @@ struct LaunchArgs {
   int NP, n, out_f32, dbl_step;  // dbl_step: -1 for chain ops, else i
   int nseg, total, item_base, pad;
   Seg seg[MAXSEG];
+  // Block-row (slab) mode for the distributed chain: every slot holds M
+  // rows of the NP x NP matrix starting at global row row0, and the right
+  // operand is the all-gathered full matrix rhs_full.  Batch mode: M = NP,
+  // row0 = 0, rhs_full = null.
+  const double* rhs_full;
+  int M, row0;
 };
 
 // One 64x64 output tile of one matrix: acc = L R over the full NP-deep
@@ -115,13 +122,14 @@ __global__ void __launch_bounds__(THREADS, 4) gemm_epi_kernel(const LaunchArgs a
   __syncthreads();
   const int b = sh_b;
   const int NP = args.NP;
+  const int M = args.M;
   const int tiles_n = NP / BN;
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x - tm * tiles_n;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
   const int n = args.n;
   const size_t nn = static_cast<size_t>(n) * n;
-  const size_t slotsz = static_cast<size_t>(NP) * NP;
+  const size_t slotsz = static_cast<size_t>(M) * NP;
   {
     double* base = args.ws + static_cast<size_t>(b) * args.mat_stride;
     auto slot = [&](int sl) -> double* {
@@ -130,7 +138,7 @@ __global__ void __launch_bounds__(THREADS, 4) gemm_epi_kernel(const LaunchArgs a
       return base + sl * slotsz;
     };
     const double* L = slot(op.lhs) + static_cast<size_t>(tm) * BM * NP;
-    const double* R = slot(op.rhs) + static_cast<size_t>(tn) * BN;
+    const double* R = (args.rhs_full ? args.rhs_full : slot(op.rhs)) + static_cast<size_t>(tn) * BN;
 
     auto load_stage = [&](int stage, int k0) {
       double* as = As + stage * A_STAGE;
@@ -208,7 +216,8 @@ __global__ void __launch_bounds__(THREADS, 4) gemm_epi_kernel(const LaunchArgs a
       const int r = r0 + rr, c = c0 + cc;
       const size_t off = static_cast<size_t>(r) * NP + c;
       const double2 av = *reinterpret_cast<const double2*>(E + rr * LDE + cc);
-      const double i0 = (r == c) ? 1.0 : 0.0, i1 = (r == c + 1) ? 1.0 : 0.0;
+      const int rg = r + args.row0;  // global row (slab mode)
+      const double i0 = (rg == c) ? 1.0 : 0.0, i1 = (rg == c + 1) ? 1.0 : 0.0;
       double o0[2] = {0.0, 0.0}, o1[2] = {0.0, 0.0};  // outputs 0 and 1 of this pair
       for (int q = 0; q < nout; ++q) {
         const OutSpec& os = op.out[q];
@@ -657,6 +666,9 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     A.NP = NP;
     A.n = n;
     A.out_f32 = out_f32;
+    A.M = NP;
+    A.row0 = 0;
+    A.rhs_full = nullptr;
     prof_begin(stream);
     for (const LaunchPlan& L : plans) {
       A.dbl_step = L.dbl_step;
@@ -689,6 +701,97 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// Block-row (slab) primitives for the distributed chain (python driver
+// paper_2010_00465_b200/distchain.py does the all-gathers).
+
+size_t op_bytes() { return sizeof(Op); }
+
+// Chain program of (family, k) as a flat op list; returns the step count.
+int chain_program(bool wave, int k, bool fold, void* ops_out, int max_ops, int32_t* step_nops,
+                  int max_steps, int32_t* cos_slot, int32_t* sin_slot) {
+  Program P = build_program(wave, k, fold);
+  if (static_cast<int>(P.steps.size()) > max_steps) return -1;
+  int nops = 0;
+  for (auto& st : P.steps) nops += static_cast<int>(st.size());
+  if (nops > max_ops) return -1;
+  Op* out = static_cast<Op*>(ops_out);
+  int o = 0;
+  for (size_t i = 0; i < P.steps.size(); ++i) {
+    step_nops[i] = static_cast<int32_t>(P.steps[i].size());
+    for (auto& op : P.steps[i]) out[o++] = op;
+  }
+  *cos_slot = P.cos_slot;
+  *sin_slot = P.sin_slot;
+  return static_cast<int>(P.steps.size());
+}
+
+void doubling_program(int c0, int s0, int c1, int s1, void* ops_out) {
+  auto v = doubling_ops(c0, s0, c1, s1);
+  Op* out = static_cast<Op*>(ops_out);
+  out[0] = v[0];
+  out[1] = v[1];
+}
+
+size_t slab_scratch_bytes() { return sizeof(Op) + 64; }
+
+// Run one Op on a block-row slab: out rows = L_rows * rhs_full (+ epilogue).
+// scratch: device buffer of slab_scratch_bytes() (op descriptor, s, t').
+cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
+                    const double* rhs_full, const double* in0, int s, double tp, int dbl_step,
+                    void* cout, void* sout, int out_f32, void* scratch, cudaStream_t stream,
+                    int64_t* launches) {
+  if (M % tk::BM != 0 || NP % tk::BN != 0) return cudaErrorInvalidValue;
+  struct alignas(16) Staged {
+    Op op;
+    int32_t idx, s, pad0, pad1;
+    double tp;
+  };
+  static_assert(sizeof(Staged) <= sizeof(Op) + 64, "scratch layout");
+  Staged h{};
+  std::memcpy(&h.op, op_host, sizeof(Op));
+  h.idx = 0;
+  h.s = s;
+  h.tp = tp;
+  cudaError_t e = cudaMemcpyAsync(scratch, &h, sizeof(Staged), cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamSynchronize(stream);  // h lives on this stack frame
+  if (e != cudaSuccess) return e;
+  static bool attr_done = false;
+  if (!attr_done) {
+    e = cudaFuncSetAttribute(tk::gemm_epi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(tk::SMEM));
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  Staged* d = static_cast<Staged*>(scratch);
+  tk::LaunchArgs A{};
+  A.ws = slab;
+  A.in0 = in0;
+  A.idx = &d->idx;
+  A.ops = &d->op;
+  A.tsc = &d->tp;
+  A.S = &d->s;
+  A.cout = cout;
+  A.sout = sout;
+  A.mat_stride = 0;
+  A.NP = NP;
+  A.n = NP;
+  A.out_f32 = out_f32;
+  A.dbl_step = dbl_step;
+  A.nseg = 1;
+  A.total = 1;
+  A.item_base = 0;
+  A.seg[0] = {0, 0, 0};
+  A.rhs_full = rhs_full;
+  A.M = M;
+  A.row0 = row0;
+  dim3 grid(static_cast<unsigned>((M / tk::BM) * (NP / tk::BN)), 1, 1);
+  tk::gemm_epi_kernel<<<grid, tk::THREADS, tk::SMEM, stream>>>(A);
+  ++*launches;
+  return cudaGetLastError();
 }
 
 }  // namespace csm

@@ -1,0 +1,204 @@
+"""Block-row distributed cos/sin of ONE large matrix (configs[4]: 8192^2).
+
+SURVEY.md 8e: the matrix is split by rows over the W ranks (M = n / W rows
+each, one process per GPU).  Every product of the chain is
+
+    out_rows = L_rows @ R_full,
+
+so the only exchange is an all-gather of the current right operand over
+NVLink (NCCL, through torch.distributed).  Polynomials in A commute, which
+removes gathers: the input A is replicated on every rank, so A A and the
+final sine product (computed as sc A instead of A sc) need none, and a
+gathered operand is cached until its slot is overwritten -- the degree-12
+chain then gathers y, c4, mid, cos and one C per doubling step (5 + s).
+
+The products and their fused linear combinations run in the sm_100a library
+(csm_slab_op); the chain programs come from the library too
+(csm_chain_program / csm_doubling_program), so this driver only schedules
+gathers and launches.  Selection uses the full replicated matrix on every
+rank (bit-exact norm, driver.py:64-88).
+"""
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass
+
+from . import _lib
+from .records import Precision, _PREC_CODE
+
+NSLOT = 9  # CSM_SLAB_SLOTS
+_OP_HEAD = struct.Struct("<4i")
+_OUT_HEAD = struct.Struct("<4i")
+_TERM = struct.Struct("<iid")
+MAXT = 8
+
+
+@dataclass
+class OpView:
+    """Decoded view of one op descriptor (tiled.cu tk::Op)."""
+
+    raw: bytearray
+    lhs: int
+    rhs: int
+    outs: list  # [(slot, scale, final, [(src, coef), ...])]
+
+    def swapped(self) -> "OpView":
+        raw = bytearray(self.raw)
+        _OP_HEAD.pack_into(raw, 0, self.rhs, self.lhs, len(self.outs), 0)
+        return OpView(raw, self.rhs, self.lhs, self.outs)
+
+
+def decode_op(raw: bytes) -> OpView:
+    lhs, rhs, nout, _ = _OP_HEAD.unpack_from(raw, 0)
+    outs = []
+    off = _OP_HEAD.size
+    per_out = _OUT_HEAD.size + MAXT * _TERM.size
+    for q in range(3):
+        base = off + q * per_out
+        slot, nterms, scale, final = _OUT_HEAD.unpack_from(raw, base)
+        terms = [_TERM.unpack_from(raw, base + _OUT_HEAD.size + t * _TERM.size)
+                 for t in range(nterms)]
+        if q < nout:
+            outs.append((slot, scale, final, [(src, c) for src, _, c in terms]))
+    return OpView(bytearray(raw), lhs, rhs, outs)
+
+
+def chain_program(k: int, fold: bool = True):
+    """(steps, cos_slot, sin_slot): steps = list of lists of OpView."""
+    L = _lib.lib()
+    ob = int(L.csm_op_bytes())
+    buf = ctypes.create_string_buffer(ob * 16)
+    nops = (ctypes.c_int32 * 16)()
+    cs, ss = ctypes.c_int32(), ctypes.c_int32()
+    nsteps = _lib.check(L.csm_chain_program(_lib.FAMILY_TAYLOR, k, 1 if fold else 0,
+                                            buf, 16, nops, 16, ctypes.byref(cs),
+                                            ctypes.byref(ss)), "csm_chain_program")
+    steps, o = [], 0
+    for i in range(nsteps):
+        step = []
+        for _ in range(nops[i]):
+            step.append(decode_op(buf.raw[o * ob:(o + 1) * ob]))
+            o += 1
+        steps.append(step)
+    return steps, cs.value, ss.value
+
+
+def doubling_program(c0: int, s0: int, c1: int, s1: int):
+    L = _lib.lib()
+    ob = int(L.csm_op_bytes())
+    buf = ctypes.create_string_buffer(ob * 2)
+    _lib.check(L.csm_doubling_program(c0, s0, c1, s1, buf), "csm_doubling_program")
+    return [decode_op(buf.raw[:ob]), decode_op(buf.raw[ob:2 * ob])]
+
+
+# -- device primitives (replaceable by test doubles in the CPU tests) --------
+
+def _device_slab_op(op: OpView, slab, M, n, row0, rhs_full, in0, s, dbl_step,
+                    cos_rows, sin_rows, scratch, stream):
+    import torch
+    vp = ctypes.c_void_p
+    raw = (ctypes.c_char * len(op.raw)).from_buffer(op.raw)
+    _lib.check(_lib.lib().csm_slab_op(
+        raw, vp(slab.data_ptr()), M, n, row0, vp(rhs_full.data_ptr()),
+        vp(in0.data_ptr()), s, 0.0, dbl_step, vp(cos_rows.data_ptr()),
+        vp(sin_rows.data_ptr()), 0, vp(scratch.data_ptr()),
+        vp(int((stream or torch.cuda.current_stream()).cuda_stream))), "csm_slab_op")
+
+
+def _device_select(a, precision: Precision):
+    from .api import norm1, select_batch
+    k, s, st = select_batch([norm1(a)], precision=precision)
+    if st[0] != 0:
+        raise ValueError("norm must be finite and nonnegative")
+    return int(k[0]), int(s[0])
+
+
+slab_op = _device_slab_op
+select = _device_select
+
+
+@dataclass
+class DistStats:
+    k: int
+    s: int
+    gathers: int
+    products: int
+
+
+def cos_sin_distributed(a, precision: Precision = Precision.DOUBLE, *,
+                        group=None, gather_outputs: bool = True):
+    """cos(a), sin(a) for one n x n float64 matrix replicated on every rank
+    of `group`, computed block-row over the ranks.  Returns (cos, sin,
+    stats): the full matrices if gather_outputs, else this rank's rows."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n = int(a.shape[0])
+    if a.shape != (n, n) or a.dtype != torch.float64:
+        raise ValueError("expected a square float64 tensor")
+    if n % (64 * world):
+        raise ValueError(f"n={n} must be a multiple of 64 x world ({world})")
+    M, row0 = n // world, rank * (n // world)
+    a = a.contiguous()
+    k, s = select(a, precision)
+    steps, cos_slot, sin_slot = chain_program(k, fold=True)
+    dev = a.device
+    slab = torch.empty((NSLOT, M, n), dtype=torch.float64, device=dev)
+    cos_rows = torch.empty((M, n), dtype=torch.float64, device=dev)
+    sin_rows = torch.empty_like(cos_rows)
+    scratch = None
+    if dev.type == "cuda":
+        scratch = torch.empty(int(_lib.lib().csm_slab_scratch_bytes()), dtype=torch.uint8,
+                              device=dev)
+    in0 = a[row0:row0 + M]
+    cache: dict[int, object] = {}
+    stats = DistStats(k, s, 0, 0)
+
+    def full(slot: int):
+        if slot == 0:
+            return a
+        if slot not in cache:
+            buf = torch.empty((n, n), dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_gather_into_tensor(buf, slab[slot].contiguous(), group=group)
+            else:
+                buf.copy_(slab[slot])
+            cache[slot] = buf
+            stats.gathers += 1
+        return cache[slot]
+
+    def run(op: OpView, dbl_step: int):
+        if op.lhs == 0 and op.rhs != 0:  # A sc = sc A: keep A as the gathered side
+            op = op.swapped()
+        rf = full(op.rhs)
+        slab_op(op, slab, M, n, row0, rf, in0, s, dbl_step, cos_rows, sin_rows,
+                scratch, None)
+        stats.products += 1
+        return [o[0] for o in op.outs]
+
+    for step in steps:
+        written = []
+        for op in step:
+            written += run(op, -1)
+        for w in written:
+            cache.pop(w, None)
+    c0, s0 = cos_slot, sin_slot
+    free = [i for i in range(1, NSLOT) if i not in (c0, s0)]
+    c1, s1 = free[0], free[1]
+    for i in range(s):
+        ops = doubling_program(c0, s0, c1, s1)
+        written = []
+        for op in ops:  # both products share the gathered C
+            written += run(op, i)
+        for w in written:
+            cache.pop(w, None)
+        c0, s0, c1, s1 = c1, s1, c0, s0
+    if not gather_outputs or world == 1:
+        return cos_rows, sin_rows, stats
+    cfull = torch.empty((n, n), dtype=torch.float64, device=dev)
+    sfull = torch.empty_like(cfull)
+    dist.all_gather_into_tensor(cfull, cos_rows, group=group)
+    dist.all_gather_into_tensor(sfull, sin_rows, group=group)
+    return cfull, sfull, stats

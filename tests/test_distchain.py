@@ -1,0 +1,116 @@
+"""Block-row distributed chain (configs[4] path).
+
+CPU: world_size 2 over gloo, with a torch-CPU TEST DOUBLE of the slab
+product (the library's op programs, gathers, operand caching, commuting of
+the sine product and doubling bookkeeping all run for real); the assembled
+result is checked against the oracle.  GPU: world_size 1 through the real
+sm_100a slab kernel against the oracle and the single-GPU path."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import cossin_oracle as orc
+from tests._util import rel1
+
+
+def np_slab_op(op, slab, M, n, row0, rhs_full, in0, s, dbl_step, cos_rows,
+               sin_rows, scratch, stream):
+    """Test double of csm_slab_op: the same op semantics in torch float64."""
+    def slot(i):
+        return in0 if i == 0 else slab[i]
+    acc = slot(op.lhs) @ rhs_full
+    eye = torch.eye(n, dtype=torch.float64)[row0:row0 + M]
+    outs = []
+    final_now = (s == 0) if dbl_step < 0 else (s == dbl_step + 1)
+    for sl, scale, final, terms in op.outs:
+        v = torch.zeros((M, n), dtype=torch.float64)
+        for src, c in terms:
+            x = acc if src == -1 else eye if src == -2 else (
+                outs[-3 - src] if src <= -3 else slot(src))
+            v = v + c * x
+        if scale == 2:
+            v = v * 2.0 ** -s
+        elif scale == 3:
+            v = v * 2.0 ** (-2 * s)
+        slab[sl] = v
+        outs.append(v)
+        if final and final_now:
+            (cos_rows if final == 1 else sin_rows).copy_(v)
+
+
+def _np_select(a, precision):
+    return orc.select(orc.norm1(a.numpy()))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2010_00465_b200 import distchain
+        distchain.slab_op = np_slab_op
+        distchain.select = _np_select
+        g = np.random.default_rng(0).standard_normal((n, n))
+        a = torch.from_numpy(20.0 * (g + g.T) / (2.0 * np.sqrt(n)))
+        c, s, st = distchain.cos_sin_distributed(a)
+        q.put((rank, c.numpy(), s.numpy(), st.k, st.s, st.gathers, st.products))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+def test_block_row_two_ranks_gloo():
+    n, world = 128, 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=150) for _ in range(world)), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=30)
+    g = np.random.default_rng(0).standard_normal((n, n))
+    a = 20.0 * (g + g.T) / (2.0 * np.sqrt(n))
+    c_ref, s_ref, k, s = orc.cos_sin(a)
+    for rank, c, sn, kk, ss, gathers, prods in res:
+        assert (kk, ss) == (k, s)
+        assert rel1(c, c_ref) <= 1e-12 and rel1(sn, s_ref) <= 1e-12
+        # products: k + 2s.  Gathers for k = 7: A never (replicated), y once
+        # (cached for y2 y), c4, mid, cos (reused by the first doubling step),
+        # the sine product as sc A, then one C per later doubling: 3 + s.
+        assert prods == k + 2 * s
+        if k == 7:
+            assert gathers == 3 + s if s else gathers == 4
+    assert np.array_equal(res[0][1], res[1][1])
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_block_row_single_gpu_against_oracle(cuda):
+    from paper_2010_00465_b200 import distchain
+    import paper_2010_00465_b200 as csm
+    n = 1024
+    g = np.random.default_rng(0).standard_normal((n, n))
+    a = 20.0 * (g + g.T) / (2.0 * np.sqrt(n))
+    c, s, st = distchain.cos_sin_distributed(torch.from_numpy(a).to(cuda))
+    c_ref, s_ref, k, sc = orc.cos_sin(a)
+    assert (st.k, st.s) == (k, sc)
+    single = csm.cos_sin(a)
+    # noise gate as in test_large_symmetric_against_oracle_noise_floor
+    assert rel1(c.cpu().numpy(), c_ref) <= 2e-11
+    assert rel1(s.cpu().numpy(), s_ref) <= 2e-11
+    assert rel1(c.cpu().numpy(), single.result.cos_part) <= 2e-11
