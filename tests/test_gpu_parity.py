@@ -175,7 +175,7 @@ def test_batched_float32(cuda, n):
         assert rel1(rep.sin_part[i], s64) <= TOL32
 
 
-@pytest.mark.parametrize("n", [48, 130])
+@pytest.mark.parametrize("n", [48, 100, 130])
 def test_batched_wave_laplacian(cuda, n):
     """configs[3] family (SPD Laplacian + potential), smaller n."""
     rng = np.random.default_rng(400 + n)
