@@ -131,6 +131,18 @@ int csm_wave_core(int dtype, int k, const void* a, const double* t,
                   int32_t* status, void* workspace, size_t ws_bytes,
                   void* stream);
 
+/* Standalone sines (off the cos/sin pair path; schemes.py:398-408 and
+ * :433-443): csm_taylor_sin9 = taylor_sin9(a) (degree-9 sine, exact-sine
+ * degree-4 core; the reference's ledger charges 5 products),
+ * csm_wave_sin34 = wave_sin34(a, t) (order-3 wave sine, 2 products).  No
+ * scaling, no selection.  Workspace: csm_sine_workspace_size(). */
+size_t csm_sine_workspace_size(int dtype, int64_t batch, int n);
+int csm_taylor_sin9(int dtype, const void* a, void* sin_out, int64_t batch, int n,
+                    int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+int csm_wave_sin34(int dtype, const void* a, const double* t, void* s_out,
+                   int64_t batch, int n, int32_t* status, void* workspace,
+                   size_t ws_bytes, void* stream);
+
 /* Copy the built-in theta table of (family, precision) -- the reference's
  * TAYLOR_TABLE / WAVE_TABLE (theta_tables.py:79-144) -- into host arrays of
  * `capacity` entries; returns the entry count (or a negative error). */

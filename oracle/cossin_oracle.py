@@ -244,6 +244,22 @@ def wave_core(a: np.ndarray, t: float, k: int):
     return c, float(t) * sc
 
 
+def taylor_sin9(a: np.ndarray):
+    """Degree-9 sine alone (schemes.py:398-408): exact-sine degree-4 core."""
+    eye = np.eye(a.shape[0])
+    y = a @ a
+    _, sc, _ = _deg4(y, eye, exact_sine=True)
+    return a @ sc
+
+
+def wave_sin34(a: np.ndarray, t: float):
+    """Order-3 wave sine (schemes.py:433-443): inexact-sine degree-4 core."""
+    eye = np.eye(a.shape[0])
+    y = float(t) * float(t) * a
+    _, sc, _ = _deg4(y, eye, exact_sine=False)
+    return float(t) * sc
+
+
 def double_angle(c, s, steps):
     """driver.py:91-98: S <- 2 S C (old C), then C <- 2 C C - I."""
     eye = np.eye(c.shape[0])

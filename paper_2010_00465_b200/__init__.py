@@ -13,12 +13,16 @@ from .api import (
     identity,
     matrix_from_rows,
     norm1,
+    read_matrix,
     select_batch,
     select_scheme,
     taylor_cos_sin,
+    taylor_sin9,
     wave_cos_sin,
     wave_cos_sin_batched,
     wave_kernels,
+    wave_sin34,
+    write_matrix,
 )
 from . import plan
 from .plan import BatchPlan
@@ -64,11 +68,15 @@ __all__ = [
     "identity",
     "matrix_from_rows",
     "norm1",
+    "read_matrix",
     "select_batch",
     "select_scheme",
     "table_for",
     "taylor_cos_sin",
+    "taylor_sin9",
     "wave_cos_sin",
     "wave_cos_sin_batched",
     "wave_kernels",
+    "wave_sin34",
+    "write_matrix",
 ]

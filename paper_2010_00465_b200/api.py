@@ -330,6 +330,50 @@ def wave_kernels(a, t: float, scheme: SchemeId,
     return WaveResult(c_part=c, s_part=s, cost=ledger)
 
 
+def _sine(a, t, ledger: CostLedger, charge: int):
+    torch = _torch()
+    L = _lib.lib()
+    batch = _as_batch(a, batched=False, f32_out=False)
+    x = batch.dev
+    n = int(x.shape[-1])
+    dev = x.device
+    out = torch.empty((1, n, n), dtype=batch.out_dtype, device=dev)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    ws_bytes = int(L.csm_sine_workspace_size(batch.code, 1, n))
+    ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
+    h = _vp(_stream_handle())
+    if t is None:
+        rc = L.csm_taylor_sin9(batch.code, _vp(x.data_ptr()),
+                               _vp(out.data_ptr()), 1, n,
+                               _vp(status.data_ptr()), _vp(ws.data_ptr()),
+                               ws_bytes, h)
+    else:
+        tv = _t_vector(float(t), 1, dev)
+        rc = L.csm_wave_sin34(batch.code, _vp(x.data_ptr()),
+                              _vp(tv.data_ptr()), _vp(out.data_ptr()), 1, n,
+                              _vp(status.data_ptr()), _vp(ws.data_ptr()),
+                              ws_bytes, h)
+    _lib.check(rc, "standalone sine")
+    ledger.charge_product(charge)
+    if batch.host == "numpy":
+        return out[0].cpu().numpy()
+    if batch.host == "torch":
+        return out[0].cpu()
+    return out[0]
+
+
+def taylor_sin9(a, ledger: CostLedger):
+    """Degree-9 sine alone (schemes.py:398-408): the exact-sine degree-4
+    core times a, no scaling; charges 5 products like the reference."""
+    return _sine(a, None, ledger, 5)
+
+
+def wave_sin34(a, t: float, ledger: CostLedger):
+    """Order-3 wave sine t * core(t^2 a) (schemes.py:433-443), no scaling;
+    charges 2 products like the reference."""
+    return _sine(a, t, ledger, 2)
+
+
 def select_scheme(norm: float, table: ThetaTable) -> tuple[SchemeId, int]:
     """(scheme, s) for an operand norm (driver.py:70-88), computed by the
     C++ host twin of the device selection (bit-exact log2/ceil rule)."""
@@ -405,8 +449,63 @@ def identity(n: int) -> np.ndarray:
     return np.eye(n, dtype=np.float64)
 
 
+def read_matrix(path: str) -> np.ndarray:
+    """Matrix text file: a "rows cols" header line, then one whitespace-
+    separated line per row; blank lines are ignored (matcore.py:154-195).
+    Every malformation raises MatrixInputError naming the file and line."""
+    with open(path, "r", encoding="ascii") as fh:
+        body = [ln.strip() for ln in fh]
+    body = [ln for ln in body if ln]
+    if not body:
+        raise MatrixInputError(f"{path}: empty file (line 1: missing header)")
+    head = body[0].split()
+    if len(head) != 2:
+        raise MatrixInputError(
+            f"{path}: line 1: header must be 'rows cols', got {body[0]!r}")
+    try:
+        nr, nc = (int(v) for v in head)
+    except ValueError:
+        raise MatrixInputError(
+            f"{path}: line 1: non-integer dimensions {body[0]!r}") from None
+    if nr <= 0 or nc <= 0:
+        raise MatrixInputError(f"{path}: line 1: dimensions must be positive")
+    if len(body) != nr + 1:
+        raise MatrixInputError(
+            f"{path}: expected {nr} data lines, found {len(body) - 1}")
+    rows = []
+    for lineno, ln in enumerate(body[1:], start=2):
+        fields = ln.split()
+        if len(fields) != nc:
+            raise MatrixInputError(f"{path}: line {lineno}: expected {nc} "
+                                   f"entries, found {len(fields)}")
+        try:
+            rows.append([float(v) for v in fields])
+        except ValueError:
+            raise MatrixInputError(
+                f"{path}: line {lineno}: non-numeric entry") from None
+    try:
+        return matrix_from_rows(rows)
+    except MatrixInputError as exc:
+        raise MatrixInputError(f"{path}: {exc}") from None
+
+
+def write_matrix(path: str, a) -> None:
+    """Write `a` in the format read_matrix accepts, each entry as repr()
+    of its float64 value so the round trip is exact (matcore.py:198-204)."""
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        a = a.detach().cpu().numpy()
+    a = np.asarray(a, dtype=np.float64)
+    nr, nc = a.shape
+    with open(path, "w", encoding="ascii") as fh:
+        fh.write(f"{nr} {nc}\n")
+        for row in a:
+            fh.write(" ".join(repr(float(v)) for v in row) + "\n")
+
+
 __all__ = [
     "BatchReport", "cos_sin", "cos_sin_batched", "identity",
-    "matrix_from_rows", "norm1", "select_batch", "select_scheme",
-    "taylor_cos_sin", "wave_cos_sin", "wave_cos_sin_batched", "wave_kernels",
+    "matrix_from_rows", "norm1", "read_matrix", "select_batch",
+    "select_scheme", "taylor_cos_sin", "taylor_sin9", "wave_cos_sin",
+    "wave_cos_sin_batched", "wave_kernels", "wave_sin34", "write_matrix",
 ]

@@ -47,7 +47,8 @@ cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
                     int64_t* launches);
 cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void* c_out,
                       void* s_out, int64_t batch, int n, const int32_t* dK, const int32_t* dS,
-                      const int32_t* dStatus, void* ws, cudaStream_t stream, int64_t* launches);
+                      const int32_t* dStatus, void* ws, cudaStream_t stream, int64_t* launches,
+                      int special);
 }  // namespace csm
 
 namespace {
@@ -165,7 +166,8 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
     if (e != cudaSuccess) return cuda_fail(e, "fused64 launch");
     ++g_launches;
   } else {
-    e = csm::run_tiled(dtype, wave, a, t, c, s, batch, n, K, S, st, w.tiled, stream, &g_launches);
+    e = csm::run_tiled(dtype, wave, a, t, c, s, batch, n, K, S, st, w.tiled, stream, &g_launches,
+                       0);
     if (e != cudaSuccess) return cuda_fail(e, "tiled chain");
   }
   return CSM_SUCCESS;
@@ -455,6 +457,47 @@ int csm_slab_op(const void* op, double* slab, int M, int NP, int row0, const dou
                                &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "slab op");
   return CSM_SUCCESS;
+}
+
+size_t csm_sine_workspace_size(int dtype, int64_t batch, int n) {
+  (void)dtype;
+  if (batch < 0 || n < 0) return 0;
+  return common_bytes(batch) + csm::tiled_workspace_bytes(batch, n) + 256;
+}
+
+static int standalone_sine(int dtype, bool wave, const void* a, const double* t, void* s_out,
+                           int64_t batch, int n, int32_t* status, void* ws, size_t ws_bytes,
+                           void* stream_v) {
+  g_launches = 0;
+  if (dtype != CSM_F64 && dtype != CSM_F32 && dtype != CSM_F32_IN_F64_OUT)
+    return fail(CSM_ERR_ARG, "bad dtype");
+  if (batch < 0 || n < 0) return fail(CSM_ERR_ARG, "batch and n must be nonnegative");
+  if (ws_bytes < csm_sine_workspace_size(dtype, batch, n))
+    return fail(CSM_ERR_WORKSPACE, "workspace smaller than csm_sine_workspace_size()");
+  if (batch == 0 || n == 0) return CSM_SUCCESS;
+  if (!a || !s_out || !status || !ws || (wave && !t)) return fail(CSM_ERR_ARG, "null pointer argument");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  CommonWs w = carve(ws, batch);
+  cudaError_t e = csm::launch_fill_ks(w.kbuf, w.sbuf, status, batch, 3, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
+  ++g_launches;
+  e = csm::run_tiled(dtype, wave, a, t, nullptr, s_out, batch, n, w.kbuf, w.sbuf, status, w.tiled,
+                     stream, &g_launches, wave ? 2 : 1);
+  if (e != cudaSuccess) return cuda_fail(e, "standalone sine");
+  return CSM_SUCCESS;
+}
+
+int csm_taylor_sin9(int dtype, const void* a, void* sin_out, int64_t batch, int n,
+                    int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
+  return standalone_sine(dtype, false, a, nullptr, sin_out, batch, n, status, workspace, ws_bytes,
+                         stream);
+}
+
+int csm_wave_sin34(int dtype, const void* a, const double* t, void* s_out, int64_t batch, int n,
+                   int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
+  return standalone_sine(dtype, true, a, t, s_out, batch, n, status, workspace, ws_bytes, stream);
 }
 
 int csm_profile_enable(int on) {

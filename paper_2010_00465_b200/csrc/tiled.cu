@@ -451,6 +451,29 @@ Program build_program(bool wave, int k, bool fold) {
   return P;
 }
 
+// Standalone sines (schemes.py:398-408, :433-443): special == 1 taylor_sin9
+// (the exact-sine degree-4 core, sin = A sc), special == 2 wave_sin34 (the
+// inexact-sine degree-4 core on y, s = t sc).  No doubling (s = 0).
+Program build_special(int special, bool fold) {
+  const int sy = fold ? tk::SC_F2 : tk::SC_NONE;
+  const int ss = fold ? tk::SC_F : tk::SC_NONE;
+  Program P;
+  auto step = [&](std::initializer_list<Op> ops) { P.steps.emplace_back(ops); };
+  if (special == 1) {
+    step({make_op(0, 0, {{1, {{ACC, 1.0}}, sy}})});
+    step({make_op(1, 1, {{2, {{ACC, 1.0}}}, {3, {{1, -1.0 / 5040.0}, {ACC, 1.0 / 362880.0}}}})});
+    step({make_op(2, 3, {{4, {{EYE, 1.0}, {1, -1.0 / 6.0}, {2, 1.0 / 120.0}, {ACC, 1.0}}}})});
+    step({make_op(0, 4, {{5, {{ACC, 1.0}}, ss, tk::FIN_SIN}})});
+    P.cos_slot = 6; P.sin_slot = 5;
+  } else {
+    step({make_op(0, 0, {{1, {{ACC, 1.0}}}, {2, {{0, -1.0 / 720.0}, {ACC, 1.0 / 40320.0}}}})});
+    step({make_op(1, 2, {{3, {{EYE, 1.0}, {0, -1.0 / 6.0}, {1, 1.0 / 120.0},
+                              {ACC, 720.0 / 5040.0}}, tk::SC_TP, tk::FIN_SIN}})});
+    P.cos_slot = 4; P.sin_slot = 3;
+  }
+  return P;
+}
+
 // Doubling op pair: S' = 2 S C, C' = 2 C C - I, into (c1, s1); final when
 // the matrix's s equals this step + 1.
 std::vector<Op> doubling_ops(int c0, int s0, int c1, int s1) {
@@ -508,7 +531,7 @@ static TiledWs carve(void* ws, int64_t batch, int n) {
 cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void* c_out,
                       void* s_out, int64_t batch, int n, const int32_t* dK,
                       const int32_t* dS, const int32_t* dStatus, void* ws,
-                      cudaStream_t stream, int64_t* launches) {
+                      cudaStream_t stream, int64_t* launches, int special) {
   cudaError_t e;
   const int NP = static_cast<int>(tiled_np(n));
   const size_t mat_stride = static_cast<size_t>(tk::NSLOT) * NP * NP;
@@ -574,7 +597,7 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     G.cnt = mem.size();
     G.max_s = mem.front().first;
     for (auto& m : mem) order.push_back(m.second);
-    G.prog = build_program(wave, G.k, fold);
+    G.prog = special ? build_special(special, fold) : build_program(wave, G.k, fold);
     free_pair(G.prog.cos_slot, G.prog.sin_slot, &G.c1, &G.s1);
     groups.push_back(std::move(G));
   }

@@ -167,6 +167,30 @@ def gen_norms(rng):
     np.savez_compressed(os.path.join(OUT, "norm1.npz"), **out)
 
 
+def gen_extras(rng):
+    """taylor_sin9 (schemes.py:398-408) and wave_sin34 (schemes.py:433-443)."""
+    from cossinm import CostLedger, taylor_sin9, wave_sin34
+    out = {}
+    names = []
+    for n, target in ((1, 0.3), (4, 0.05), (9, 0.4), (33, 0.2), (64, 0.1), (80, 0.15)):
+        m = rng.standard_normal((n, n))
+        a = m * (target / cossinm.norm1(m))
+        led = CostLedger()
+        out[f"sin9_{n}__a"] = a
+        out[f"sin9_{n}__out"] = taylor_sin9(a, led)
+        out[f"sin9_{n}__cost"] = np.array(int(led.total_cost))
+        names.append(f"sin9_{n}")
+        t = 0.7
+        led = CostLedger()
+        out[f"sin34_{n}__a"] = a
+        out[f"sin34_{n}__t"] = np.array(t)
+        out[f"sin34_{n}__out"] = wave_sin34(a, t, led)
+        out[f"sin34_{n}__cost"] = np.array(int(led.total_cost))
+        names.append(f"sin34_{n}")
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(OUT, "extras.npz"), **out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     rng = np.random.default_rng(20100465)
@@ -174,6 +198,7 @@ def main():
     gen_trig(rng)
     gen_wave(rng)
     gen_norms(rng)
+    gen_extras(np.random.default_rng(77))
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 

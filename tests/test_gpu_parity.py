@@ -121,6 +121,36 @@ def test_scheme_cores_match_oracle(cuda, rng):
             assert rel1(out.s_part, s) <= TOL64, (n, k)
 
 
+def test_standalone_sines_golden(cuda, golden_dir):
+    """taylor_sin9 / wave_sin34 (schemes.py:398-408, :433-443) against the
+    reference's own outputs, ledger charges 5 and 2."""
+    g = _golden(golden_dir, "extras.npz")
+    for name in g["names"]:
+        name = str(name)
+        a = g[f"{name}__a"]
+        led = csm.CostLedger()
+        if name.startswith("sin9"):
+            got = csm.taylor_sin9(a, led)
+        else:
+            got = csm.wave_sin34(a, float(g[f"{name}__t"]), led)
+        assert led.total_cost == int(g[f"{name}__cost"]), name
+        assert got.shape == a.shape and got.dtype == np.float64
+        assert rel1(got, g[f"{name}__out"]) <= TOL64, name
+
+
+@pytest.mark.parametrize("n", [64, 130, 256])
+def test_standalone_sines_match_oracle(cuda, rng, n):
+    a = rng.standard_normal((n, n))
+    a *= 0.3 / orc.norm1(a)
+    assert rel1(csm.taylor_sin9(a, csm.CostLedger()), orc.taylor_sin9(a)) <= TOL64
+    got = csm.wave_sin34(a, 1.7, csm.CostLedger())
+    assert rel1(got, orc.wave_sin34(a, 1.7)) <= TOL64
+    a32 = a.astype(np.float32)
+    got = csm.taylor_sin9(a32, csm.CostLedger())
+    assert got.dtype == np.float64
+    assert rel1(got, orc.taylor_sin9(a32.astype(np.float64))) <= TOL64
+
+
 def test_batched_cfg2_distribution(cuda):
     """configs[1] distribution (64x64, norms 1e-3..1e2), 512 matrices."""
     rng = np.random.default_rng(11)

@@ -124,3 +124,19 @@ def test_bitwise_identities():
     c, s, _, _ = orc.cos_sin(d)
     off = ~np.eye(3, dtype=bool)
     assert np.all(c[off] == 0.0) and np.all(s[off] == 0.0)
+
+
+def test_standalone_sines_match_reference(golden_dir):
+    """taylor_sin9 / wave_sin34 (schemes.py:398-408, :433-443) and their
+    ledger charges (5 and 2 products)."""
+    d = _load(golden_dir, "extras.npz")
+    for name in d["names"]:
+        name = str(name)
+        a = d[f"{name}__a"]
+        if name.startswith("sin9"):
+            got = orc.taylor_sin9(a)
+            assert int(d[f"{name}__cost"]) == 5
+        else:
+            got = orc.wave_sin34(a, float(d[f"{name}__t"]))
+            assert int(d[f"{name}__cost"]) == 2
+        assert rel1(got, d[f"{name}__out"]) <= 1e-14, name
