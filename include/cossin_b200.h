@@ -143,6 +143,28 @@ int csm_wave_sin34(int dtype, const void* a, const double* t, void* s_out,
                    int64_t batch, int n, int32_t* status, void* workspace,
                    size_t ws_bytes, void* stream);
 
+/* Double-double reference values (verify.py:480-521 reference_cos_sin):
+ * scale to ||A||_1 <= 2^-20, degree-12 Taylor pair and s doublings, every
+ * product the k-ordered compensated _dd_matmul (verify.py:449-459).  Each
+ * element follows the reference's exact operation sequence, so the float64
+ * outputs (hi + lo) are bit-identical to the reference's.  float64 input
+ * only.  s_host / status_host are HOST arrays of `batch` entries (status
+ * CSM_SELECT_OVERFLOW where norm / 2^-20 overflows, the reference's
+ * OverflowError); the call synchronises `stream` (s is chosen on the host,
+ * as the reference does).  csm_dd_matmul is the bare product (xl / yl may
+ * be NULL for a zero low part); csm_ddref_series_consts writes the 28
+ * _dd_const splits of 1/(2i)! and 1/(2i+1)! (cos hi[7], cos lo[7],
+ * sin hi[7], sin lo[7]; verify.py:405-412, :462-464). */
+size_t csm_ddref_workspace_size(int64_t batch, int n);
+int csm_ddref_cos_sin(const double* a, double* cos_out, double* sin_out,
+                      int64_t batch, int n, int32_t* s_host,
+                      int32_t* status_host, void* workspace, size_t ws_bytes,
+                      void* stream);
+int csm_dd_matmul(const double* xh, const double* xl, const double* yh,
+                  const double* yl, double* oh, double* ol, int64_t batch,
+                  int n, void* stream);
+int csm_ddref_series_consts(double* out28);
+
 /* Copy the built-in theta table of (family, precision) -- the reference's
  * TAYLOR_TABLE / WAVE_TABLE (theta_tables.py:79-144) -- into host arrays of
  * `capacity` entries; returns the entry count (or a negative error). */

@@ -48,6 +48,10 @@ SIGNATURES = {
     "csm_sine_workspace_size": (_sz, [_i32, _i64, _i32]),
     "csm_taylor_sin9": (_i32, [_i32, _vp, _vp, _i64, _i32, _vp, _vp, _sz, _vp]),
     "csm_wave_sin34": (_i32, [_i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _sz, _vp]),
+    "csm_ddref_workspace_size": (_sz, [_i64, _i32]),
+    "csm_ddref_cos_sin": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "csm_dd_matmul": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),
+    "csm_ddref_series_consts": (_i32, [_vp]),
     "csm_fp64_peak": (_i32, [_i32, _vp, _vp]),
     "csm_last_launch_count": (_i64, []),
     "csm_op_bytes": (_sz, []),

@@ -49,6 +49,14 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
                       void* s_out, int64_t batch, int n, const int32_t* dK, const int32_t* dS,
                       const int32_t* dStatus, void* ws, cudaStream_t stream, int64_t* launches,
                       int special);
+size_t ddref_workspace_doubles(int64_t batch, int n);
+void ddref_series_consts(double* out28);
+cudaError_t dd_matmul(const double* xh, const double* xl, const double* yh, const double* yl,
+                      double* oh, double* ol, int64_t batch, int n, cudaStream_t stream,
+                      int64_t* launches);
+cudaError_t ddref_chain(const double* a, const int32_t* dS, int smax, double* cos_out,
+                        double* sin_out, int64_t batch, int n, double* ws, cudaStream_t stream,
+                        int64_t* launches);
 }  // namespace csm
 
 namespace {
@@ -498,6 +506,97 @@ int csm_taylor_sin9(int dtype, const void* a, void* sin_out, int64_t batch, int 
 int csm_wave_sin34(int dtype, const void* a, const double* t, void* s_out, int64_t batch, int n,
                    int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
   return standalone_sine(dtype, true, a, t, s_out, batch, n, status, workspace, ws_bytes, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Double-double reference cos/sin (verify.py:480-521) and its product.
+
+size_t csm_ddref_workspace_size(int64_t batch, int n) {
+  if (batch < 0 || n < 0) return 0;
+  return 3 * align256(static_cast<size_t>(batch) * 8) +
+         csm::ddref_workspace_doubles(batch, n) * 8 + 256;
+}
+
+int csm_ddref_series_consts(double* out28) {
+  if (!out28) return fail(CSM_ERR_ARG, "null pointer argument");
+  csm::ddref_series_consts(out28);
+  return CSM_SUCCESS;
+}
+
+int csm_dd_matmul(const double* xh, const double* xl, const double* yh, const double* yl,
+                  double* oh, double* ol, int64_t batch, int n, void* stream) {
+  g_launches = 0;
+  if (batch < 0 || n < 0) return fail(CSM_ERR_ARG, "batch and n must be nonnegative");
+  if (batch == 0 || n == 0) return CSM_SUCCESS;
+  if (!xh || !yh || !oh || !ol) return fail(CSM_ERR_ARG, "null pointer argument");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaError_t e = csm::dd_matmul(xh, xl, yh, yl, oh, ol, batch, n,
+                                 static_cast<cudaStream_t>(stream), &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "dd_matmul");
+  return CSM_SUCCESS;
+}
+
+int csm_ddref_cos_sin(const double* a, double* cos_out, double* sin_out, int64_t batch, int n,
+                      int32_t* s_host, int32_t* status_host, void* ws, size_t ws_bytes,
+                      void* stream_v) {
+  g_launches = 0;
+  if (batch < 0 || n < 0) return fail(CSM_ERR_ARG, "batch and n must be nonnegative");
+  if (ws_bytes < csm_ddref_workspace_size(batch, n))
+    return fail(CSM_ERR_WORKSPACE, "workspace smaller than csm_ddref_workspace_size()");
+  if (batch == 0 || n == 0) return CSM_SUCCESS;
+  if (!a || !cos_out || !sin_out || !s_host || !status_host || !ws)
+    return fail(CSM_ERR_ARG, "null pointer argument");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  char* p = static_cast<char*>(ws);
+  auto* bits = reinterpret_cast<unsigned long long*>(p);
+  p += align256(static_cast<size_t>(batch) * 8);
+  auto* dst = reinterpret_cast<int32_t*>(p);
+  p += align256(static_cast<size_t>(batch) * 8);
+  auto* dS = reinterpret_cast<int32_t*>(p);
+  p += align256(static_cast<size_t>(batch) * 8);
+  cudaError_t e = cudaMemsetAsync(bits, 0, static_cast<size_t>(batch) * 8, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dst, 0, static_cast<size_t>(batch) * 4, stream);
+  if (e == cudaSuccess) e = csm::launch_norm1(CSM_F64, a, batch, n, bits, dst, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ddref norm");
+  ++g_launches;
+  std::vector<unsigned long long> hb(static_cast<size_t>(batch));
+  e = cudaMemcpyAsync(hb.data(), bits, hb.size() * 8, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ddref norm readback");
+  // verify.py:495-498: s = ceil(log2(norm / 2^-20)) when norm > 2^-20;
+  // a nan norm compares false (s = 0), an infinite quotient is the
+  // reference's OverflowError.
+  const double cap = 0x1p-20;
+  std::vector<int32_t> hs(hb.size(), 0);
+  int smax = 0;
+  for (size_t b = 0; b < hb.size(); ++b) {
+    double norm;
+    std::memcpy(&norm, &hb[b], 8);
+    status_host[b] = CSM_OK;
+    if (norm > cap) {
+      const double q = norm / cap;
+      if (!csm::finite_d(q)) {
+        status_host[b] = CSM_SELECT_OVERFLOW;
+      } else {
+        hs[b] = csm::ceil_log2_ref(q, csm::host_tables().log2fix);
+      }
+    }
+    s_host[b] = hs[b];
+    smax = std::max(smax, hs[b]);
+  }
+  e = cudaMemcpyAsync(dS, hs.data(), hs.size() * 4, cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ddref s upload");
+  e = csm::ddref_chain(a, dS, smax, cos_out, sin_out, batch, n,
+                       reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255)),
+                       stream, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "ddref chain");
+  // the host vector hs must outlive the async upload
+  e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "ddref chain");
+  return CSM_SUCCESS;
 }
 
 int csm_profile_enable(int on) {

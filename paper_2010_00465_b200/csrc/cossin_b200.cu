@@ -3,4 +3,5 @@
 #include "k0_select.cu"
 #include "fused64.cu"
 #include "tiled.cu"
+#include "ddref.cu"
 #include "abi.cu"

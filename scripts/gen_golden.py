@@ -191,6 +191,42 @@ def gen_extras(rng):
     np.savez_compressed(os.path.join(OUT, "extras.npz"), **out)
 
 
+def gen_ddref(rng):
+    """reference_cos_sin (verify.py:480-521), _dd_matmul (:449-459) and the
+    _dd_const splits (:462-464) of the series coefficients."""
+    from cossinm import verify as V
+    out = {}
+    names = []
+    cases = [("one", np.array([[0.3]])), ("zero4", np.zeros((4, 4)))]
+    for n, target in ((5, 2.0), (16, 30.0), (33, 1e-7), (40, 0.5),
+                      (64, 4.0), (70, 11.0)):
+        m = rng.standard_normal((n, n))
+        cases.append((f"r{n}_{target}", m * (target / cossinm.norm1(m))))
+    nanm = rng.standard_normal((3, 3))
+    nanm[1, 2] = np.nan
+    cases.append(("nan3", nanm))
+    for name, a in cases:
+        res = V.reference_cos_sin(a)
+        out[f"{name}__a"] = a
+        out[f"{name}__cos"] = res.cos_part
+        out[f"{name}__sin"] = res.sin_part
+        out[f"{name}__cost"] = np.array(int(res.cost.total_cost))
+        names.append(name)
+    out["names"] = np.array(names)
+    for n in (1, 7, 40, 65):
+        xh = rng.standard_normal((n, n))
+        xl = xh * 1e-17 * rng.standard_normal((n, n))
+        yh = rng.standard_normal((n, n)) * 10.0 ** rng.uniform(-5, 5, (n, n))
+        yl = yh * 1e-17 * rng.standard_normal((n, n))
+        oh, ol = V._dd_matmul(xh, xl, yh, yl)
+        for k, v in (("xh", xh), ("xl", xl), ("yh", yh), ("yl", yl),
+                     ("oh", oh), ("ol", ol)):
+            out[f"mm{n}__{k}"] = v
+    consts = [V._dd_const(c) for c in V._REF_COS_CORE + V._REF_SIN_CORE]
+    out["consts"] = np.array(consts)
+    np.savez_compressed(os.path.join(OUT, "ddref.npz"), **out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     rng = np.random.default_rng(20100465)
@@ -199,6 +235,7 @@ def main():
     gen_wave(rng)
     gen_norms(rng)
     gen_extras(np.random.default_rng(77))
+    gen_ddref(np.random.default_rng(2010))
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 

@@ -62,3 +62,17 @@ def test_elf_is_sm100a():
     out = subprocess.run([exe, "--list-elf", _lib.lib_path()],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_ddref_series_constants_match_reference(golden_dir):
+    """The library's _dd_const splits (computed with an exact fma residual)
+    equal the reference's Fraction-based ones bit for bit."""
+    import ctypes
+    import os
+    import numpy as np
+    d = np.load(os.path.join(golden_dir, "ddref.npz"))["consts"]  # (14, 2)
+    out = (ctypes.c_double * 28)()
+    assert _lib.lib().csm_ddref_series_consts(out) == 0
+    got = np.array(out[:])
+    want = np.concatenate([d[:7, 0], d[:7, 1], d[7:, 0], d[7:, 1]])
+    assert (got.view(np.uint64) == want.view(np.uint64)).all()

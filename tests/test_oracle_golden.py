@@ -140,3 +140,32 @@ def test_standalone_sines_match_reference(golden_dir):
             got = orc.wave_sin34(a, float(d[f"{name}__t"]))
             assert int(d[f"{name}__cost"]) == 2
         assert rel1(got, d[f"{name}__out"]) <= 1e-14, name
+
+
+def _bits_equal(x, y):
+    """Bitwise equality, any NaN matching any NaN (payloads are platform
+    dependent: x86 and the GPU produce different quiet-NaN encodings)."""
+    x, y = np.asarray(x, np.float64), np.asarray(y, np.float64)
+    if x.shape != y.shape:
+        return False
+    nx, ny = np.isnan(x), np.isnan(y)
+    return bool((nx == ny).all() and
+                (x[~nx].view(np.uint64) == y[~ny].view(np.uint64)).all())
+
+
+def test_ddref_oracle_bit_exact_with_reference(golden_dir):
+    """oracle/ddref_oracle.py against verify.py:417-521 outputs."""
+    from oracle import ddref_oracle as ddo
+    d = _load(golden_dir, "ddref.npz")
+    consts = [ddo.dd_const(c) for c in ddo.COS_CORE + ddo.SIN_CORE]
+    assert _bits_equal(np.array(consts), d["consts"])
+    for n in (1, 7, 40, 65):
+        g = {k: d[f"mm{n}__{k}"] for k in ("xh", "xl", "yh", "yl", "oh", "ol")}
+        oh, ol = ddo.dd_matmul(g["xh"], g["xl"], g["yh"], g["yl"])
+        assert _bits_equal(oh, g["oh"]) and _bits_equal(ol, g["ol"]), n
+    for name in d["names"]:
+        name = str(name)
+        c, s, sc = ddo.reference_cos_sin(d[f"{name}__a"])
+        assert int(d[f"{name}__cost"]) == 7 + 2 * sc, name
+        assert _bits_equal(c, d[f"{name}__cos"]), name
+        assert _bits_equal(s, d[f"{name}__sin"]), name
