@@ -24,7 +24,7 @@ from .api import (
     wave_sin34,
     write_matrix,
 )
-from . import plan
+from . import plan, verify
 from .plan import BatchPlan
 from .records import (
     TAYLOR_TABLE,
