@@ -8,6 +8,7 @@
 // CSM_ERR_NO_DEVICE.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -159,13 +160,25 @@ int check_common(int dtype, int64_t batch, int n, size_t ws_bytes) {
   return CSM_SUCCESS;
 }
 
-// After K/S/status are on the device: run K1 or the tiled chain.
+// Largest n served by the fused kernels (K1: n <= 64, K1c: n <= 128); larger
+// n runs the tiled chain.  CSM_FUSED_MAX=64 (environment) keeps 64 < n <=
+// 128 on the tiled chain, for A/B measurements.
+int fused_max() {
+  static const int v = [] {
+    const char* e = std::getenv("CSM_FUSED_MAX");
+    const int x = e ? std::atoi(e) : 128;
+    return x >= 128 ? 128 : (x >= 64 ? 64 : 0);
+  }();
+  return v;
+}
+
+// After K/S/status are on the device: run K1/K1c or the tiled chain.
 int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, void* s,
                 int64_t batch, int n, const int32_t* K, const int32_t* S, const int32_t* st,
                 const CommonWs& w, cudaStream_t stream) {
   if (n == 0 || batch == 0) return CSM_SUCCESS;
   cudaError_t e;
-  if (n <= 64) {
+  if (n <= fused_max()) {
     e = csm::launch_schedule(K, S, st, batch, w.bins, w.order, stream, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "schedule kernels");
     csm::prof_begin(stream);

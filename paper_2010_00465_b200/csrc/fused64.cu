@@ -1,5 +1,7 @@
 // fused64.cu -- K1: the whole cos/sin (or wave) pipeline for n <= 64 with
-// every intermediate resident in shared memory.
+// every intermediate resident in shared memory, and K1c: the same program
+// for 64 < n <= 128 on a 4-CTA thread-block cluster whose distributed shared
+// memory holds the 128 x 128 slots as four 32-row bands.
 //
 // One persistent CTA per SM (256 threads, 8 warps) walks a static snake
 // schedule over the matrices sorted by cost k + 2s (K0 builds it), so the
@@ -27,6 +29,16 @@
 // and sin = 2^-s (A sc) are exact power-of-two rescalings of the
 // accumulators (driver.py:115); the wave family materialises y = (t')^2 A
 // (schemes.py:424) in place.
+//
+// K1c (CL = 4): CTA q of the cluster owns rows [32q, 32q+32) of every
+// slot (7 x 32 KiB, the same footprint as K1).  A product band
+// out[32q.., :] = L[32q.., :] R reads L from the CTA's own band and R, the
+// full matrix, through distributed shared memory (generic loads on
+// __cluster_map_shared_rank pointers); the per-step barrier becomes a
+// cluster barrier (release/acquire).  Each warp computes a 32 x 16 tile so
+// every R element crosses the cluster once per product: 96 KiB per CTA per
+// 2 x 32 x 128^2 flop, 11.7 B/clk at the DMMA rate against a measured
+// 14-15 B/clk DSMEM bandwidth (tools/dsmem_bw.cu, tools/dsmem_bulk.cu).
 //
 // Reference mapping: chains schemes.py:264-361, trig use :376-395, wave use
 // :411-430, scaling driver.py:115/:139, doubling driver.py:91-98.
@@ -61,12 +73,21 @@ __device__ __forceinline__ int& trace_count() {
 #endif
 #define TRACE_T(tag) CSM_TRACE_EV(tag, static_cast<unsigned long long>(clock64()))
 
-constexpr int NP = 64;
-constexpr int SLOT = NP * NP;  // doubles per slot
+// Geometry: CL = CTAs per matrix (1: K1, 4: K1c).  BAND rows of NP columns
+// per CTA and slot; each warp owns an (8 MI) x (8 NI) accumulator tile.
+template <int CL> struct Geo;
+template <> struct Geo<1> {
+  static constexpr int NP = 64, BAND = 64, MI = 2, NI = 4;
+};
+template <> struct Geo<4> {
+  static constexpr int NP = 128, BAND = 32, MI = 4, NI = 2;
+};
+constexpr int SLOT = 4096;  // doubles per slot band (64 x 64 or 32 x 128)
 constexpr int NSLOTS = 7;
 constexpr int THREADS = 256;
 
 __host__ __device__ constexpr int swz_f(int r) { return ((r & 1) << 2) | (r & 2); }
+template <int NP>
 __device__ __forceinline__ int swz(int r, int c) {
   return r * NP + 2 * ((c >> 1) ^ swz_f(r)) + (c & 1);
 }
@@ -172,69 +193,157 @@ __constant__ Chain kChains[7] = {
 #undef S_
 
 // ---------------------------------------------------------------------------
-// Per-thread geometry: warp w owns rows [16(w/2), +16) x cols [32(w%2), +32)
-// = 2 x 4 DMMA tiles; lane = 4g + t.
+// Per-thread geometry, lane = 4g + t.  K1: warp w owns rows [16(w/2), +16) x
+// cols [32(w%2), +32) = 2 x 4 DMMA tiles.  K1c: warp w owns the band's 32
+// rows x cols [16w, +16) = 4 x 2 tiles.
 
+template <int CL>
 struct Lane {
-  int rb, cb, g, t;
-  int aoff[2][4];  // A-fragment element offsets: row mi, chunk q (+16 m)
-  int boff[4];     // B-fragment element offsets for tile ni (+64 kk)
+  int rb, cb, g, t, row0;  // row0: first global row of this CTA's band
+  int aoff[Geo<CL>::MI][4];  // A-fragment offsets: tile mi, chunk q (+16 m)
+  int boff[Geo<CL>::NI];     // B-fragment offsets for tile ni (+NP kk)
 };
 
-__device__ __forceinline__ void make_lane(Lane& ln) {
+template <int CL>
+__device__ __forceinline__ void make_lane(Lane<CL>& ln, int rank) {
+  constexpr int NP = Geo<CL>::NP, MI = Geo<CL>::MI, NI = Geo<CL>::NI;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  ln.rb = (warp >> 1) * 16;
-  ln.cb = (warp & 1) * 32;
+  if (CL == 1) {
+    ln.rb = (warp >> 1) * 16;
+    ln.cb = (warp & 1) * 32;
+  } else {
+    ln.rb = 0;
+    ln.cb = warp * 16;
+  }
+  ln.row0 = rank * Geo<CL>::BAND;
   ln.g = lane >> 2;
   ln.t = lane & 3;
   // A: element (r = rb + 8 mi + g, c = 4 j + t), j = 4 m + q
-  //    -> r*64 + 4 ((j) ^ h) + t with h = f(g)/2 (affects the low 2 bits of j)
+  //    -> r*NP + 4 ((j) ^ h) + t with h = f(g)/2 (affects the low 2 bits of j)
   const int h = swz_f(ln.g) >> 1;
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       ln.aoff[mi][q] = (ln.rb + mi * 8 + ln.g) * NP + 4 * (q ^ h) + ln.t;
-  // B: element (r = kk + t, c = cb + 8 ni + g) -> kk*64 + swz(t, c) (f(r) = f(t))
+  // B: element (r = kk + t, c = cb + 8 ni + g) -> kk*NP + swz(t, c) (f(r) = f(t))
 #pragma unroll
-  for (int ni = 0; ni < 4; ++ni) ln.boff[ni] = swz(ln.t, ln.cb + ni * 8 + ln.g);
+  for (int ni = 0; ni < NI; ++ni) ln.boff[ni] = swz<NP>(ln.t, ln.cb + ni * 8 + ln.g);
 }
 
-typedef double Acc[2][4][2];
+typedef double Acc[8][2];  // 8 DMMA tiles x 2 accumulators (p = mi * NI + ni)
 
 __device__ __forceinline__ void zero(Acc& a) {
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) a[i][j][0] = a[i][j][1] = 0.0;
+  for (int i = 0; i < 8; ++i) a[i][0] = a[i][1] = 0.0;
 }
 
-// acc = L * R (and acc2 = L2 * R when DUAL), full 64-deep contraction.
-template <bool DUAL>
+// Cross-CTA view of a slot: K1 reads R from its own shared memory; K1c maps
+// the same slot of each cluster rank (rows [32 o, 32 o + 32)).
+// K1c walks the k bands starting at its own rank (p[i] = band (rank + i) %
+// CL, lcol[i] its column offset in L), so the four CTAs of a cluster read
+// four different owners at any time instead of all hammering one.
+template <int CL>
+struct RView {
+  const double* p[CL];
+  int lcol[CL];
+};
+template <int CL>
+__device__ __forceinline__ RView<CL> rview(const double* R, int rank) {
+  RView<CL> v;
+  if constexpr (CL == 1) {
+    v.p[0] = R;
+    v.lcol[0] = 0;
+  } else {
+#pragma unroll
+    for (int i = 0; i < CL; ++i) {
+      const int o = (rank + i) & (CL - 1);
+      // own band (i = 0) through the local shared window: no cluster
+      // round trip for the k-steps right after the barrier
+      v.p[i] = i == 0 ? R
+                      : static_cast<const double*>(
+                            __cluster_map_shared_rank(const_cast<double*>(R), o));
+      v.lcol[i] = Geo<CL>::BAND * o;  // L columns of band o (swizzle keeps 8-chunk blocks)
+    }
+  }
+  return v;
+}
+
+// acc = L * R (and acc2 = L2 * R when DUAL), full NP-deep contraction; L
+// and L2 are this CTA's bands, R the whole slot.
+template <int CL, bool DUAL>
 __device__ __forceinline__ void gemm(const double* __restrict__ L,
                                      const double* __restrict__ L2,
-                                     const double* __restrict__ R, Acc& acc,
-                                     Acc& acc2, const Lane& ln) {
+                                     const RView<CL>& R, Acc& acc, Acc& acc2,
+                                     const Lane<CL>& ln) {
+  constexpr int NP = Geo<CL>::NP, BAND = Geo<CL>::BAND, MI = Geo<CL>::MI, NI = Geo<CL>::NI;
   zero(acc);
   if (DUAL) zero(acc2);
+  if constexpr (CL > 1) {
+    // R arrives over DSMEM (hundreds of cycles): keep PF k-steps of B
+    // fragments in flight in a register ring.
+    constexpr int NK = NP / 4;
+#ifndef CSM_K1C_PF
+#define CSM_K1C_PF 6
+#endif
+    constexpr int PF = CSM_K1C_PF;
+    double ring[PF][NI];
+#pragma unroll
+    for (int d = 0; d < PF; ++d) {
+      const double* Rk = R.p[(4 * d) / BAND] + ((4 * d) % BAND) * NP;
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) ring[d][ni] = Rk[ln.boff[ni]];
+    }
+#pragma unroll
+    for (int j = 0; j < NK; ++j) {
+      // k-step j of the rotated order: band j / 8, local k-step j % 8
+      const int bi = (4 * j) / BAND, jl = j % (BAND / 4), m = jl >> 2, q = jl & 3;
+      double b[NI];
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) b[ni] = ring[j % PF][ni];
+      if (j + PF < NK) {
+        const int kn = 4 * (j + PF);
+        const double* Rk = R.p[kn / BAND] + (kn % BAND) * NP;
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) ring[j % PF][ni] = Rk[ln.boff[ni]];
+      }
+      const double* Lb = L + R.lcol[bi];
+      const double* L2b = DUAL ? L2 + R.lcol[bi] : nullptr;
+      double a[MI], a2[MI];
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) {
+        a[mi] = Lb[ln.aoff[mi][q] + 16 * m];
+        if (DUAL) a2[mi] = L2b[ln.aoff[mi][q] + 16 * m];
+      }
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          dmma(acc[mi * NI + ni], a[mi], b[ni]);
+          if (DUAL) dmma(acc2[mi * NI + ni], a2[mi], b[ni]);
+        }
+    }
+  } else {
 #pragma unroll
   for (int kk = 0; kk < NP; kk += 4) {
     const int j = kk >> 2, m = j >> 2, q = j & 3;
-    double a[2], a2[2], b[4];
+    const double* Rk = R.p[kk / BAND] + (kk % BAND) * NP;
+    double a[MI], a2[MI], b[NI];
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
+    for (int mi = 0; mi < MI; ++mi) {
       a[mi] = L[ln.aoff[mi][q] + 16 * m];
       if (DUAL) a2[mi] = L2[ln.aoff[mi][q] + 16 * m];
     }
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) b[ni] = R[ln.boff[ni] + NP * kk];
+    for (int ni = 0; ni < NI; ++ni) b[ni] = Rk[ln.boff[ni]];
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
+    for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        dmma(acc[mi][ni], a[mi], b[ni]);
-        if (DUAL) dmma(acc2[mi][ni], a2[mi], b[ni]);
+      for (int ni = 0; ni < NI; ++ni) {
+        dmma(acc[mi * NI + ni], a[mi], b[ni]);
+        if (DUAL) dmma(acc2[mi * NI + ni], a2[mi], b[ni]);
       }
+  }
   }
 }
 
@@ -243,6 +352,27 @@ __device__ __forceinline__ double2 ld2(const double* p, int off) {
 }
 __device__ __forceinline__ void st2(double* p, int off, double x, double y) {
   *reinterpret_cast<double2*>(p + off) = make_double2(x, y);
+}
+
+// Barrier between dependent steps: the CTA (K1) or the whole cluster (K1c,
+// release/acquire so band writes are visible to the peers' DSMEM loads).
+template <int CL>
+__device__ __forceinline__ void step_sync() {
+  if constexpr (CL == 1) {
+    __syncthreads();
+  } else {
+#ifdef CSM_CLUSTER_RELAXED
+    // experiment: CTA barrier (band writes performed in this SM's shared
+    // memory) + relaxed cluster arrive, avoiding the GPU-scope MEMBAR that
+    // a .release arrive compiles to
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+#else
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+#endif
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -257,82 +387,84 @@ struct EpiArgs {
   int n;
 };
 
-// Store one accumulator-layout pair (r, c), (r, c+1) of an n x n result.
-template <typename TOut>
-__device__ __forceinline__ void gstore(TOut* __restrict__ dst, int n, int r, int c,
+// Store one accumulator-layout pair (rg, c), (rg, c+1) of an n x n result
+// (rg = global row).
+template <int NP, typename TOut>
+__device__ __forceinline__ void gstore(TOut* __restrict__ dst, int n, int rg, int c,
                                        double v0, double v1) {
-#ifdef CSM_NO_STORE
-  if (v0 != 12345.678) return;  // experiment: measure without output traffic
-#endif
   if (n == NP) {
     if constexpr (sizeof(TOut) == 8)
-      *reinterpret_cast<double2*>(reinterpret_cast<double*>(dst) + r * NP + c) =
+      *reinterpret_cast<double2*>(reinterpret_cast<double*>(dst) + rg * NP + c) =
           make_double2(v0, v1);
     else
-      *reinterpret_cast<float2*>(reinterpret_cast<float*>(dst) + r * NP + c) =
+      *reinterpret_cast<float2*>(reinterpret_cast<float*>(dst) + rg * NP + c) =
           make_float2(static_cast<float>(v0), static_cast<float>(v1));
-  } else if (r < n) {
-    if (c < n) dst[r * n + c] = static_cast<TOut>(v0);
-    if (c + 1 < n) dst[r * n + c + 1] = static_cast<TOut>(v1);
+  } else if (rg < n) {
+    if (c < n) dst[rg * n + c] = static_cast<TOut>(v0);
+    if (c + 1 < n) dst[rg * n + c + 1] = static_cast<TOut>(v1);
   }
 }
 
-template <typename TOut>
-__device__ __forceinline__ void put(const EpiArgs<TOut>& E, int q, int r, int c, int off,
+template <int NP, typename TOut>
+__device__ __forceinline__ void put(const EpiArgs<TOut>& E, int q, int rg, int c, int off,
                                     double v0, double v1) {
   st2(E.o[q], off, v0, v1);
-  if (E.g[q]) gstore(E.g[q], E.n, r, c, v0, v1);
+  if (E.g[q]) gstore<NP>(E.g[q], E.n, rg, c, v0, v1);
 }
 
 // Run BODY on each of the thread's 8 owned pairs (accumulator layout) with
-// r, c, off (swizzled), I0/I1 (identity entries) and p0/p1 (accumulator).
+// P (tile index), r (band row), rg (global row), c, off (swizzled), I0/I1
+// (identity entries) and p0/p1 (accumulator).
 #define FOR_PAIRS(...)                                                        \
-  _Pragma("unroll") for (int mi = 0; mi < 2; ++mi) {                          \
-    _Pragma("unroll") for (int ni = 0; ni < 4; ++ni) {                        \
+  _Pragma("unroll") for (int mi = 0; mi < Geo<CL>::MI; ++mi) {                \
+    _Pragma("unroll") for (int ni = 0; ni < Geo<CL>::NI; ++ni) {              \
+      const int P = mi * Geo<CL>::NI + ni;                                    \
       const int r = ln.rb + mi * 8 + ln.g;                                    \
+      const int rg = ln.row0 + r;                                             \
       const int c = ln.cb + ni * 8 + 2 * ln.t;                                \
-      const int off = swz(r, c);                                              \
-      const double I0 = (r == c) ? 1.0 : 0.0, I1 = (r == c + 1) ? 1.0 : 0.0;  \
-      const double p0 = acc[mi][ni][0], p1 = acc[mi][ni][1];                  \
+      const int off = swz<Geo<CL>::NP>(r, c);                                 \
+      const double I0 = (rg == c) ? 1.0 : 0.0, I1 = (rg == c + 1) ? 1.0 : 0.0; \
+      const double p0 = acc[P][0], p1 = acc[P][1];                            \
       (void)I0; (void)I1; (void)off;                                          \
       __VA_ARGS__                                                             \
     }                                                                         \
   }
 
-template <typename TOut>
+template <int CL, typename TOut>
 __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const Acc& acc,
-                                         const Acc& acc2, Acc& keep, const Lane& ln) {
+                                         const Acc& acc2, Acc& keep, const Lane<CL>& ln) {
+  constexpr int NP = Geo<CL>::NP;
   const double* x = dTables.x8;  // x[0] = x1
   const double* z8 = dTables.z8;
   const double(*a)[4] = dTables.a12;  // a[j-1][i]
   const double* z = dTables.z12;
   switch (epi) {
     case E_SCALED:
-      FOR_PAIRS(put(E, 0, r, c, off, E.scale * p0, E.scale * p1);)
+      FOR_PAIRS(put<NP>(E, 0, rg, c, off, E.scale * p0, E.scale * p1);)
       break;
     case E_DEG2:
       FOR_PAIRS({
           const double2 y = ld2(E.in[0], off);
-          put(E, 0, r, c, off, fma(1.0 / 24.0, p0, fma(-0.5, y.x, I0)),
+          put<NP>(E, 0, rg, c, off, fma(1.0 / 24.0, p0, fma(-0.5, y.x, I0)),
               fma(1.0 / 24.0, p1, fma(-0.5, y.y, I1)));
-          put(E, 1, r, c, off, fma(1.0 / 120.0, p0, fma(-1.0 / 6.0, y.x, I0)),
+          put<NP>(E, 1, rg, c, off, fma(1.0 / 120.0, p0, fma(-1.0 / 6.0, y.x, I0)),
               fma(1.0 / 120.0, p1, fma(-1.0 / 6.0, y.y, I1)));
         })
       break;
     case E_DEG4A:
       FOR_PAIRS({
           const double2 y = ld2(E.in[0], off);
-          put(E, 0, r, c, off, p0, p1);
-          put(E, 1, r, c, off, fma(1.0 / 40320.0, p0, (-1.0 / 720.0) * y.x),
+          put<NP>(E, 0, rg, c, off, p0, p1);
+          put<NP>(E, 1, rg, c, off, fma(1.0 / 40320.0, p0, (-1.0 / 720.0) * y.x),
               fma(1.0 / 40320.0, p1, (-1.0 / 720.0) * y.y));
         })
       break;
     case E_DEG4B:
       FOR_PAIRS({
           const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
-          put(E, 0, r, c, off, p0 + fma(1.0 / 24.0, y2.x, fma(-0.5, y.x, I0)),
+          put<NP>(E, 0, rg, c, off, p0 + fma(1.0 / 24.0, y2.x, fma(-0.5, y.x, I0)),
               p1 + fma(1.0 / 24.0, y2.y, fma(-0.5, y.y, I1)));
-          put(E, 1, r, c, off,
+          put<NP>(E, 1, rg, c, off,
               fma(720.0 / 5040.0, p0, fma(1.0 / 120.0, y2.x, fma(-1.0 / 6.0, y.x, I0))),
               fma(720.0 / 5040.0, p1, fma(1.0 / 120.0, y2.y, fma(-1.0 / 6.0, y.y, I1))));
         })
@@ -340,20 +472,20 @@ __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const 
     case E_DEG4W1:
       FOR_PAIRS({
           const double2 y = ld2(E.in[0], off);
-          put(E, 0, r, c, off, p0, p1);
-          put(E, 1, r, c, off, fma(1.0 / 40320.0, p0, (-1.0 / 720.0) * y.x),
+          put<NP>(E, 0, rg, c, off, p0, p1);
+          put<NP>(E, 1, rg, c, off, fma(1.0 / 40320.0, p0, (-1.0 / 720.0) * y.x),
               fma(1.0 / 40320.0, p1, (-1.0 / 720.0) * y.y));
-          put(E, 2, r, c, off, fma(1.0 / 362880.0, p0, (-1.0 / 5040.0) * y.x),
+          put<NP>(E, 2, rg, c, off, fma(1.0 / 362880.0, p0, (-1.0 / 5040.0) * y.x),
               fma(1.0 / 362880.0, p1, (-1.0 / 5040.0) * y.y));
         })
       break;
     case E_DEG4W2:
       FOR_PAIRS({
           const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
-          const double q0 = acc2[mi][ni][0], q1 = acc2[mi][ni][1];
-          put(E, 0, r, c, off, p0 + fma(1.0 / 24.0, y2.x, fma(-0.5, y.x, I0)),
+          const double q0 = acc2[P][0], q1 = acc2[P][1];
+          put<NP>(E, 0, rg, c, off, p0 + fma(1.0 / 24.0, y2.x, fma(-0.5, y.x, I0)),
               p1 + fma(1.0 / 24.0, y2.y, fma(-0.5, y.y, I1)));
-          put(E, 1, r, c, off,
+          put<NP>(E, 1, rg, c, off,
               E.scale * (q0 + fma(1.0 / 120.0, y2.x, fma(-1.0 / 6.0, y.x, I0))),
               E.scale * (q1 + fma(1.0 / 120.0, y2.y, fma(-1.0 / 6.0, y.y, I1))));
         })
@@ -361,16 +493,16 @@ __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const 
     case E_DEG8A:
       FOR_PAIRS({
           const double2 y = ld2(E.in[0], off);
-          put(E, 0, r, c, off, p0, p1);
-          put(E, 1, r, c, off, fma(x[1], p0, x[0] * y.x), fma(x[1], p1, x[0] * y.y));
+          put<NP>(E, 0, rg, c, off, p0, p1);
+          put<NP>(E, 1, rg, c, off, fma(x[1], p0, x[0] * y.x), fma(x[1], p1, x[0] * y.y));
         })
       break;
     case E_DEG8B:
       FOR_PAIRS({
           const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
-          put(E, 0, r, c, off, p0, p1);
-          put(E, 1, r, c, off, fma(x[2], y2.x, p0), fma(x[2], y2.y, p1));
-          put(E, 2, r, c, off, fma(x[6], p0, fma(x[5], y2.x, fma(x[4], y.x, x[3] * I0))),
+          put<NP>(E, 0, rg, c, off, p0, p1);
+          put<NP>(E, 1, rg, c, off, fma(x[2], y2.x, p0), fma(x[2], y2.y, p1));
+          put<NP>(E, 2, rg, c, off, fma(x[6], p0, fma(x[5], y2.x, fma(x[4], y.x, x[3] * I0))),
               fma(x[6], p1, fma(x[5], y2.y, fma(x[4], y.y, x[3] * I1))));
         })
       break;
@@ -384,20 +516,20 @@ __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const 
           const double n0 = fma(z8[8], c0, fma(z8[7], p8.x, fma(z8[6], y2.x, fma(z8[5], y.x, z8[5] * I0))));
           const double n1 = fma(z8[8], c1, fma(z8[7], p8.y, fma(z8[6], y2.y, fma(z8[5], y.y, z8[5] * I1))));
           // sin base = z0 I + z1 y + z2 y2 + z3 p8 + z4 cos
-          keep[mi][ni][0] = fma(z8[4], c0, fma(z8[3], p8.x, fma(z8[2], y2.x, fma(z8[1], y.x, z8[0] * I0))));
-          keep[mi][ni][1] = fma(z8[4], c1, fma(z8[3], p8.y, fma(z8[2], y2.y, fma(z8[1], y.y, z8[0] * I1))));
-          put(E, 0, r, c, off, c0, c1);
-          put(E, 1, r, c, off, n0, n1);  // may overwrite y at this thread's own pair
+          keep[P][0] = fma(z8[4], c0, fma(z8[3], p8.x, fma(z8[2], y2.x, fma(z8[1], y.x, z8[0] * I0))));
+          keep[P][1] = fma(z8[4], c1, fma(z8[3], p8.y, fma(z8[2], y2.y, fma(z8[1], y.y, z8[0] * I1))));
+          put<NP>(E, 0, rg, c, off, c0, c1);
+          put<NP>(E, 1, rg, c, off, n0, n1);  // may overwrite y at this thread's own pair
         })
       break;
     case E_KEEP:
-      FOR_PAIRS(put(E, 0, r, c, off, E.scale * (keep[mi][ni][0] + p0), E.scale * (keep[mi][ni][1] + p1));)
+      FOR_PAIRS(put<NP>(E, 0, rg, c, off, E.scale * (keep[P][0] + p0), E.scale * (keep[P][1] + p1));)
       break;
     case E_DEG12B:
       FOR_PAIRS({
           const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
-          put(E, 0, r, c, off, p0, p1);
-          put(E, 1, r, c, off, fma(a[3][3], p0, fma(a[3][2], y2.x, fma(a[3][1], y.x, a[3][0] * I0))),
+          put<NP>(E, 0, rg, c, off, p0, p1);
+          put<NP>(E, 1, rg, c, off, fma(a[3][3], p0, fma(a[3][2], y2.x, fma(a[3][1], y.x, a[3][0] * I0))),
               fma(a[3][3], p1, fma(a[3][2], y2.y, fma(a[3][1], y.y, a[3][0] * I1))));
         })
       break;
@@ -409,8 +541,8 @@ __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const 
           const double m1 = fma(a[2][3], y3.y, fma(a[2][2], y2.y, fma(a[2][1], y.y, a[2][0] * I1))) + p1;
           const double l0 = fma(a[1][3], y3.x, fma(a[1][2], y2.x, fma(a[1][1], y.x, a[1][0] * I0))) + m0;
           const double l1 = fma(a[1][3], y3.y, fma(a[1][2], y2.y, fma(a[1][1], y.y, a[1][0] * I1))) + m1;
-          put(E, 0, r, c, off, m0, m1);
-          put(E, 1, r, c, off, l0, l1);
+          put<NP>(E, 0, rg, c, off, m0, m1);
+          put<NP>(E, 1, rg, c, off, l0, l1);
         })
       break;
     case E_DEG12D:
@@ -421,10 +553,10 @@ __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const 
           const double c1 = fma(a[0][3], y3.y, fma(a[0][2], y2.y, fma(a[0][1], y.y, a[0][0] * I1))) + p1;
           const double n0 = fma(z[11], c0, fma(z[10], md.x, fma(z[9], y3.x, fma(z[8], y2.x, fma(z[7], y.x, z[6] * I0)))));
           const double n1 = fma(z[11], c1, fma(z[10], md.y, fma(z[9], y3.y, fma(z[8], y2.y, fma(z[7], y.y, z[6] * I1)))));
-          keep[mi][ni][0] = fma(z[5], c0, fma(z[4], md.x, fma(z[3], y3.x, fma(z[2], y2.x, fma(z[1], y.x, z[0] * I0)))));
-          keep[mi][ni][1] = fma(z[5], c1, fma(z[4], md.y, fma(z[3], y3.y, fma(z[2], y2.y, fma(z[1], y.y, z[0] * I1)))));
-          put(E, 0, r, c, off, c0, c1);
-          put(E, 1, r, c, off, n0, n1);  // may overwrite y at this thread's own pair
+          keep[P][0] = fma(z[5], c0, fma(z[4], md.x, fma(z[3], y3.x, fma(z[2], y2.x, fma(z[1], y.x, z[0] * I0)))));
+          keep[P][1] = fma(z[5], c1, fma(z[4], md.y, fma(z[3], y3.y, fma(z[2], y2.y, fma(z[1], y.y, z[0] * I1)))));
+          put<NP>(E, 0, rg, c, off, c0, c1);
+          put<NP>(E, 1, rg, c, off, n0, n1);  // may overwrite y at this thread's own pair
         })
       break;
     default:
@@ -435,36 +567,43 @@ __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const 
 // s doubling steps (driver.py:91-98): S <- 2 S C (old C), C <- 2 C C - I as
 // one dual product [S; C] * C into the two free slots, then swap; the last
 // step writes the results straight from registers to global memory.
-template <typename TOut>
+
+// s doubling steps (driver.py:91-98): S <- 2 S C (old C), C <- 2 C C - I as
+// one dual product [S; C] * C into the two free slots, then swap; the last
+// step writes the results straight from registers to global memory.
+template <int CL, typename TOut>
 __device__ __forceinline__ void doubling(double*& C, double*& S, double*& F1,
-                                         double*& F2, int steps, const Lane& ln,
+                                         double*& F2, int steps, const Lane<CL>& ln,
                                          TOut* cdst, TOut* sdst, int n) {
+  constexpr int NP = Geo<CL>::NP;
   Acc sc, cc;
   for (int it = 0; it < steps; ++it) {
     TRACE_T(6);
-    gemm<true>(S, C, C, sc, cc, ln);
+    gemm<CL, true>(S, C, rview<CL>(C, ln.row0 / Geo<CL>::BAND), sc, cc, ln);
     const bool last = it == steps - 1;
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
+    for (int mi = 0; mi < Geo<CL>::MI; ++mi)
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
+      for (int ni = 0; ni < Geo<CL>::NI; ++ni) {
+        const int P = mi * Geo<CL>::NI + ni;
         const int r = ln.rb + mi * 8 + ln.g;
+        const int rg = ln.row0 + r;
         const int c = ln.cb + ni * 8 + 2 * ln.t;
-        const double s0 = 2.0 * sc[mi][ni][0], s1 = 2.0 * sc[mi][ni][1];
-        const double c0 = fma(2.0, cc[mi][ni][0], (r == c) ? -1.0 : 0.0);
-        const double c1 = fma(2.0, cc[mi][ni][1], (r == c + 1) ? -1.0 : 0.0);
+        const double s0 = 2.0 * sc[P][0], s1 = 2.0 * sc[P][1];
+        const double c0 = fma(2.0, cc[P][0], (rg == c) ? -1.0 : 0.0);
+        const double c1 = fma(2.0, cc[P][1], (rg == c + 1) ? -1.0 : 0.0);
         if (last) {
-          gstore(sdst, n, r, c, s0, s1);
-          gstore(cdst, n, r, c, c0, c1);
+          gstore<NP>(sdst, n, rg, c, s0, s1);
+          gstore<NP>(cdst, n, rg, c, c0, c1);
         } else {
-          const int off = swz(r, c);
+          const int off = swz<NP>(r, c);
           st2(F1, off, s0, s1);
           st2(F2, off, c0, c1);
         }
       }
     TRACE_T(7);
     if (!last) {
-      __syncthreads();
+      step_sync<CL>();
       double* t = S; S = F1; F1 = t;
       t = C; C = F2; F2 = t;
     }
@@ -473,6 +612,7 @@ __device__ __forceinline__ void doubling(double*& C, double*& S, double*& F1,
 
 // ---------------------------------------------------------------------------
 // Global <-> shared movement.
+
 
 __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
   unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -500,73 +640,13 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // Load matrix (n x n, row-major) into slot dst: async for fp64 input.  For
 // n < 64 the padding is rewritten with zeros (the slot may hold a previous
 // chain's intermediate).
-template <typename TIn>
-__device__ __forceinline__ void load_matrix(double* dst, const TIn* __restrict__ src,
-                                            int n) {
-  const int tid = threadIdx.x;
-  if (n < NP) {
-    for (int p = tid; p < SLOT; p += THREADS) {
-      const int r = p >> 6, c = p & 63;
-      if (r >= n || c >= n) dst[swz(r, c)] = 0.0;
-    }
-  }
-  if constexpr (sizeof(TIn) == 8) {
-    const double* s = reinterpret_cast<const double*>(src);
-    if (n == NP) {
-#pragma unroll
-      for (int i = 0; i < (NP * NP / 2) / THREADS; ++i) {
-        const int p = tid + i * THREADS;
-        const int r = p >> 5, c = (p & 31) * 2;
-        cp_async16(dst + swz(r, c), s + r * NP + c);
-      }
-    } else if ((n & 1) == 0) {
-      const int half = n >> 1;
-      for (int p = tid; p < n * half; p += THREADS) {
-        const int r = p / half, c = (p - r * half) * 2;
-        cp_async16(dst + swz(r, c), s + static_cast<size_t>(r) * n + c);
-      }
-    } else {
-      for (int p = tid; p < n * n; p += THREADS) {
-        const int r = p / n, c = p - r * n;
-        cp_async8(dst + swz(r, c), s + p);
-      }
-    }
-    cp_async_commit();
-  } else {
-    for (int p = tid; p < n * n; p += THREADS) {
-      const int r = p / n, c = p - r * n;
-      dst[swz(r, c)] = static_cast<double>(src[p]);
-    }
-  }
-}
-
+// NaN-fill this CTA's rows [r0, r0 + rows) of an n x n output.
 template <typename TOut>
-__device__ __forceinline__ void store_matrix(TOut* __restrict__ dst, const double* src,
-                                             int n) {
-  const int tid = threadIdx.x;
-  if (sizeof(TOut) == 8 && n == NP) {
-#pragma unroll
-    for (int i = 0; i < (NP * NP / 2) / THREADS; ++i) {
-      const int p = tid + i * THREADS;
-      const int r = p >> 5, c = (p & 31) * 2;
-      *reinterpret_cast<double2*>(reinterpret_cast<double*>(dst) + r * NP + c) =
-          ld2(src, swz(r, c));
-    }
-  } else {
-    for (int p = tid; p < n * n; p += THREADS) {
-      const int r = p / n, c = p - r * n;
-      dst[p] = static_cast<TOut>(src[swz(r, c)]);
-    }
-  }
-}
-
-template <typename TOut>
-__device__ __forceinline__ void store_nan(TOut* __restrict__ dst, int n) {
-  for (int p = threadIdx.x; p < n * n; p += THREADS)
+__device__ __forceinline__ void store_nan(TOut* __restrict__ dst, int n, int r0, int rows) {
+  const int lo = r0 * n, hi = min(n, r0 + rows) * n;
+  for (int p = lo + threadIdx.x; p < hi; p += THREADS)
     dst[p] = static_cast<TOut>(__longlong_as_double(0x7ff8000000000000ll));
 }
-
-// ---------------------------------------------------------------------------
 
 // ---------------------------------------------------------------------------
 // Input staging: the next matrix lands, in its natural row-major layout, in
@@ -606,16 +686,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
-template <typename TIn, typename TOut, bool WAVE>
+template <int CL, typename TIn, typename TOut, bool WAVE>
 __global__ void __launch_bounds__(THREADS, 1)
 fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
-               TOut* __restrict__ Sout, const double* __restrict__ T,
-               const int32_t* __restrict__ K, const int32_t* __restrict__ Sx,
-               const int32_t* __restrict__ ST, const int32_t* __restrict__ order,
-               int64_t batch, int n, int tma) {
+             TOut* __restrict__ Sout, const double* __restrict__ T,
+             const int32_t* __restrict__ K, const int32_t* __restrict__ Sx,
+             const int32_t* __restrict__ ST, const int32_t* __restrict__ order,
+             int64_t batch, int n, int tma) {
+  constexpr int NP = Geo<CL>::NP, BAND = Geo<CL>::BAND;
   extern __shared__ __align__(128) double smem[];
-  // Static schedule: CTA c takes order[] positions c, 2G-1-c, 2G+c, ... (a
-  // snake over the cost-sorted list).  Thread 0 stages the matrix ids two
+  // Static schedule: cluster c takes order[] positions c, 2G-1-c, 2G+c, ...
+  // (a snake over the cost-sorted list).  Thread 0 stages the matrix ids two
   // turns ahead and the next matrix's (k, s, status, t) by 4/8-byte
   // cp.async into small rings, so no global latency is ever exposed.
   __shared__ int sh_b[4];
@@ -624,17 +705,23 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
   __shared__ __align__(8) uint64_t sh_bar;
   __shared__ Chain sh_chain[7];
   const int tid = threadIdx.x;
-  const int G = gridDim.x, cta = blockIdx.x;
-  Lane ln;
-  make_lane(ln);
+  const int G = gridDim.x / CL, cta = blockIdx.x / CL, rank = blockIdx.x % CL;
+  Lane<CL> ln;
+  make_lane(ln, rank);
   const size_t nn = static_cast<size_t>(n) * n;
   double* const land = smem + 6 * SLOT;
-  const unsigned in_bytes = static_cast<unsigned>(nn * sizeof(TIn));
+  // this CTA's input band: rows [row0, row0 + rows_here) of each matrix
+  const int row0 = ln.row0;
+  const int rows_here = max(0, min(BAND, n - row0));
+  const size_t band_off = static_cast<size_t>(row0) * n;
+  const unsigned in_bytes = static_cast<unsigned>(rows_here * n * sizeof(TIn));
+  const bool tma_here = tma && rows_here > 0 && (in_bytes % 16) == 0;
   auto posof = [&](int i) -> long long {
     return static_cast<long long>(i) * G + ((i & 1) ? (G - 1 - cta) : cta);
   };
-  auto prefetch = [&](int b) {  // thread 0 only: next input -> slot 6
-    if (tma && b >= 0) tma_load_1d(land, Ain + static_cast<size_t>(b) * nn, in_bytes, &sh_bar);
+  auto prefetch = [&](int b) {  // thread 0 only: next input band -> slot 6
+    if (tma_here && b >= 0)
+      tma_load_1d(land, Ain + static_cast<size_t>(b) * nn + band_off, in_bytes, &sh_bar);
   };
 
 #ifdef CSM_TRACE
@@ -662,7 +749,7 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
     __syncthreads();
     const int b = sh_b[it & 3], bn = sh_b[(it + 1) & 3];
     if (b < 0) break;
-    if (tma) mbar_wait(&sh_bar, it & 1);  // this matrix's input has landed
+    if (tma_here) mbar_wait(&sh_bar, it & 1);  // this matrix's band has landed
     const int k = sh_meta[it & 1][0], s = sh_meta[it & 1][1], status = sh_meta[it & 1][2];
     const double tcur = sh_t[it & 1];
     TRACE_T(1);
@@ -679,17 +766,17 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
       }
       cp_async_commit();
     }
-    const TIn* src = Ain + static_cast<size_t>(b) * nn;
-    if (!tma) {  // odd n: synchronous staging copy
-      for (int p = tid; p < static_cast<int>(nn); p += THREADS)
+    const TIn* src = Ain + static_cast<size_t>(b) * nn + band_off;
+    if (!tma_here && rows_here > 0) {  // unaligned band: synchronous staging copy
+      for (int p = tid; p < rows_here * n; p += THREADS)
         reinterpret_cast<TIn*>(land)[p] = src[p];
       __syncthreads();
     }
     TOut* cdst = Cout + static_cast<size_t>(b) * nn;
     TOut* sdst = Sout + static_cast<size_t>(b) * nn;
-    if (status != 0) {
-      store_nan(cdst, n);
-      store_nan(sdst, n);
+    if (status != 0) {  // uniform across the cluster (same matrix)
+      store_nan(cdst, n, row0, BAND);
+      store_nan(sdst, n, row0, BAND);
       __syncthreads();
       if (tid == 0) prefetch(bn);
       continue;
@@ -701,24 +788,24 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
     } else {
       f = ldexp(1.0, -s);  // driver.py:115, a * 2**-s (folded into P1/Pk)
     }
-    {  // slot 6 (natural) -> slot 0 (swizzled, zero padded)
+    {  // slot 6 (natural band) -> slot 0 (swizzled, zero padded)
       const double g = WAVE ? f : 1.0;
       const TIn* nat = reinterpret_cast<const TIn*>(land);
 #pragma unroll 2
       for (int p = tid; p < SLOT / 2; p += THREADS) {
-        const int r = p >> 5, c = (p & 31) * 2;
+        const int r = p / (NP / 2), c = (p % (NP / 2)) * 2;
         double v0 = 0.0, v1 = 0.0;
         if (n == NP) {
           v0 = static_cast<double>(nat[r * NP + c]);
           v1 = static_cast<double>(nat[r * NP + c + 1]);
-        } else if (r < n) {
+        } else if (r < rows_here) {
           if (c < n) v0 = static_cast<double>(nat[r * n + c]);
           if (c + 1 < n) v1 = static_cast<double>(nat[r * n + c + 1]);
         }
-        st2(smem, swz(r, c), g * v0, g * v1);
+        st2(smem, swz<NP>(r, c), g * v0, g * v1);
       }
     }
-    __syncthreads();
+    step_sync<CL>();  // the first product reads slot 0 of every band
     auto slotp = [&](int i) -> double* { return smem + i * SLOT; };
     const int ci = WAVE ? (k == 3 ? 4 : (k == 4 ? 5 : 6))
                         : (k == 3 ? 0 : (k == 4 ? 1 : (k == 6 ? 2 : 3)));
@@ -728,9 +815,10 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
       const Step st = ch.step[i];
       TRACE_T(2);
       if (st.dual)
-        gemm<true>(slotp(st.l1), slotp(st.l2), slotp(st.r), acc, acc2, ln);
+        gemm<CL, true>(slotp(st.l1), slotp(st.l2), rview<CL>(slotp(st.r), rank), acc, acc2, ln);
       else
-        gemm<false>(slotp(st.l1), nullptr, slotp(st.r), acc, acc2, ln);
+        gemm<CL, false>(slotp(st.l1), nullptr, rview<CL>(slotp(st.r), rank), acc, acc2, ln);
+      TRACE_T(3);
       EpiArgs<TOut> E;
       E.o[0] = slotp(st.o0);
       E.o[1] = slotp(st.o1);
@@ -747,9 +835,9 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
       E.scale = st.scale == SC_F ? f : st.scale == SC_F2 ? f * f
               : st.scale == SC_TP ? tp : 1.0;
       E.n = n;
-      epilogue(st.epi, E, acc, acc2, keep, ln);
+      epilogue<CL>(st.epi, E, acc, acc2, keep, ln);
       TRACE_T(4);
-      __syncthreads();
+      step_sync<CL>();
       TRACE_T(5);
       if (i == pf_after && tid == 0) prefetch(bn);
     }
@@ -757,8 +845,10 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
     double* S = slotp(ch.sin_slot);
     double* F1 = slotp(ch.free1);
     double* F2 = slotp(ch.free2);
-    doubling(C, S, F1, F2, s, ln, cdst, sdst, n);
+    doubling<CL>(C, S, F1, F2, s, ln, cdst, sdst, n);
   }
+  // no CTA may leave while a peer can still read its bands
+  if (CL > 1) step_sync<CL>();
 }
 
 }  // namespace f64k
@@ -767,45 +857,73 @@ size_t fused64_smem_bytes() {
   return static_cast<size_t>(f64k::NSLOTS) * f64k::SLOT * sizeof(double);
 }
 
-template <typename TIn, typename TOut, bool WAVE>
+template <int CL, typename TIn, typename TOut, bool WAVE>
 static cudaError_t launch_one(const void* a, void* c, void* s, const double* t,
                               const int32_t* k, const int32_t* sx,
                               const int32_t* st, const int32_t* order, int64_t batch,
-                              int n, int grid, cudaStream_t stream) {
-  auto kern = f64k::fused64_kernel<TIn, TOut, WAVE>;
+                              int n, int sms, cudaStream_t stream) {
+  auto kern = f64k::fused64_kernel<CL, TIn, TOut, WAVE>;
   const size_t smem = fused64_smem_bytes();
-  const size_t in_bytes = static_cast<size_t>(n) * n * sizeof(TIn);
-  const int tma = (in_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0) ? 1 : 0;
+  const size_t mat_bytes = static_cast<size_t>(n) * n * sizeof(TIn);
+  // TMA needs 16-byte aligned matrix starts; K1c checks each band's size
+  const int tma = (mat_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0) ? 1 : 0;
   cudaError_t e = cudaFuncSetAttribute(
       kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  kern<<<grid, f64k::THREADS, smem, stream>>>(
-      static_cast<const TIn*>(a), static_cast<TOut*>(c), static_cast<TOut*>(s),
-      t, k, sx, st, order, batch, n, tma);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.blockDim = dim3(f64k::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  int clusters = sms;
+  if (CL > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(CL * (sms / CL));
+    int active = 0;
+    e = cudaOccupancyMaxActiveClusters(&active, kern, &cfg);
+    if (e != cudaSuccess) return e;
+    clusters = active > 0 ? active : sms / CL;  // persistent: every cluster resident
+  }
+  if (clusters > batch) clusters = static_cast<int>(batch);
+  if (clusters < 1) return cudaSuccess;
+  cfg.gridDim = dim3(CL * clusters);
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<const TIn*>(a), static_cast<TOut*>(c),
+                            static_cast<TOut*>(s), t, k, sx, st, order, batch, n, tma);
 }
 
-// Launch K1 for a batch of n <= 64 matrices whose (k, s, status) and
-// cost-sorted order[] are already on the device.
+template <int CL>
+static cudaError_t launch_fused(int dtype, bool wave, const void* a, void* c, void* s,
+                                const double* t, const int32_t* k, const int32_t* sx,
+                                const int32_t* st, const int32_t* order, int64_t batch, int n,
+                                cudaStream_t stream) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (dtype == 0) {
+    return wave ? launch_one<CL, double, double, true>(a, c, s, t, k, sx, st, order, batch, n, sms, stream)
+                : launch_one<CL, double, double, false>(a, c, s, t, k, sx, st, order, batch, n, sms, stream);
+  }
+  if (dtype == 2) {
+    return wave ? launch_one<CL, float, double, true>(a, c, s, t, k, sx, st, order, batch, n, sms, stream)
+                : launch_one<CL, float, double, false>(a, c, s, t, k, sx, st, order, batch, n, sms, stream);
+  }
+  return wave ? launch_one<CL, float, float, true>(a, c, s, t, k, sx, st, order, batch, n, sms, stream)
+              : launch_one<CL, float, float, false>(a, c, s, t, k, sx, st, order, batch, n, sms, stream);
+}
+
+// Launch K1 (n <= 64) or K1c (64 < n <= 128) for a batch whose (k, s,
+// status) and cost-sorted order[] are already on the device.
 cudaError_t launch_fused64(int dtype, bool wave, const void* a, void* c,
                            void* s, const double* t, const int32_t* k,
                            const int32_t* sx, const int32_t* st, const int32_t* order,
                            int64_t batch, int n, cudaStream_t stream) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int grid = static_cast<int>(batch < sms ? batch : sms);
-  if (grid < 1) return cudaSuccess;
-  if (dtype == 0) {
-    return wave ? launch_one<double, double, true>(a, c, s, t, k, sx, st, order, batch, n, grid, stream)
-                : launch_one<double, double, false>(a, c, s, t, k, sx, st, order, batch, n, grid, stream);
-  }
-  if (dtype == 2) {
-    return wave ? launch_one<float, double, true>(a, c, s, t, k, sx, st, order, batch, n, grid, stream)
-                : launch_one<float, double, false>(a, c, s, t, k, sx, st, order, batch, n, grid, stream);
-  }
-  return wave ? launch_one<float, float, true>(a, c, s, t, k, sx, st, order, batch, n, grid, stream)
-              : launch_one<float, float, false>(a, c, s, t, k, sx, st, order, batch, n, grid, stream);
+  if (n <= 64) return launch_fused<1>(dtype, wave, a, c, s, t, k, sx, st, order, batch, n, stream);
+  return launch_fused<4>(dtype, wave, a, c, s, t, k, sx, st, order, batch, n, stream);
 }
 
 }  // namespace csm

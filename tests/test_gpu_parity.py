@@ -188,7 +188,35 @@ def test_batched_tiled_orders(cuda, n):
         assert rel1(rep.sin_part[i], s) <= TOL64, (n, i)
 
 
-@pytest.mark.parametrize("n", [64, 256])
+@pytest.mark.parametrize("n", [66, 99, 127])
+def test_cluster_kernel_orders(cuda, n):
+    """64 < n <= 128 runs on the 4-CTA cluster kernel (K1c): partial last
+    bands, odd n (unaligned bands take the synchronous staging path)."""
+    rng = np.random.default_rng(250 + n)
+    a = cfg2_like(rng, 10, n=n, lo=-3, hi=2.0)
+    rep = csm.cos_sin_batched(a)
+    for i in range(a.shape[0]):
+        c, s, k, sc = orc.cos_sin(a[i])
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc)
+        assert rel1(rep.cos_part[i], c) <= TOL64, (n, i)
+        assert rel1(rep.sin_part[i], s) <= TOL64, (n, i)
+
+
+def test_cluster_kernel_many_turns(cuda):
+    """More matrices than clusters: every cluster walks several turns of the
+    snake schedule, with s = 0 matrices (direct stores) mixed in."""
+    rng = np.random.default_rng(260)
+    a = cfg2_like(rng, 300, n=128, lo=-4, hi=2.0)
+    rep = csm.cos_sin_batched(a)
+    for i in list(range(0, 300, 23)) + [299]:
+        c, s, k, sc = orc.cos_sin(a[i])
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc)
+        assert rel1(rep.cos_part[i], c) <= TOL64, i
+        assert rel1(rep.sin_part[i], s) <= TOL64, i
+    assert (rep.s == 0).any() and (rep.s > 3).any()
+
+
+@pytest.mark.parametrize("n", [64, 99, 128, 256])
 def test_batched_float32(cuda, n):
     """configs[2] variant: float32 storage, float64 compute, SINGLE table."""
     rng = np.random.default_rng(300 + n)

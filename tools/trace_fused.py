@@ -19,7 +19,8 @@ from paper_2010_00465_b200 import _lib
 import paper_2010_00465_b200 as csm
 from tests._util import cfg2_like
 L = _lib.lib(); L.csm_trace_dump.restype = ctypes.c_int
-a = torch.from_numpy(cfg2_like(np.random.default_rng(0), 16384)).cuda()
+N = int(os.environ.get("TRACE_N", "64")); B = int(os.environ.get("TRACE_B", "16384"))
+a = torch.from_numpy(cfg2_like(np.random.default_rng(0), B, n=N)).cuda()
 csm.cos_sin_batched(a); torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 65536)(); L.csm_trace_dump(buf, 65536)
 csm.cos_sin_batched(a); torch.cuda.synchronize()
