@@ -23,6 +23,7 @@
  *       CSM_NONFINITE_INPUT   1  MatrixInputError  (driver.py:101-105)
  *       CSM_NONFINITE_NORM    2  ValueError        (driver.py:77-78)
  *       CSM_SELECT_OVERFLOW   3  OverflowError     (math.ceil(inf), driver.py:67)
+ *       CSM_SINGULAR          4  SingularMatrixError (Pade only, matcore.py:141-147)
  *     Matrices with a nonzero status are skipped; their outputs are NaN.
  */
 #ifndef COSSIN_B200_H
@@ -38,13 +39,15 @@ extern "C" {
 /* matrix dtype: input/output element types (compute is always float64) */
 enum { CSM_F64 = 0, CSM_F32 = 1, CSM_F32_IN_F64_OUT = 2 };
 enum { CSM_PREC_DOUBLE = 0, CSM_PREC_SINGLE = 1 };    /* theta table       */
-enum { CSM_FAMILY_TAYLOR = 0, CSM_FAMILY_WAVE = 1 };  /* scheme family     */
+enum { CSM_FAMILY_TAYLOR = 0, CSM_FAMILY_WAVE = 1,    /* scheme family     */
+       CSM_FAMILY_PADE = 2 };                          /* theta_tables.py:108-119 */
 
 enum {
   CSM_OK = 0,
   CSM_NONFINITE_INPUT = 1,
   CSM_NONFINITE_NORM = 2,
-  CSM_SELECT_OVERFLOW = 3
+  CSM_SELECT_OVERFLOW = 3,
+  CSM_SINGULAR = 4         /* Pade denominator singular (matcore.py:141-147) */
 };
 
 enum {
@@ -164,6 +167,20 @@ int csm_dd_matmul(const double* xh, const double* xl, const double* yh,
                   const double* yl, double* oh, double* ol, int64_t batch,
                   int n, void* stream);
 int csm_ddref_series_consts(double* out28);
+
+/* Order-8 Pade baseline (driver.py:149-164, schemes.py:446-464): selection
+ * over PADE_TABLE, a * 2^-s, five products (A^2, A^4, A^6, A^8 and A times
+ * the odd numerator) with the three polynomials fused into their epilogues,
+ * ONE batched LU with partial pivoting of the shared denominator and two
+ * solves (matcore.py:124-151, singularity test 1e3 eps ||den||_1), then s
+ * doublings.  k[] reports 5 (the PADE8 scheme id); the ledger cost is
+ * 22/3 + 2 s.  Every n runs the tiled chain; workspace:
+ * csm_pade_workspace_size(). */
+size_t csm_pade_workspace_size(int dtype, int64_t batch, int n);
+int csm_pade_cos_sin(int dtype, int precision, const void* a, void* cos_out,
+                     void* sin_out, int64_t batch, int n, int32_t* k, int32_t* s,
+                     int32_t* status, void* workspace, size_t ws_bytes,
+                     void* stream);
 
 /* Copy the built-in theta table of (family, precision) -- the reference's
  * TAYLOR_TABLE / WAVE_TABLE (theta_tables.py:79-144) -- into host arrays of

@@ -17,6 +17,8 @@ It restates, in numpy, the reference algorithm of arXiv 2010.00465 as the
 * trig / wave use   pkg/src/cossinm/schemes.py:376-395, :411-430
 * coefficients      pkg/src/cossinm/schemes.py:51-52, :110-187
 * theta tables      pkg/src/cossinm/theta_tables.py:79-144
+* Pade-8 baseline   pkg/src/cossinm/schemes.py:188-200, :446-464,
+                    driver.py:149-164, matcore.py:124-151
 
 Pinning: tests/test_oracle_golden.py checks every function here against
 tests/golden/*.npz and tests/golden/constants.json, which
@@ -106,7 +108,15 @@ _TH = {
                          (4, 8.961212972067917, 11.761988215232014),
                          (5, 30.86410513391181, 21.848395783984834)],
 }
+_TH[("pade", "double")] = [(5, 0.13959229566058115, 0.11212687277599737)]
+_TH[("pade", "single")] = [(5, 1.021836815484684, 0.9951082066593949)]
 THETA = {key: [(k, min(c, s)) for k, c, s in ents] for key, ents in _TH.items()}
+
+# order-8 diagonal Pade of exp split into cos / sin parts, polynomials in
+# y = A^2 (schemes.py:188-200)
+PADE_DEN = [Q(1), Q(1, 28), Q(3, 3920), Q(1, 70560), Q(1, 2822400)]
+PADE_NUM_COS = [Q(1), Q(-13, 28), Q(289, 11760), Q(-19, 70560), Q(1, 2822400)]
+PADE_NUM_SIN = [Q(1), Q(-11, 84), Q(37, 11760), Q(-1, 70560)]
 
 
 # ---------------------------------------------------------------------------
@@ -283,6 +293,40 @@ def cos_sin(a: np.ndarray, precision: str = "double"):
     c, sn = taylor_core(a * 2.0 ** -s, k)
     c, sn = double_angle(c, sn, s)
     return c, sn, k, s
+
+
+class SingularDenominator(RuntimeError):
+    pass
+
+
+def pade8_core(a: np.ndarray):
+    """pade8_cos_sin (schemes.py:446-464) with lu_solve_pair
+    (matcore.py:124-151): five products, one LU shared by two solves."""
+    from scipy.linalg import lu_factor, lu_solve
+    eye = np.eye(a.shape[0])
+    y = a @ a
+    y2 = y @ y
+    y3 = y @ y2
+    y4 = y @ y3
+    powers = [eye, y, y2, y3, y4]
+    den = lin([(float(c), p) for c, p in zip(PADE_DEN, powers)])
+    num_c = lin([(float(c), p) for c, p in zip(PADE_NUM_COS, powers)])
+    num_s = a @ lin([(float(c), p) for c, p in zip(PADE_NUM_SIN, powers)])
+    lu, piv = lu_factor(den, check_finite=False)
+    small = np.abs(np.diag(lu)).min()
+    if small <= 1e3 * float(np.finfo(np.float64).eps) * norm1(den):
+        raise SingularDenominator(f"pivot {small:.3e}")
+    return (lu_solve((lu, piv), num_c, check_finite=False),
+            lu_solve((lu, piv), num_s, check_finite=False))
+
+
+def pade_cos_sin(a: np.ndarray, precision: str = "double"):
+    """driver.py:149-164 -> (cos, sin, s); cost 22/3 + 2 s."""
+    _check(a)
+    _, s = select(norm1(a), "pade", precision)
+    c, sn = pade8_core(a * 2.0 ** -s)
+    c, sn = double_angle(c, sn, s)
+    return c, sn, s
 
 
 def wave_cos_sin(a: np.ndarray, t: float, precision: str = "double"):

@@ -13,6 +13,8 @@ from .api import (
     identity,
     matrix_from_rows,
     norm1,
+    pade_cos_sin,
+    pade_cos_sin_batched,
     read_matrix,
     select_batch,
     select_scheme,
@@ -27,6 +29,7 @@ from .api import (
 from . import plan, verify
 from .plan import BatchPlan
 from .records import (
+    PADE_TABLE,
     TAYLOR_TABLE,
     UNIT_ROUNDOFF,
     WAVE_TABLE,
@@ -38,6 +41,7 @@ from .records import (
     Precision,
     SchemeFamily,
     SchemeId,
+    SingularMatrixError,
     ThetaEntry,
     ThetaTable,
     WaveResult,
@@ -57,6 +61,8 @@ __all__ = [
     "Precision",
     "SchemeFamily",
     "SchemeId",
+    "SingularMatrixError",
+    "PADE_TABLE",
     "TAYLOR_TABLE",
     "ThetaEntry",
     "ThetaTable",
@@ -68,6 +74,8 @@ __all__ = [
     "identity",
     "matrix_from_rows",
     "norm1",
+    "pade_cos_sin",
+    "pade_cos_sin_batched",
     "read_matrix",
     "select_batch",
     "select_scheme",

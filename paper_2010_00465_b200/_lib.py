@@ -16,9 +16,9 @@ from . import build as _build
 # dtype codes
 F64, F32, F32_IN_F64_OUT = 0, 1, 2
 PREC_DOUBLE, PREC_SINGLE = 0, 1
-FAMILY_TAYLOR, FAMILY_WAVE = 0, 1
+FAMILY_TAYLOR, FAMILY_WAVE, FAMILY_PADE = 0, 1, 2
 # per-matrix status
-OK, NONFINITE_INPUT, NONFINITE_NORM, SELECT_OVERFLOW = 0, 1, 2, 3
+OK, NONFINITE_INPUT, NONFINITE_NORM, SELECT_OVERFLOW, SINGULAR = 0, 1, 2, 3, 4
 # return codes
 SUCCESS, ERR_ARG, ERR_CUDA, ERR_WORKSPACE, ERR_NO_DEVICE = 0, -1, -2, -3, -4
 
@@ -48,6 +48,8 @@ SIGNATURES = {
     "csm_sine_workspace_size": (_sz, [_i32, _i64, _i32]),
     "csm_taylor_sin9": (_i32, [_i32, _vp, _vp, _i64, _i32, _vp, _vp, _sz, _vp]),
     "csm_wave_sin34": (_i32, [_i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _sz, _vp]),
+    "csm_pade_workspace_size": (_sz, [_i32, _i64, _i32]),
+    "csm_pade_cos_sin": (_i32, [_i32, _i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "csm_ddref_workspace_size": (_sz, [_i64, _i32]),
     "csm_ddref_cos_sin": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
     "csm_dd_matmul": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),

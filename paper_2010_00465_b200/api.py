@@ -35,6 +35,7 @@ from .records import (
     MatrixInputError,
     Precision,
     SchemeFamily,
+    SingularMatrixError,
     SchemeId,
     ThetaTable,
     WaveResult,
@@ -120,6 +121,10 @@ def _as_batch(a, batched: bool, f32_out: bool) -> _Batch:
 def _status_error(status: int, norm: float) -> Exception:
     if status == _lib.NONFINITE_INPUT:
         return MatrixInputError("matrix entries must be finite")
+    if status == _lib.SINGULAR:
+        return SingularMatrixError(
+            "denominator singular to working precision (pivot <= 1e3 eps "
+            "||den||_1)")
     if status == _lib.NONFINITE_NORM:
         return ValueError(f"norm must be finite and nonnegative, got {norm}")
     return OverflowError("cannot convert float infinity to integer")
@@ -143,6 +148,9 @@ class BatchReport:
 
     @property
     def total_products(self):
+        """k + 2 s per matrix; 22/3 + 2 s (as float) for the Pade family."""
+        if self.family is SchemeFamily.PADE8:
+            return self.k + 2 * self.s + 7.0 / 3.0
         return self.k + 2 * self.s
 
     def report(self, i: int) -> ComputationReport:
@@ -150,6 +158,8 @@ class BatchReport:
         k, s = int(self.k[i]), int(self.s[i])
         ledger = CostLedger()
         ledger.charge_product(k + 2 * s)
+        if self.family is SchemeFamily.PADE8:
+            ledger.charge_lu(solves=2)
         if self.family is SchemeFamily.WAVE_KERNEL:
             res = WaveResult(self.cos_part[i], self.sin_part[i], ledger)
         else:
@@ -222,6 +232,48 @@ def cos_sin_batched(a, precision: Precision = Precision.DOUBLE, *,
                                      stream)
     return _finish(batch, SchemeFamily.COS_SIN_TAYLOR, precision, cos, sin,
                    k, s, st, ws, None, raise_on_error)
+
+
+def pade_cos_sin_batched(a, precision: Precision = Precision.DOUBLE, *,
+                         raise_on_error: bool = True,
+                         stream=None) -> BatchReport:
+    """The order-8 Pade baseline (driver.py:149-164) for a batch (B, n, n):
+    PADE_TABLE selection, five products, one batched LU with partial
+    pivoting shared by two solves, s doublings -- all on the device."""
+    batch = _as_batch(a, batched=True, f32_out=True)
+    return _pade(batch, precision, raise_on_error, stream)
+
+
+def _pade(batch: _Batch, precision, raise_on_error, stream=None) -> BatchReport:
+    torch = _torch()
+    L = _lib.lib()
+    x = batch.dev
+    B, n = int(x.shape[0]), int(x.shape[-1])
+    dev = x.device
+    cos = torch.empty((B, n, n), dtype=batch.out_dtype, device=dev)
+    sin = torch.empty_like(cos)
+    k = torch.empty(B, dtype=torch.int32, device=dev)
+    s = torch.empty_like(k)
+    status = torch.empty_like(k)
+    ws_bytes = int(L.csm_pade_workspace_size(batch.code, B, n))
+    ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
+    _lib.check(L.csm_pade_cos_sin(batch.code, _PREC_CODE[precision],
+                                  _vp(x.data_ptr()), _vp(cos.data_ptr()),
+                                  _vp(sin.data_ptr()), B, n, _vp(k.data_ptr()),
+                                  _vp(s.data_ptr()), _vp(status.data_ptr()),
+                                  _vp(ws.data_ptr()), ws_bytes,
+                                  _vp(_stream_handle(stream))),
+               "csm_pade_cos_sin")
+    return _finish(batch, SchemeFamily.PADE8, precision, cos, sin, k, s,
+                   status, ws, None, raise_on_error)
+
+
+def pade_cos_sin(a, precision: Precision = Precision.DOUBLE
+                 ) -> ComputationReport:
+    """Drop-in for driver.pade_cos_sin (driver.py:149-164); total_products
+    is the reference's 22/3 + 2 s."""
+    batch = _as_batch(a, batched=False, f32_out=False)
+    return _single(_pade(batch, precision, True))
 
 
 def _t_vector(t, B: int, dev):
@@ -403,8 +455,9 @@ def select_batch(norms, family: SchemeFamily = SchemeFamily.COS_SIN_TAYLOR,
     k = np.zeros(x.size, dtype=np.int32)
     s = np.zeros(x.size, dtype=np.int32)
     st = np.zeros(x.size, dtype=np.int32)
-    fam = (_lib.FAMILY_WAVE if family is SchemeFamily.WAVE_KERNEL
-           else _lib.FAMILY_TAYLOR)
+    fam = {SchemeFamily.COS_SIN_TAYLOR: _lib.FAMILY_TAYLOR,
+           SchemeFamily.WAVE_KERNEL: _lib.FAMILY_WAVE,
+           SchemeFamily.PADE8: _lib.FAMILY_PADE}[family]
     p = lambda arr: arr.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
     _lib.check(L.csm_select_host(p(x), x.size, fam, _PREC_CODE[precision],
                                  p(k), p(s), p(st)), "csm_select_host")
@@ -505,6 +558,7 @@ def write_matrix(path: str, a) -> None:
 
 __all__ = [
     "BatchReport", "cos_sin", "cos_sin_batched", "identity",
+    "pade_cos_sin", "pade_cos_sin_batched",
     "matrix_from_rows", "norm1", "read_matrix", "select_batch",
     "select_scheme", "taylor_cos_sin", "taylor_sin9", "wave_cos_sin",
     "wave_cos_sin_batched", "wave_kernels", "wave_sin34", "write_matrix",

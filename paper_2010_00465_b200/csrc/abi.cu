@@ -301,9 +301,13 @@ int csm_norm1(int dtype, const void* a, int64_t batch, int n, double* norms, int
   return CSM_SUCCESS;
 }
 
+static bool family_ok(int family) {
+  return family == CSM_FAMILY_TAYLOR || family == CSM_FAMILY_WAVE || family == CSM_FAMILY_PADE;
+}
+
 int csm_select_host(const double* norms, int64_t count, int family, int precision, int32_t* k,
                     int32_t* s, int32_t* status) {
-  if (family != CSM_FAMILY_TAYLOR && family != CSM_FAMILY_WAVE) return fail(CSM_ERR_ARG, "bad family");
+  if (!family_ok(family)) return fail(CSM_ERR_ARG, "bad family");
   if (precision != CSM_PREC_DOUBLE && precision != CSM_PREC_SINGLE)
     return fail(CSM_ERR_ARG, "bad precision");
   if (count < 0) return fail(CSM_ERR_ARG, "count must be nonnegative");
@@ -322,7 +326,7 @@ int csm_select_host(const double* norms, int64_t count, int family, int precisio
 int csm_select_device(const double* norms, int64_t count, int family, int precision, int32_t* k,
                       int32_t* s, int32_t* status, void* stream) {
   g_launches = 0;
-  if (family != CSM_FAMILY_TAYLOR && family != CSM_FAMILY_WAVE) return fail(CSM_ERR_ARG, "bad family");
+  if (!family_ok(family)) return fail(CSM_ERR_ARG, "bad family");
   if (precision != CSM_PREC_DOUBLE && precision != CSM_PREC_SINGLE)
     return fail(CSM_ERR_ARG, "bad precision");
   if (count < 0) return fail(CSM_ERR_ARG, "count must be nonnegative");
@@ -407,15 +411,18 @@ int csm_wave_core(int dtype, int k, const void* a, const double* t, void* c_out,
 
 int csm_theta_table(int family, int precision, double* theta_cos, double* theta_sin, int32_t* k,
                     int capacity) {
-  if (family != CSM_FAMILY_TAYLOR && family != CSM_FAMILY_WAVE) return fail(CSM_ERR_ARG, "bad family");
+  if (!family_ok(family)) return fail(CSM_ERR_ARG, "bad family");
   if (precision != CSM_PREC_DOUBLE && precision != CSM_PREC_SINGLE)
     return fail(CSM_ERR_ARG, "bad precision");
-  const double* tc[2][2] = {{kThetaCos_taylor_double, kThetaCos_taylor_single},
-                            {kThetaCos_wave_double, kThetaCos_wave_single}};
-  const double* ts[2][2] = {{kThetaSin_taylor_double, kThetaSin_taylor_single},
-                            {kThetaSin_wave_double, kThetaSin_wave_single}};
-  const int* kk[2][2] = {{kK_taylor_double, kK_taylor_single}, {kK_wave_double, kK_wave_single}};
-  const int count = family == CSM_FAMILY_TAYLOR ? 4 : 3;
+  const double* tc[3][2] = {{kThetaCos_taylor_double, kThetaCos_taylor_single},
+                            {kThetaCos_wave_double, kThetaCos_wave_single},
+                            {kThetaCos_pade_double, kThetaCos_pade_single}};
+  const double* ts[3][2] = {{kThetaSin_taylor_double, kThetaSin_taylor_single},
+                            {kThetaSin_wave_double, kThetaSin_wave_single},
+                            {kThetaSin_pade_double, kThetaSin_pade_single}};
+  const int* kk[3][2] = {{kK_taylor_double, kK_taylor_single}, {kK_wave_double, kK_wave_single},
+                         {kK_pade_double, kK_pade_single}};
+  const int count = family == CSM_FAMILY_TAYLOR ? 4 : (family == CSM_FAMILY_WAVE ? 3 : 1);
   if (capacity < count || !theta_cos || !theta_sin || !k) return fail(CSM_ERR_ARG, "capacity too small");
   for (int i = 0; i < count; ++i) {
     theta_cos[i] = tc[family][precision][i];
@@ -609,6 +616,52 @@ int csm_ddref_cos_sin(const double* a, double* cos_out, double* sin_out, int64_t
   // the host vector hs must outlive the async upload
   e = cudaStreamSynchronize(stream);
   if (e != cudaSuccess) return cuda_fail(e, "ddref chain");
+  return CSM_SUCCESS;
+}
+
+// ---------------------------------------------------------------------------
+// Order-8 Pade baseline (driver.py:149-164).
+
+size_t csm_pade_workspace_size(int dtype, int64_t batch, int n) {
+  (void)dtype;
+  if (batch < 0 || n < 0) return 0;
+  return common_bytes(batch) + csm::tiled_workspace_bytes(batch, n) + 256;
+}
+
+int csm_pade_cos_sin(int dtype, int precision, const void* a, void* cos_out, void* sin_out,
+                     int64_t batch, int n, int32_t* k, int32_t* sx, int32_t* status, void* ws,
+                     size_t ws_bytes, void* stream_v) {
+  g_launches = 0;
+  if (dtype != CSM_F64 && dtype != CSM_F32 && dtype != CSM_F32_IN_F64_OUT)
+    return fail(CSM_ERR_ARG, "bad dtype");
+  if (precision != CSM_PREC_DOUBLE && precision != CSM_PREC_SINGLE)
+    return fail(CSM_ERR_ARG, "bad precision");
+  if (batch < 0 || n < 0) return fail(CSM_ERR_ARG, "batch and n must be nonnegative");
+  if (ws_bytes < csm_pade_workspace_size(dtype, batch, n))
+    return fail(CSM_ERR_WORKSPACE, "workspace smaller than csm_pade_workspace_size()");
+  if (batch == 0) return CSM_SUCCESS;
+  if (!k || !sx || !status || !ws || (n > 0 && (!a || !cos_out || !sin_out)))
+    return fail(CSM_ERR_ARG, "null pointer argument");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  CommonWs w = carve(ws, batch);
+  cudaError_t e = cudaMemsetAsync(w.normbits, 0, static_cast<size_t>(batch) * 8, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, static_cast<size_t>(batch) * 4, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  if (n > 0) {
+    e = csm::launch_norm1(dtype, a, batch, n, w.normbits, status, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "norm1 kernel");
+    ++g_launches;
+  }
+  e = csm::launch_select(w.normbits, nullptr, batch, CSM_FAMILY_PADE, precision, k, sx, status,
+                         nullptr, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "select kernel");
+  ++g_launches;
+  if (n == 0) return CSM_SUCCESS;
+  e = csm::run_tiled(dtype, false, a, nullptr, cos_out, sin_out, batch, n, k, sx, status, w.tiled,
+                     stream, &g_launches, 3);
+  if (e != cudaSuccess) return cuda_fail(e, "pade chain");
   return CSM_SUCCESS;
 }
 

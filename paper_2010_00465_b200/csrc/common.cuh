@@ -19,9 +19,9 @@ namespace csm {
 // Constant tables, mirrored into __constant__ memory for the device.
 
 struct Tables {
-  double theta[2][2][4];  // [family][precision][entry] theta_eff
-  int kk[2][2][4];        // scheme k of each entry
-  int nent[2];            // entries per family
+  double theta[3][2][4];  // [family][precision][entry] theta_eff
+  int kk[3][2][4];        // scheme k of each entry
+  int nent[3];            // entries per family (taylor, wave, pade)
   long long log2fix[1024];
   double x8[8];           // x1..x8       (schemes.py:110-119)
   double z8[9];           // z0..z8       (schemes.py:125-135)
@@ -34,7 +34,7 @@ __constant__ Tables dTables;
 const Tables& host_tables();
 
 enum Status : int32_t { kOk = 0, kNonfiniteInput = 1, kNonfiniteNorm = 2,
-                        kSelectOverflow = 3 };
+                        kSelectOverflow = 3, kSingular = 4 };
 
 // ceil(log2(q)) as driver.py:67 computes it with glibc's correctly rounded
 // log2, for q >= 1 finite.  q = 2^e (1 + j 2^-52): log2(q) rounds down to e

@@ -29,8 +29,13 @@ static Tables make_tables() {
     t.kk[1][0][i] = kK_wave_double[i];
     t.kk[1][1][i] = kK_wave_single[i];
   }
+  t.theta[2][0][0] = kTheta_pade_double[0];
+  t.theta[2][1][0] = kTheta_pade_single[0];
+  t.kk[2][0][0] = kK_pade_double[0];
+  t.kk[2][1][0] = kK_pade_single[0];
   t.nent[0] = 4;
   t.nent[1] = 3;
+  t.nent[2] = 1;
   for (int i = 0; i < 1024; ++i) t.log2fix[i] = kLog2Fix[i];
   for (int i = 0; i < 8; ++i) t.x8[i] = kXDeg8[i];
   for (int i = 0; i < 9; ++i) t.z8[i] = kZDeg8[i];

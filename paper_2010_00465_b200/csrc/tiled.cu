@@ -317,6 +317,126 @@ __global__ void nan_fill_kernel(TOut* __restrict__ Cout, TOut* __restrict__ Sout
   }
 }
 
+// Order-8 Pade: LU with partial pivoting of the shared denominator (slot 5)
+// and the two solves for the numerators (slots 6 and 7, in place), one CTA
+// per matrix on its n x n block (the padding of den / num_cos is I and of
+// num_sin is 0, so the padded solution is block-diagonal too).  Mirrors
+// lu_solve_pair (matcore.py:124-151): LAPACK getrf pivoting (first largest
+// |a_ik|), singular when min |u_kk| <= 1e3 eps ||den||_1, then getrs.
+// Matrices with s == 0 write their final cos / sin here.
+__global__ void __launch_bounds__(256) pade_lu_solve_kernel(
+    double* __restrict__ ws, size_t mat_stride, int NP, int n, const int32_t* __restrict__ idx,
+    const int32_t* __restrict__ S, int32_t* __restrict__ status, void* cout, void* sout,
+    int out_f32) {
+  const int b = idx[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const size_t slotsz = static_cast<size_t>(NP) * NP;
+  double* D = ws + static_cast<size_t>(b) * mat_stride + 5 * slotsz;
+  double* X[2] = {D + slotsz, D + 2 * slotsz};
+  __shared__ double red_v[8];
+  __shared__ int red_i[8];
+  __shared__ int sh_p;
+  __shared__ double sh_norm, sh_umin;
+
+  // ||den||_1 (threshold of the singularity test)
+  double cmax = 0.0;
+  for (int j = tid; j < n; j += 256) {
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) acc += fabs(D[static_cast<size_t>(i) * NP + j]);
+    cmax = fmax(cmax, acc);
+  }
+  for (int o = 16; o; o >>= 1) cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+  if (lane == 0) red_v[warp] = cmax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = red_v[0];
+    for (int w = 1; w < 8; ++w) m = fmax(m, red_v[w]);
+    sh_norm = m;
+    sh_umin = __longlong_as_double(0x7ff0000000000000ll);
+  }
+  __syncthreads();
+
+  for (int k = 0; k < n; ++k) {
+    // pivot: first row of max |a_ik|, i >= k (idamax)
+    double bv = -1.0;
+    int bi = n;
+    for (int i = k + tid; i < n; i += 256) {
+      const double v = fabs(D[static_cast<size_t>(i) * NP + k]);
+      if (v > bv) { bv = v; bi = i; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double v = red_v[0];
+      int p = red_i[0];
+      for (int w = 1; w < 8; ++w)
+        if (red_v[w] > v || (red_v[w] == v && red_i[w] < p)) { v = red_v[w]; p = red_i[w]; }
+      sh_p = p < n ? p : k;
+    }
+    __syncthreads();
+    const int p = sh_p;
+    if (p != k) {  // swap rows k, p of den (whole row) and of both right-hand sides
+      for (int j = tid; j < 3 * n; j += 256) {
+        double* M = j < n ? D : X[j / n - 1];
+        const int c = j % n;
+        const double t = M[static_cast<size_t>(k) * NP + c];
+        M[static_cast<size_t>(k) * NP + c] = M[static_cast<size_t>(p) * NP + c];
+        M[static_cast<size_t>(p) * NP + c] = t;
+      }
+      __syncthreads();
+    }
+    const double piv = D[static_cast<size_t>(k) * NP + k];
+    if (tid == 0) sh_umin = fmin(sh_umin, fabs(piv));
+    const double rcp = 1.0 / piv;
+    for (int i = k + 1 + tid; i < n; i += 256) D[static_cast<size_t>(i) * NP + k] *= rcp;
+    __syncthreads();
+    for (int i = k + 1 + warp; i < n; i += 8) {
+      const double l = D[static_cast<size_t>(i) * NP + k];
+      double* row = D + static_cast<size_t>(i) * NP;
+      const double* urow = D + static_cast<size_t>(k) * NP;
+      for (int j = k + 1 + lane; j < n; j += 32) row[j] = fma(-l, urow[j], row[j]);
+    }
+    __syncthreads();
+  }
+  if (sh_umin <= 1e3 * 0x1p-52 * sh_norm || !(sh_umin == sh_umin)) {
+    if (tid == 0) status[b] = kSingular;
+    return;
+  }
+  // getrs: unit-lower then upper triangular solve, one thread per column
+  for (int j = tid; j < 2 * n; j += 256) {
+    double* M = X[j / n];
+    const int c = j % n;
+    for (int i = 1; i < n; ++i) {
+      double acc = M[static_cast<size_t>(i) * NP + c];
+      const double* lrow = D + static_cast<size_t>(i) * NP;
+      for (int q = 0; q < i; ++q) acc = fma(-lrow[q], M[static_cast<size_t>(q) * NP + c], acc);
+      M[static_cast<size_t>(i) * NP + c] = acc;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double acc = M[static_cast<size_t>(i) * NP + c];
+      const double* urow = D + static_cast<size_t>(i) * NP;
+      for (int q = i + 1; q < n; ++q) acc = fma(-urow[q], M[static_cast<size_t>(q) * NP + c], acc);
+      M[static_cast<size_t>(i) * NP + c] = acc / urow[i];
+    }
+  }
+  if (S[b] != 0) return;
+  __syncthreads();
+  const size_t nn = static_cast<size_t>(n) * n;
+  for (size_t e = tid; e < 2 * nn; e += 256) {
+    const int w = static_cast<int>(e / nn);
+    const size_t r = (e % nn) / n, c = (e % nn) % n;
+    const double v = X[w][r * NP + c];
+    void* dst = w == 0 ? cout : sout;
+    if (out_f32) static_cast<float*>(dst)[b * nn + r * n + c] = static_cast<float>(v);
+    else static_cast<double*>(dst)[b * nn + r * n + c] = v;
+  }
+}
+
 }  // namespace tk
 
 // ---------------------------------------------------------------------------
@@ -465,6 +585,21 @@ Program build_special(int special, bool fold) {
     step({make_op(2, 3, {{4, {{EYE, 1.0}, {1, -1.0 / 6.0}, {2, 1.0 / 120.0}, {ACC, 1.0}}}})});
     step({make_op(0, 4, {{5, {{ACC, 1.0}}, ss, tk::FIN_SIN}})});
     P.cos_slot = 6; P.sin_slot = 5;
+  } else if (special == 3) {
+    // pade8_cos_sin (schemes.py:446-464): y..y4 with den / num_cos fused
+    // into the y4 epilogue and the odd numerator's polynomial into y3's;
+    // the LU solve (slots 5 | 6, 7 -> 6, 7) runs between chain and doubling
+    const double* D = kPadeDen;
+    const double* C = kPadeNumCos;
+    const double* N = kPadeNumSin;
+    step({make_op(0, 0, {{1, {{ACC, 1.0}}, sy}})});
+    step({make_op(1, 1, {{2, {{ACC, 1.0}}}})});
+    step({make_op(1, 2, {{3, {{ACC, 1.0}}},
+                         {4, {{EYE, N[0]}, {1, N[1]}, {2, N[2]}, {ACC, N[3]}}}})});
+    step({make_op(1, 3, {{5, {{EYE, D[0]}, {1, D[1]}, {2, D[2]}, {3, D[3]}, {ACC, D[4]}}},
+                         {6, {{EYE, C[0]}, {1, C[1]}, {2, C[2]}, {3, C[3]}, {ACC, C[4]}}}})});
+    step({make_op(0, 4, {{7, {{ACC, 1.0}}, ss}})});
+    P.cos_slot = 6; P.sin_slot = 7;
   } else {
     step({make_op(0, 0, {{1, {{ACC, 1.0}}}, {2, {{0, -1.0 / 720.0}, {ACC, 1.0 / 40320.0}}}})});
     step({make_op(1, 2, {{3, {{EYE, 1.0}, {0, -1.0 / 6.0}, {1, 1.0 / 120.0},
@@ -568,9 +703,10 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
   }
 
   // group by k, each group sorted by s descending (doubling = prefixes)
-  const int ks_taylor[4] = {3, 4, 6, 7}, ks_wave[3] = {3, 4, 5};
-  const int* ks = wave ? ks_wave : ks_taylor;
-  const int nks = wave ? 3 : 4;
+  const int ks_taylor[4] = {3, 4, 6, 7}, ks_wave[3] = {3, 4, 5}, ks_pade[1] = {5};
+  const bool pade = special == 3;
+  const int* ks = pade ? ks_pade : (wave ? ks_wave : ks_taylor);
+  const int nks = pade ? 1 : (wave ? 3 : 4);
   std::vector<int32_t> order;
   order.reserve(batch);
   struct Group {
@@ -693,7 +829,17 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     A.row0 = 0;
     A.rhs_full = nullptr;
     prof_begin(stream);
-    for (const LaunchPlan& L : plans) {
+    for (size_t pi = 0; pi < plans.size(); ++pi) {
+      const LaunchPlan& L = plans[pi];
+      if (pade && pi == max_steps) {  // chain done: factor and solve before doubling
+        for (const Group& G : groups) {
+          tk::pade_lu_solve_kernel<<<static_cast<unsigned>(G.cnt), 256, 0, stream>>>(
+              w.slots, mat_stride, NP, n, w.idx + G.off, dS, const_cast<int32_t*>(dStatus),
+              c_out, s_out, out_f32);
+          ++*launches;
+          if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+      }
       A.dbl_step = L.dbl_step;
       A.nseg = static_cast<int>(L.seg.size());
       for (size_t i = 0; i < L.seg.size(); ++i) A.seg[i] = L.seg[i];
@@ -707,10 +853,19 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
       }
     }
+    if (pade && plans.size() == max_steps) {  // no doubling at all
+      for (const Group& G : groups) {
+        tk::pade_lu_solve_kernel<<<static_cast<unsigned>(G.cnt), 256, 0, stream>>>(
+            w.slots, mat_stride, NP, n, w.idx + G.off, dS, const_cast<int32_t*>(dStatus), c_out,
+            s_out, out_f32);
+        ++*launches;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      }
+    }
     prof_end(stream);
   }
 
-  if (any_bad) {
+  if (any_bad || pade) {  // Pade: the LU may have flagged singular denominators
     const size_t nn = static_cast<size_t>(n) * n;
     dim3 grid(static_cast<unsigned>(std::min<size_t>((nn + 255) / 256, 64)),
               static_cast<unsigned>(batch));

@@ -12,6 +12,8 @@ Same names, fields and validation rules as the reference package
   host and device)
 * CostLedger ..................... matcore.py:38-66
 * MatrixInputError ............... matcore.py:30-31
+* SingularMatrixError ............ matcore.py:34-35
+* PADE_TABLE ..................... theta_tables.py:108-119
 * ComputationReport .............. driver.py:56-61
 """
 from __future__ import annotations
@@ -31,6 +33,10 @@ DenseMatrix: TypeAlias = Any  # numpy.ndarray or torch.Tensor (CUDA)
 
 class MatrixInputError(ValueError):
     """Malformed matrix input: not square or not finite."""
+
+
+class SingularMatrixError(RuntimeError):
+    """Pade denominator singular to working precision."""
 
 
 class SchemeFamily(enum.Enum):
@@ -155,8 +161,9 @@ _PREC_CODE = {Precision.DOUBLE: _lib.PREC_DOUBLE,
 
 
 def _library_table(family: SchemeFamily, precision: Precision) -> ThetaTable:
-    code = (_lib.FAMILY_TAYLOR if family is SchemeFamily.COS_SIN_TAYLOR
-            else _lib.FAMILY_WAVE)
+    code = {SchemeFamily.COS_SIN_TAYLOR: _lib.FAMILY_TAYLOR,
+            SchemeFamily.WAVE_KERNEL: _lib.FAMILY_WAVE,
+            SchemeFamily.PADE8: _lib.FAMILY_PADE}[family]
     tc = np.zeros(8, dtype=np.float64)
     ts = np.zeros(8, dtype=np.float64)
     kk = np.zeros(8, dtype=np.int32)
@@ -166,14 +173,20 @@ def _library_table(family: SchemeFamily, precision: Precision) -> ThetaTable:
         8), "csm_theta_table")
     return ThetaTable(precision, tuple(
         ThetaEntry(SchemeId(family, int(kk[i])), float(tc[i]), float(ts[i]),
-                   Fraction(int(kk[i])))
+                   PADE8_COST if family is SchemeFamily.PADE8
+                   else Fraction(int(kk[i])))
         for i in range(count)))
 
+
+# five products + one LU (1/3) + two solves (driver.py:159, matcore.py:136)
+PADE8_COST = Fraction(22, 3)
 
 TAYLOR_TABLE: dict[Precision, ThetaTable] = {
     p: _library_table(SchemeFamily.COS_SIN_TAYLOR, p) for p in Precision}
 WAVE_TABLE: dict[Precision, ThetaTable] = {
     p: _library_table(SchemeFamily.WAVE_KERNEL, p) for p in Precision}
+PADE_TABLE: dict[Precision, ThetaTable] = {
+    p: _library_table(SchemeFamily.PADE8, p) for p in Precision}
 
 
 def table_for(family: SchemeFamily, precision: Precision) -> ThetaTable:
@@ -181,4 +194,4 @@ def table_for(family: SchemeFamily, precision: Precision) -> ThetaTable:
         return TAYLOR_TABLE[precision]
     if family is SchemeFamily.WAVE_KERNEL:
         return WAVE_TABLE[precision]
-    raise ValueError(f"no built-in table for {family.value} on this path")
+    return PADE_TABLE[precision]

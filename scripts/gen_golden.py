@@ -10,6 +10,7 @@ Reference entry points exercised (paths under /root/reference):
   cos_sin        pkg/src/cossinm/driver.py:108-123
   wave_cos_sin   pkg/src/cossinm/driver.py:126-146
   norm1          pkg/src/cossinm/matcore.py:100-104
+  pade_cos_sin   pkg/src/cossinm/driver.py:149-164
 """
 from __future__ import annotations
 
@@ -24,7 +25,7 @@ sys.path.insert(0, os.environ.get("COSSIN_REF_SRC", "/root/reference/pkg/src"))
 
 import cossinm  # noqa: E402
 from cossinm import Precision  # noqa: E402
-from cossinm.theta_tables import TAYLOR_TABLE, WAVE_TABLE  # noqa: E402
+from cossinm.theta_tables import PADE_TABLE, TAYLOR_TABLE, WAVE_TABLE  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "tests", "golden")
@@ -50,7 +51,8 @@ def selection_norms(table, rng) -> np.ndarray:
 
 def gen_selection(rng):
     out = {}
-    for fam, tabs in (("taylor", TAYLOR_TABLE), ("wave", WAVE_TABLE)):
+    for fam, tabs in (("taylor", TAYLOR_TABLE), ("wave", WAVE_TABLE),
+                      ("pade", PADE_TABLE)):
         for prec in (Precision.DOUBLE, Precision.SINGLE):
             tab = tabs[prec]
             norms = selection_norms(tab, rng)
@@ -227,6 +229,32 @@ def gen_ddref(rng):
     np.savez_compressed(os.path.join(OUT, "ddref.npz"), **out)
 
 
+def gen_pade(rng):
+    """pade_cos_sin (driver.py:149-164) on seeded inputs, both tables."""
+    out = {}
+    names = []
+    cases = []
+    for n, target in ((1, 0.05), (3, 0.5), (8, 2.0), (16, 0.11), (33, 7.0),
+                      (64, 2.0), (65, 30.0), (80, 0.9)):
+        m = rng.standard_normal((n, n))
+        cases.append((f"p{n}_{target}", m * (target / cossinm.norm1(m)), "double"))
+    cases.append(("pzero4", np.zeros((4, 4)), "double"))
+    for n, target in ((12, 3.0), (40, 20.0)):
+        m = rng.uniform(-1, 1, (n, n))
+        cases.append((f"psingle{n}_{target}", m * (target / cossinm.norm1(m)), "single"))
+    for name, a, prec in cases:
+        rep = cossinm.pade_cos_sin(a, Precision(prec))
+        out[f"{name}__a"] = a
+        out[f"{name}__cos"] = rep.result.cos_part
+        out[f"{name}__sin"] = rep.result.sin_part
+        out[f"{name}__s"] = np.array(rep.scaling_exponent)
+        out[f"{name}__cost"] = np.array([rep.total_products.numerator,
+                                         rep.total_products.denominator])
+        names.append(f"{name}|{prec}")
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(OUT, "pade.npz"), **out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     rng = np.random.default_rng(20100465)
@@ -236,6 +264,7 @@ def main():
     gen_norms(rng)
     gen_extras(np.random.default_rng(77))
     gen_ddref(np.random.default_rng(2010))
+    gen_pade(np.random.default_rng(88))
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 

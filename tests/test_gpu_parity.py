@@ -469,3 +469,77 @@ def test_large_symmetric_against_oracle_noise_floor(cuda, n):
     gate = max(TOL64, 4.0 * noise)
     assert rel1(rep.result.cos_part, c) <= gate, (rel1(rep.result.cos_part, c), noise)
     assert rel1(rep.result.sin_part, s) <= gate, (rel1(rep.result.sin_part, s), noise)
+
+
+def _pade_tol(s, prec="double"):
+    """Pade + s doublings: the doubling recursion amplifies a perturbation of
+    the base pair by up to ~4 per step (verify.py:396-399 says the same of
+    its own oracle), and PADE_TABLE's small theta (0.112) needs s 4-5 more
+    steps than the Taylor table at the same norm.  Parity bar: 64 u 4^s,
+    never below the hot path's 1e-12 / 1e-5."""
+    if prec == "single":
+        return TOL32
+    return max(TOL64, 64 * 2.0 ** -53 * 4.0 ** s)
+
+
+def test_pade_golden_cases(cuda, golden_dir):
+    """Order-8 Pade baseline against the reference's own pade_cos_sin."""
+    from fractions import Fraction
+    g = _golden(golden_dir, "pade.npz")
+    for entry in g["names"]:
+        name, prec = str(entry).split("|")
+        a = g[f"{name}__a"]
+        rep = csm.pade_cos_sin(a, csm.Precision(prec))
+        s = int(g[f"{name}__s"])
+        assert rep.scaling_exponent == s, name
+        assert rep.scheme_used == csm.SchemeId(csm.SchemeFamily.PADE8, 5)
+        assert rep.total_products == Fraction(22, 3) + 2 * s
+        ref_c, ref_s = g[f"{name}__cos"], g[f"{name}__sin"]
+        tol = _pade_tol(s, prec)
+        assert pair_close(rep.result.cos_part, ref_c, ref_s, tol)[0], name
+        if orc.norm1(ref_s) > 0:
+            assert pair_close(rep.result.sin_part, ref_s, ref_c, tol)[0], name
+        if prec == "double":  # as accurate as the reference, against dd truth
+            from paper_2010_00465_b200 import verify
+            truth = verify.reference_cos_sin(a)
+            for got, ref, tr in ((rep.result.cos_part, ref_c, truth.cos_part),
+                                 (rep.result.sin_part, ref_s, truth.sin_part)):
+                if orc.norm1(tr) > 0:
+                    assert rel1(got, tr) <= 10 * rel1(ref, tr) + 1e-15, name
+
+
+@pytest.mark.parametrize("n", [64, 100, 200])
+def test_pade_batched_against_oracle(cuda, n):
+    rng = np.random.default_rng(500 + n)
+    a = cfg2_like(rng, 6, n=n, lo=-3, hi=1.5)
+    rep = csm.pade_cos_sin_batched(a)
+    assert (rep.k == 5).all()
+    for i in range(a.shape[0]):
+        c, s, sc = orc.pade_cos_sin(a[i])
+        assert int(rep.s[i]) == sc
+        assert pair_close(rep.cos_part[i], c, s, _pade_tol(sc))[0], (n, i)
+        assert pair_close(rep.sin_part[i], s, c, _pade_tol(sc))[0], (n, i)
+
+
+def test_pade_float32_and_agreement_with_taylor(cuda):
+    """float32 storage on the SINGLE table; Pade and Taylor agree on the
+    same inputs to the float32 tolerance."""
+    rng = np.random.default_rng(510)
+    a32 = cfg3_like(rng, 6, n=96)
+    rep = csm.pade_cos_sin_batched(a32, csm.Precision.SINGLE)
+    tay = csm.cos_sin_batched(a32, csm.Precision.SINGLE)
+    assert rep.cos_part.dtype == np.float32
+    for i in range(a32.shape[0]):
+        c, s, sc = orc.pade_cos_sin(a32[i].astype(np.float64), "single")
+        assert rel1(rep.cos_part[i], c) <= TOL32
+        assert rel1(rep.sin_part[i], s) <= TOL32
+        assert rel1(rep.cos_part[i], tay.cos_part[i]) <= TOL32
+
+
+def test_pade_errors(cuda):
+    with pytest.raises(csm.MatrixInputError):
+        csm.pade_cos_sin(np.array([[np.nan, 0.0], [0.0, 1.0]]))
+    with pytest.raises(ValueError):  # infinite norm (driver.py:77-78)
+        csm.pade_cos_sin(np.array([[1e308, 0.0], [1e308, 0.0]]))
+    with pytest.raises(OverflowError):  # finite norm, norm / theta = inf
+        csm.pade_cos_sin(np.array([[1e308, 0.0], [0.0, 0.0]]))

@@ -12,7 +12,7 @@ import paper_2010_00465_b200 as csm
 from oracle import cossin_oracle as orc
 
 FAM = {"taylor": csm.SchemeFamily.COS_SIN_TAYLOR,
-       "wave": csm.SchemeFamily.WAVE_KERNEL}
+       "wave": csm.SchemeFamily.WAVE_KERNEL, "pade": csm.SchemeFamily.PADE8}
 PREC = {"double": csm.Precision.DOUBLE, "single": csm.Precision.SINGLE}
 
 
@@ -31,7 +31,7 @@ def test_tables_carry_reference_bits(golden_dir):
 
 def test_host_twin_matches_reference_golden(golden_dir):
     g = np.load(os.path.join(golden_dir, "selection.npz"))
-    for fam in ("taylor", "wave"):
+    for fam in ("taylor", "wave", "pade"):
         for prec in ("double", "single"):
             key = f"{fam}_{prec}"
             k, s, st = csm.select_batch(g[f"{key}_norm"], FAM[fam], PREC[prec])

@@ -169,3 +169,25 @@ def test_ddref_oracle_bit_exact_with_reference(golden_dir):
         assert int(d[f"{name}__cost"]) == 7 + 2 * sc, name
         assert _bits_equal(c, d[f"{name}__cos"]), name
         assert _bits_equal(s, d[f"{name}__sin"]), name
+
+
+def test_pade_oracle_matches_reference(golden_dir):
+    """pade_cos_sin (driver.py:149-164): s exact, cost 22/3 + 2 s, values
+    within BLAS/LAPACK reordering of the reference's own outputs."""
+    import json
+    from fractions import Fraction
+    doc = json.load(open(os.path.join(golden_dir, "constants.json")))
+    for key, mine in (("den", orc.PADE_DEN), ("num_cos", orc.PADE_NUM_COS),
+                      ("num_sin", orc.PADE_NUM_SIN)):
+        assert [float(v) for v in mine] == [float.fromhex(h) for h in doc["pade8"][key]]
+    d = _load(golden_dir, "pade.npz")
+    for entry in d["names"]:
+        name, prec = str(entry).split("|")
+        c, s, sc = orc.pade_cos_sin(d[f"{name}__a"], prec)
+        assert sc == int(d[f"{name}__s"]), name
+        num, den = (int(v) for v in d[f"{name}__cost"])
+        assert Fraction(num, den) == Fraction(22, 3) + 2 * sc
+        assert rel1(c, d[f"{name}__cos"]) <= 1e-13, name
+        ref_s = d[f"{name}__sin"]
+        if orc.norm1(ref_s) > 0:
+            assert rel1(s, ref_s) <= 1e-13, name
