@@ -244,13 +244,18 @@ def run_cfg5(args, cfg):
     kind, batch, n, dt, prec, desc = cfg
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    peer = args.dist_mode == "peer"
+    if world > 1 or peer:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29571")
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    chain = distchain.cos_sin_distributed_peer if peer else distchain.cos_sin_distributed
     a_np, _ = make_inputs(kind, 1, n, seed=0)  # the same matrix on every rank
     a_host = torch.from_numpy(np.ascontiguousarray(a_np[0])).pin_memory()
     a = a_host.to(dev)
-    c, s_, st = distchain.cos_sin_distributed(a, gather_outputs=False)
+    c, s_, st = chain(a, gather_outputs=False)
     torch.cuda.synchronize()
     flops = 2.0 * n ** 3 * (st.k + 2 * st.s)
     # correctness: symmetric input -> symmetric cos rows block vs its transpose
@@ -258,7 +263,7 @@ def run_cfg5(args, cfg):
     blk = c[:, row0:row0 + M]
     assert float((blk - blk.T).abs().max() / blk.abs().max()) <= 1e-10
     for _ in range(args.warmup):
-        distchain.cos_sin_distributed(a, gather_outputs=False)
+        chain(a, gather_outputs=False)
     L = _lib.lib()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -267,7 +272,7 @@ def run_cfg5(args, cfg):
     with ClockSampler(local) as clk:
         e0.record()
         for _ in range(args.steps):
-            distchain.cos_sin_distributed(a, gather_outputs=False)
+            chain(a, gather_outputs=False)
         e1.record()
         torch.cuda.synchronize()
     ms_step = pdist.max_over_ranks(e0.elapsed_time(e1) / args.steps, device=dev)
@@ -279,7 +284,7 @@ def run_cfg5(args, cfg):
     e2.record()
     for _ in range(max(1, min(args.steps, 3))):
         ad = a_host.to(dev, non_blocking=True)
-        cr, sr, _ = distchain.cos_sin_distributed(ad, gather_outputs=False)
+        cr, sr, _ = chain(ad, gather_outputs=False)
         c_host.copy_(cr, non_blocking=True)
         s_host.copy_(sr, non_blocking=True)
     e3.record()
@@ -299,7 +304,10 @@ def run_cfg5(args, cfg):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
             "config": {"workload": args.config, "description": desc, "n": n,
                        "k": st.k, "s": st.s, "gathers_per_step": st.gathers,
-                       "parallelism": f"block-row x{world}, NCCL all-gather per product"},
+                       "parallelism": (f"block-row x{world}, right operand read from peer "
+                                       "slabs inside the GEMM (symmetric memory, no gather)"
+                                       if peer else
+                                       f"block-row x{world}, NCCL all-gather per product")},
             "roofline": {"bound": "tensor", "achieved": tfl, "peak": peak, "unit": "TFLOP/s",
                          "frac": (tfl / peak) if peak else None, "traffic": None,
                          "kernel": "gemm_epi_kernel (slab mode) + all-gathers",
@@ -311,7 +319,7 @@ def run_cfg5(args, cfg):
             "clocks": clk.summary(), "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
 
 
@@ -532,6 +540,9 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-mode", choices=["gather", "peer"], default="gather",
+                    help="cfg5 only: NCCL all-gather per product, or the fused "
+                         "peer-memory product (symmetric memory)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warm-up raised to 3 (timing rule)")

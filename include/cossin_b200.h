@@ -218,6 +218,19 @@ int csm_slab_op(const void* op, double* slab, int M, int NP, int row0,
                 const double* rhs_full, const double* in0, int s, double tp,
                 int dbl_step, void* cos_out, void* sin_out, int out_f32,
                 void* scratch, void* stream);
+/* Fused all-gather + product: like csm_slab_op, but the right operand is
+ * NOT gathered -- rhs_slabs (HOST array of nparts pointers) holds each
+ * rank's slab base, peer pointers over NVLink (e.g. from torch symmetric
+ * memory), row block j of slot op.rhs living in rhs_slabs[j].  The GEMM's
+ * cp.async stages stream those rows straight from the owning GPU, so the
+ * transfer overlaps the math tile by tile.  Requires nparts * M == NP.
+ * The caller orders steps with a cross-rank barrier (all writers of the
+ * operand done before any reader starts). */
+int csm_slab_op_peer(const void* op, double* slab, int M, int NP, int row0,
+                     const double* const* rhs_slabs, int nparts,
+                     const double* in0, int s, double tp, int dbl_step,
+                     void* cos_out, void* sin_out, int out_f32, void* scratch,
+                     void* stream);
 
 /* ---- Measurement helpers (not part of the reference surface) ------------
  * csm_fp64_peak: time a DMMA (mma.sync m8n8k4 f64) throughput loop on the

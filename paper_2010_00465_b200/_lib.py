@@ -62,6 +62,8 @@ SIGNATURES = {
     "csm_doubling_program": (_i32, [_i32, _i32, _i32, _i32, _vp]),
     "csm_slab_op": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _dp, _i32, _vp, _vp,
                            _i32, _vp, _vp]),
+    "csm_slab_op_peer": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _dp, _i32,
+                                _vp, _vp, _i32, _vp, _vp]),
     "csm_profile_enable": (_i32, [_i32]),
     "csm_profile_collect": (_i32, [_vp, _vp]),
 }

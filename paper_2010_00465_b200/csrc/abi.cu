@@ -45,7 +45,7 @@ size_t slab_scratch_bytes();
 cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
                     const double* rhs_full, const double* in0, int s, double tp, int dbl_step,
                     void* cout, void* sout, int out_f32, void* scratch, cudaStream_t stream,
-                    int64_t* launches);
+                    int64_t* launches, const double* const* parts_host, int nparts);
 cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void* c_out,
                       void* s_out, int64_t batch, int n, const int32_t* dK, const int32_t* dS,
                       const int32_t* dStatus, void* ws, cudaStream_t stream, int64_t* launches,
@@ -482,8 +482,27 @@ int csm_slab_op(const void* op, double* slab, int M, int NP, int row0, const dou
   if (rc) return rc;
   cudaError_t e = csm::slab_op(op, slab, M, NP, row0, rhs_full, in0, s, tp, dbl_step, cos_out,
                                sin_out, out_f32, scratch, static_cast<cudaStream_t>(stream),
-                               &g_launches);
+                               &g_launches, nullptr, 0);
   if (e != cudaSuccess) return cuda_fail(e, "slab op");
+  return CSM_SUCCESS;
+}
+
+int csm_slab_op_peer(const void* op, double* slab, int M, int NP, int row0,
+                     const double* const* rhs_slabs, int nparts, const double* in0, int s,
+                     double tp, int dbl_step, void* cos_out, void* sin_out, int out_f32,
+                     void* scratch, void* stream) {
+  g_launches = 0;
+  if (!op || !slab || !rhs_slabs || !scratch) return fail(CSM_ERR_ARG, "null pointer argument");
+  if (M <= 0 || NP <= 0 || M % 64 || NP % 64 || nparts <= 0 || nparts > 64 || nparts * M != NP)
+    return fail(CSM_ERR_ARG, "need M, NP multiples of 64 and nparts * M == NP (<= 64 parts)");
+  for (int i = 0; i < nparts; ++i)
+    if (!rhs_slabs[i]) return fail(CSM_ERR_ARG, "null peer slab");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaError_t e = csm::slab_op(op, slab, M, NP, row0, nullptr, in0, s, tp, dbl_step, cos_out,
+                               sin_out, out_f32, scratch, static_cast<cudaStream_t>(stream),
+                               &g_launches, rhs_slabs, nparts);
+  if (e != cudaSuccess) return cuda_fail(e, "peer slab op");
   return CSM_SUCCESS;
 }
 

@@ -99,6 +99,11 @@ struct LaunchArgs {
   // row0 = 0, rhs_full = null.
   const double* rhs_full;
   int M, row0;
+  // Peer mode (fused all-gather): the right operand's row block j lives in
+  // rank j's slab, rhs_parts[j] = that slab's base (a peer pointer over
+  // NVLink); the product streams its rows straight from the owner, tile by
+  // tile, instead of reading an all-gathered copy.  Null otherwise.
+  const double* const* rhs_parts;
 };
 
 // One 64x64 output tile of one matrix: acc = L R over the full NP-deep
@@ -139,6 +144,15 @@ __global__ void __launch_bounds__(THREADS, 4) gemm_epi_kernel(const LaunchArgs a
     };
     const double* L = slot(op.lhs) + static_cast<size_t>(tm) * BM * NP;
     const double* R = (args.rhs_full ? args.rhs_full : slot(op.rhs)) + static_cast<size_t>(tn) * BN;
+    // row k0 of the right operand (a BK-row stage never crosses a part: M % 64 == 0)
+    auto rhs_rows = [&](int k0) -> const double* {
+      if (args.rhs_parts) {
+        const int part = k0 / M;
+        return args.rhs_parts[part] + static_cast<size_t>(op.rhs) * slotsz +
+               static_cast<size_t>(k0 - part * M) * NP + static_cast<size_t>(tn) * BN;
+      }
+      return R + static_cast<size_t>(k0) * NP;
+    };
 
     auto load_stage = [&](int stage, int k0) {
       double* as = As + stage * A_STAGE;
@@ -149,11 +163,12 @@ __global__ void __launch_bounds__(THREADS, 4) gemm_epi_kernel(const LaunchArgs a
         const int r = p / (BK / 2), c = (p - r * (BK / 2)) * 2;
         cp16(as + r * LDA + c, L + static_cast<size_t>(r) * NP + k0 + c);
       }
+      const double* Rk = rhs_rows(k0);
 #pragma unroll
       for (int i = 0; i < (BK * BN / 2) / THREADS; ++i) {
         const int p = tid + i * THREADS;
         const int r = p / (BN / 2), c = (p - r * (BN / 2)) * 2;
-        cp16(bs + r * LDB + c, R + static_cast<size_t>(k0 + r) * NP + c);
+        cp16(bs + r * LDB + c, Rk + static_cast<size_t>(r) * NP + c);
       }
     };
 
@@ -828,6 +843,7 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     A.M = NP;
     A.row0 = 0;
     A.rhs_full = nullptr;
+    A.rhs_parts = nullptr;
     prof_begin(stream);
     for (size_t pi = 0; pi < plans.size(); ++pi) {
       const LaunchPlan& L = plans[pi];
@@ -913,26 +929,31 @@ void doubling_program(int c0, int s0, int c1, int s1, void* ops_out) {
   out[1] = v[1];
 }
 
-size_t slab_scratch_bytes() { return sizeof(Op) + 64; }
+constexpr int kMaxParts = 64;
+size_t slab_scratch_bytes() { return sizeof(Op) + 64 + kMaxParts * sizeof(double*); }
 
 // Run one Op on a block-row slab: out rows = L_rows * rhs_full (+ epilogue).
 // scratch: device buffer of slab_scratch_bytes() (op descriptor, s, t').
 cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
                     const double* rhs_full, const double* in0, int s, double tp, int dbl_step,
                     void* cout, void* sout, int out_f32, void* scratch, cudaStream_t stream,
-                    int64_t* launches) {
+                    int64_t* launches, const double* const* parts_host, int nparts) {
   if (M % tk::BM != 0 || NP % tk::BN != 0) return cudaErrorInvalidValue;
+  if (nparts < 0 || nparts > kMaxParts || (nparts > 0 && nparts * M != NP))
+    return cudaErrorInvalidValue;
   struct alignas(16) Staged {
     Op op;
     int32_t idx, s, pad0, pad1;
     double tp;
+    const double* parts[kMaxParts];
   };
-  static_assert(sizeof(Staged) <= sizeof(Op) + 64, "scratch layout");
+  static_assert(sizeof(Staged) <= sizeof(Op) + 64 + kMaxParts * sizeof(double*), "scratch layout");
   Staged h{};
   std::memcpy(&h.op, op_host, sizeof(Op));
   h.idx = 0;
   h.s = s;
   h.tp = tp;
+  for (int i = 0; i < nparts; ++i) h.parts[i] = parts_host[i];
   cudaError_t e = cudaMemcpyAsync(scratch, &h, sizeof(Staged), cudaMemcpyHostToDevice, stream);
   if (e != cudaSuccess) return e;
   e = cudaStreamSynchronize(stream);  // h lives on this stack frame
@@ -963,7 +984,8 @@ cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
   A.total = 1;
   A.item_base = 0;
   A.seg[0] = {0, 0, 0};
-  A.rhs_full = rhs_full;
+  A.rhs_full = nparts > 0 ? nullptr : rhs_full;
+  A.rhs_parts = nparts > 0 ? d->parts : nullptr;
   A.M = M;
   A.row0 = row0;
   dim3 grid(static_cast<unsigned>((M / tk::BM) * (NP / tk::BN)), 1, 1);

@@ -6,7 +6,10 @@ each, one process per GPU).  Every product of the chain is
     out_rows = L_rows @ R_full,
 
 so the only exchange is an all-gather of the current right operand over
-NVLink (NCCL, through torch.distributed).  Polynomials in A commute, which
+NVLink (NCCL, through torch.distributed) -- or, in peer mode, no gather at
+all: the slabs live in torch symmetric memory and csm_slab_op_peer streams
+the right operand's row blocks straight from the owning GPUs inside the
+GEMM (cos_sin_distributed_peer below).  Polynomials in A commute, which
 removes gathers: the input A is replicated on every rank, so A A and the
 final sine product (computed as sc A instead of A sc) need none, and a
 gathered operand is cached until its slot is overwritten -- the degree-12
@@ -114,7 +117,22 @@ def _device_select(a, precision: Precision):
     return int(k[0]), int(s[0])
 
 
+def _device_slab_op_peer(op: OpView, slab, M, n, row0, rhs_slabs, in0, s, dbl_step,
+                         cos_rows, sin_rows, scratch, stream):
+    import torch
+    vp = ctypes.c_void_p
+    raw = (ctypes.c_char * len(op.raw)).from_buffer(op.raw)
+    ptrs = [x if isinstance(x, int) else x.data_ptr() for x in rhs_slabs]
+    parts = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    _lib.check(_lib.lib().csm_slab_op_peer(
+        raw, vp(slab.data_ptr()), M, n, row0, parts, len(rhs_slabs), vp(in0.data_ptr()), s,
+        0.0, dbl_step, vp(cos_rows.data_ptr()), vp(sin_rows.data_ptr()), 0,
+        vp(scratch.data_ptr()),
+        vp(int((stream or torch.cuda.current_stream()).cuda_stream))), "csm_slab_op_peer")
+
+
 slab_op = _device_slab_op
+slab_op_peer = _device_slab_op_peer
 select = _device_select
 
 
@@ -195,6 +213,136 @@ def cos_sin_distributed(a, precision: Precision = Precision.DOUBLE, *,
         for w in written:
             cache.pop(w, None)
         c0, s0, c1, s1 = c1, s1, c0, s0
+    if not gather_outputs or world == 1:
+        return cos_rows, sin_rows, stats
+    cfull = torch.empty((n, n), dtype=torch.float64, device=dev)
+    sfull = torch.empty_like(cfull)
+    dist.all_gather_into_tensor(cfull, cos_rows, group=group)
+    dist.all_gather_into_tensor(sfull, sin_rows, group=group)
+    return cfull, sfull, stats
+
+
+# ---------------------------------------------------------------------------
+# Peer mode: the all-gather fused into the product (no gathered copies).
+
+def _peer_rank_program(a, precision, rank: int, world: int, slab, rhs_slabs,
+                       cos_rows, sin_rows, scratch, stats: DistStats):
+    """One rank's chain as a generator that yields at every point where all
+    ranks must have finished writing before anyone reads (a cross-rank
+    barrier).  A is replicated, so products whose right operand is A (and
+    A sc, run as sc A) read it locally; every other right operand is read
+    row block by row block from its owner through rhs_slabs."""
+    n = int(a.shape[0])
+    M, row0 = n // world, rank * (n // world)
+    in0 = a[row0:row0 + M]
+    k, s = stats.k, stats.s
+    steps, cos_slot, sin_slot = chain_program(k, fold=True)
+
+    def run(op: OpView, dbl_step: int):
+        if op.lhs == 0 and op.rhs != 0:  # A X = X A: polynomials in A commute
+            op = op.swapped()
+        if op.rhs == 0:
+            slab_op(op, slab, M, n, row0, a, in0, s, dbl_step, cos_rows, sin_rows,
+                    scratch, None)
+        else:
+            slab_op_peer(op, slab, M, n, row0, rhs_slabs, in0, s, dbl_step, cos_rows,
+                         sin_rows, scratch, None)
+        if rank == 0:
+            stats.products += 1
+
+    for step in steps:
+        for op in step:
+            run(op, -1)
+        yield
+    c0, s0 = cos_slot, sin_slot
+    free = [i for i in range(1, NSLOT) if i not in (c0, s0)]
+    c1, s1 = free[0], free[1]
+    for i in range(s):
+        for op in doubling_program(c0, s0, c1, s1):
+            run(op, i)
+        yield
+        c0, s0, c1, s1 = c1, s1, c0, s0
+
+
+def cos_sin_virtual_ranks(a, world: int, precision: Precision = Precision.DOUBLE):
+    """The peer-mode chain with `world` virtual ranks in ONE process (all
+    slabs on this device, stepped in lock-step): exercises the multi-part
+    right-operand addressing of csm_slab_op_peer and the step/barrier
+    structure on a single GPU.  Returns (cos, sin, stats)."""
+    import torch
+    n = int(a.shape[0])
+    if a.shape != (n, n) or a.dtype != torch.float64:
+        raise ValueError("expected a square float64 tensor")
+    if n % (64 * world):
+        raise ValueError(f"n={n} must be a multiple of 64 x world ({world})")
+    a = a.contiguous()
+    M = n // world
+    k, s = select(a, precision)
+    dev = a.device
+    slabs = [torch.empty((NSLOT, M, n), dtype=torch.float64, device=dev) for _ in range(world)]
+    cos = torch.empty((n, n), dtype=torch.float64, device=dev)
+    sin = torch.empty_like(cos)
+    scratch = None
+    if dev.type == "cuda":
+        scratch = torch.empty(int(_lib.lib().csm_slab_scratch_bytes()), dtype=torch.uint8,
+                              device=dev)
+    stats = DistStats(k, s, 0, 0)
+    gens = [_peer_rank_program(a, precision, r, world, slabs[r], slabs,
+                               cos[r * M:(r + 1) * M], sin[r * M:(r + 1) * M], scratch, stats)
+            for r in range(world)]
+    done = False
+    while not done:
+        for g in gens:  # one step of every rank, then the (implicit) barrier
+            try:
+                next(g)
+            except StopIteration:
+                done = True
+    return cos, sin, stats
+
+
+_PEER_CTX: dict = {}
+
+
+def cos_sin_distributed_peer(a, precision: Precision = Precision.DOUBLE, *, group=None,
+                             gather_outputs: bool = True):
+    """cos_sin_distributed with the all-gather fused into the product: the
+    slabs are allocated in torch symmetric memory (NVLink peer mappings), a
+    device-side barrier separates dependent steps, and every product reads
+    the remote row blocks of its right operand directly.  One process per
+    GPU; needs peer access between the GPUs of the group."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm_mem
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = int(a.shape[0])
+    if a.shape != (n, n) or a.dtype != torch.float64:
+        raise ValueError("expected a square float64 tensor")
+    if n % (64 * world):
+        raise ValueError(f"n={n} must be a multiple of 64 x world ({world})")
+    a = a.contiguous()
+    M = n // world
+    k, s = select(a, precision)
+    dev = a.device
+    grp = group if group is not None else dist.group.WORLD
+    key = (n, world, str(dev), grp.group_name)
+    ctx = _PEER_CTX.get(key)
+    if ctx is None:  # symmetric slabs are allocated and mapped once per shape
+        slab = symm_mem.empty((NSLOT, M, n), dtype=torch.float64, device=dev)
+        hdl = symm_mem.rendezvous(slab, grp.group_name)
+        ctx = (slab, hdl, [int(p) for p in hdl.buffer_ptrs],
+               torch.empty(int(_lib.lib().csm_slab_scratch_bytes()), dtype=torch.uint8,
+                           device=dev))
+        _PEER_CTX[key] = ctx
+        hdl.barrier(channel=0)  # every peer mapping is live
+    slab, hdl, ptrs, scratch = ctx
+    cos_rows = torch.empty((M, n), dtype=torch.float64, device=dev)
+    sin_rows = torch.empty_like(cos_rows)
+    stats = DistStats(k, s, 0, 0)
+    hdl.barrier(channel=0)  # no rank still reads the previous call's slabs
+    for _ in _peer_rank_program(a, precision, rank, world, slab, ptrs, cos_rows, sin_rows,
+                                scratch, stats):
+        hdl.barrier(channel=0)  # this step's rows are written on every rank
     if not gather_outputs or world == 1:
         return cos_rows, sin_rows, stats
     cfull = torch.empty((n, n), dtype=torch.float64, device=dev)

@@ -43,6 +43,36 @@ def np_slab_op(op, slab, M, n, row0, rhs_full, in0, s, dbl_step, cos_rows,
             (cos_rows if final == 1 else sin_rows).copy_(v)
 
 
+def np_slab_op_peer(op, slab, M, n, row0, rhs_slabs, in0, s, dbl_step, cos_rows,
+                    sin_rows, scratch, stream):
+    """Test double of csm_slab_op_peer: row block j of the right operand
+    comes from rank j's slab (no gathered copy exists)."""
+    rhs = torch.cat([x[op.rhs] for x in rhs_slabs], dim=0)
+    np_slab_op(op, slab, M, n, row0, rhs, in0, s, dbl_step, cos_rows, sin_rows, scratch,
+               stream)
+
+
+def test_peer_mode_virtual_ranks_cpu():
+    """Peer mode's step/barrier structure with 4 lock-stepped virtual ranks
+    and test doubles: no gathers, every rank's rows of cos/sin correct."""
+    from paper_2010_00465_b200 import distchain
+    old = (distchain.slab_op, distchain.slab_op_peer, distchain.select)
+    distchain.slab_op, distchain.slab_op_peer, distchain.select = (
+        np_slab_op, np_slab_op_peer, _np_select)
+    try:
+        n = 256
+        g = np.random.default_rng(1).standard_normal((n, n))
+        a = torch.from_numpy(8.0 * (g + g.T) / (2.0 * np.sqrt(n)))
+        c, s, st = distchain.cos_sin_virtual_ranks(a, 4)
+    finally:
+        distchain.slab_op, distchain.slab_op_peer, distchain.select = old
+    rc, rs, k, sc = orc.cos_sin(a.numpy())
+    assert (st.k, st.s, st.gathers) == (k, sc, 0)
+    assert st.products == k + 2 * sc
+    assert rel1(c.numpy(), rc) <= 1e-12
+    assert rel1(s.numpy(), rs) <= 1e-12
+
+
 def _np_select(a, precision):
     return orc.select(orc.norm1(a.numpy()))
 
@@ -114,3 +144,35 @@ def test_block_row_single_gpu_against_oracle(cuda):
     assert rel1(c.cpu().numpy(), c_ref) <= 2e-11
     assert rel1(s.cpu().numpy(), s_ref) <= 2e-11
     assert rel1(c.cpu().numpy(), single.result.cos_part) <= 2e-11
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_mode_virtual_ranks_gpu(cuda, world):
+    """csm_slab_op_peer with the right operand split over `world` slabs (all
+    on this GPU): bit-identical to the gather-mode chain, and the oracle."""
+    from paper_2010_00465_b200 import distchain
+    n = 512
+    g = np.random.default_rng(3).standard_normal((n, n))
+    a_np = 20.0 * (g + g.T) / (2.0 * np.sqrt(n))
+    a = torch.from_numpy(a_np).cuda()
+    c, s, st = distchain.cos_sin_virtual_ranks(a, world)
+    c1, s1, st1 = distchain.cos_sin_distributed(a)
+    assert (st.k, st.s) == (st1.k, st1.s) and st.gathers == 0
+    assert torch.equal(c, c1) and torch.equal(s, s1)
+    rc, rs, k, sc = orc.cos_sin(a_np)
+    assert rel1(c.cpu().numpy(), rc) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_peer_mode_symmetric_memory_single_rank(cuda):
+    """cos_sin_distributed_peer through torch symmetric memory (NCCL, one
+    rank, in a subprocess): allocation, rendezvous, device barriers and
+    the peer-pointer product; bit-identical to the gather-mode chain."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "peer_smoke.py")],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert "peer == gather: True True" in out.stdout, out.stdout + out.stderr[-2000:]
