@@ -26,7 +26,7 @@ from .api import (
     wave_sin34,
     write_matrix,
 )
-from . import plan, verify
+from . import corpus, plan, verify
 from .plan import BatchPlan
 from .records import (
     PADE_TABLE,

@@ -11,6 +11,7 @@ Reference entry points exercised (paths under /root/reference):
   wave_cos_sin   pkg/src/cossinm/driver.py:126-146
   norm1          pkg/src/cossinm/matcore.py:100-104
   pade_cos_sin   pkg/src/cossinm/driver.py:149-164
+  bench corpus   pkg/src/cossinm/gallery.py:186-220, cli.py:128-163
 """
 from __future__ import annotations
 
@@ -255,6 +256,38 @@ def gen_pade(rng):
     np.savez_compressed(os.path.join(OUT, "pade.npz"), **out)
 
 
+def gen_corpus():
+    """The reference's own bench corpus (gallery.py:186-220) at a small spec,
+    with its per-matrix (k, s, products) for cos_sin and pade_cos_sin and
+    its errors against reference_cos_sin (cli.py:128-163)."""
+    from cossinm.gallery import CorpusSpec, generate_corpus
+    from cossinm.verify import reference_cos_sin, relative_error_2
+    spec = CorpusSpec(dimension_cap=16, count_per_class=(24, 24, 12, 9), seed=0)
+    mats, tags, dims = [], [], []
+    rec = {k: [] for k in ("t_k", "t_s", "t_prod", "t_ec", "t_es", "p_s", "p_prod",
+                           "p_ec", "p_es")}
+    for m, tag in generate_corpus(spec):
+        mats.append(m.ravel())
+        tags.append(tag)
+        dims.append(m.shape[0])
+        with np.errstate(over="ignore", invalid="ignore"):
+            ref = reference_cos_sin(m)
+            t = cossinm.cos_sin(m)
+            p = cossinm.pade_cos_sin(m)
+        rec["t_k"].append(t.scheme_used.k_products)
+        rec["t_s"].append(t.scaling_exponent)
+        rec["t_prod"].append(float(t.total_products))
+        rec["t_ec"].append(relative_error_2(t.result.cos_part, ref.cos_part))
+        rec["t_es"].append(relative_error_2(t.result.sin_part, ref.sin_part))
+        rec["p_s"].append(p.scaling_exponent)
+        rec["p_prod"].append(float(p.total_products))
+        rec["p_ec"].append(relative_error_2(p.result.cos_part, ref.cos_part))
+        rec["p_es"].append(relative_error_2(p.result.sin_part, ref.sin_part))
+    out = {"data": np.concatenate(mats), "dims": np.array(dims), "tags": np.array(tags)}
+    out.update({k: np.array(v) for k, v in rec.items()})
+    np.savez_compressed(os.path.join(OUT, "corpus.npz"), **out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     rng = np.random.default_rng(20100465)
@@ -265,6 +298,7 @@ def main():
     gen_extras(np.random.default_rng(77))
     gen_ddref(np.random.default_rng(2010))
     gen_pade(np.random.default_rng(88))
+    gen_corpus()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 
