@@ -37,6 +37,7 @@ cudaError_t launch_schedule(const int32_t* K, const int32_t* S, const int32_t* s
                             int64_t batch, int* bins, int32_t* order, cudaStream_t stream,
                             int64_t* launches);
 size_t tiled_workspace_bytes(int64_t batch, int n);
+int k1c_resident_sms();
 size_t op_bytes();
 int chain_program(bool wave, int k, bool fold, void* ops_out, int max_ops, int32_t* step_nops,
                   int max_steps, int32_t* cos_slot, int32_t* sin_slot);
@@ -64,16 +65,17 @@ namespace {
 thread_local bool g_prof = false;
 thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_ev;
 thread_local cudaEvent_t g_prof_open = nullptr;
+thread_local bool g_prof_hold = false;  // an enclosing interval is open
 }  // namespace
 
 namespace csm {
 void prof_begin(cudaStream_t stream) {
-  if (!g_prof) return;
+  if (!g_prof || g_prof_hold) return;
   if (cudaEventCreate(&g_prof_open) != cudaSuccess) { g_prof_open = nullptr; return; }
   cudaEventRecord(g_prof_open, stream);
 }
 void prof_end(cudaStream_t stream) {
-  if (!g_prof || !g_prof_open) return;
+  if (!g_prof || g_prof_hold || !g_prof_open) return;
   cudaEvent_t e1;
   if (cudaEventCreate(&e1) != cudaSuccess) return;
   cudaEventRecord(e1, stream);
@@ -172,6 +174,31 @@ int fused_max() {
   return v;
 }
 
+// Matrices of a 64 < n <= 128 batch given to the side tiled chain.
+int64_t side_count(int64_t batch) {
+  static const double share = [] {
+    const char* e = std::getenv("CSM_SIDE_SHARE");
+    const double x = e ? std::atof(e) : 0.08;
+    return x < 0.0 ? 0.0 : (x > 0.5 ? 0.5 : x);
+  }();
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int idle = sms - csm::k1c_resident_sms();
+  if (share <= 0.0 || idle < 8 || batch < 1024) return 0;
+  return static_cast<int64_t>(share * static_cast<double>(batch));
+}
+
+// One non-blocking side stream per device (created on first use).
+cudaStream_t side_stream() {
+  static cudaStream_t streams[32] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 32) dev = 31;
+  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  return streams[dev];
+}
+
 // After K/S/status are on the device: run K1/K1c or the tiled chain.
 int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, void* s,
                 int64_t batch, int n, const int32_t* K, const int32_t* S, const int32_t* st,
@@ -179,13 +206,41 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
   if (n == 0 || batch == 0) return CSM_SUCCESS;
   cudaError_t e;
   if (n <= fused_max()) {
-    e = csm::launch_schedule(K, S, st, batch, w.bins, w.order, stream, &g_launches);
+    // K1c leaves the SMs outside whole 4-SM clusters idle (GPC boundaries):
+    // a share of the batch sized to them runs the tiled chain concurrently
+    // on a side stream (CSM_SIDE_SHARE, default 0.08; 0 disables).
+    int64_t bf = batch;
+    if (n > 64) bf = batch - side_count(batch);
+    cudaEvent_t ev_sel = nullptr, ev_done = nullptr;
+    if (bf < batch) {
+      cudaEventCreateWithFlags(&ev_sel, cudaEventDisableTiming);
+      cudaEventRecord(ev_sel, stream);  // (k, s, status) are final here
+    }
+    e = csm::launch_schedule(K, S, st, bf, w.bins, w.order, stream, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "schedule kernels");
     csm::prof_begin(stream);
-    e = csm::launch_fused64(dtype, wave, a, c, s, t, K, S, st, w.order, batch, n, stream);
-    csm::prof_end(stream);
+    e = csm::launch_fused64(dtype, wave, a, c, s, t, K, S, st, w.order, bf, n, stream);
     if (e != cudaSuccess) return cuda_fail(e, "fused64 launch");
     ++g_launches;
+    if (bf < batch) {
+      cudaStream_t side = side_stream();
+      cudaStreamWaitEvent(side, ev_sel, 0);
+      const size_t in_elt = dtype == CSM_F64 ? 8 : 4, out_elt = dtype == CSM_F32 ? 4 : 8;
+      const size_t nn = static_cast<size_t>(n) * n;
+      g_prof_hold = true;
+      e = csm::run_tiled(dtype, wave, static_cast<const char*>(a) + bf * nn * in_elt,
+                         t ? t + bf : nullptr, static_cast<char*>(c) + bf * nn * out_elt,
+                         static_cast<char*>(s) + bf * nn * out_elt, batch - bf, n, K + bf, S + bf,
+                         st + bf, w.tiled, side, &g_launches, 0);
+      g_prof_hold = false;
+      if (e != cudaSuccess) return cuda_fail(e, "side tiled chain");
+      cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
+      cudaEventRecord(ev_done, side);
+      cudaStreamWaitEvent(stream, ev_done, 0);
+      cudaEventDestroy(ev_sel);
+      cudaEventDestroy(ev_done);
+    }
+    csm::prof_end(stream);
   } else {
     e = csm::run_tiled(dtype, wave, a, t, c, s, batch, n, K, S, st, w.tiled, stream, &g_launches,
                        0);

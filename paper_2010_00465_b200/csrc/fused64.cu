@@ -916,6 +916,33 @@ static cudaError_t launch_fused(int dtype, bool wave, const void* a, void* c, vo
               : launch_one<CL, float, float, false>(a, c, s, t, k, sx, st, order, batch, n, sms, stream);
 }
 
+// SMs the K1c grid occupies (4 x co-resident clusters; the rest of the GPU
+// is free for concurrent work).
+int k1c_resident_sms() {
+  static int cached = -1;
+  if (cached >= 0) return cached;
+  auto kern = f64k::fused64_kernel<4, double, double, false>;
+  const size_t smem = fused64_smem_bytes();
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess)
+    return 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 4;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(f64k::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.gridDim = dim3(4 * 32);
+  int active = 0;
+  if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) != cudaSuccess) return 0;
+  cached = 4 * active;
+  return cached;
+}
+
 // Launch K1 (n <= 64) or K1c (64 < n <= 128) for a batch whose (k, s,
 // status) and cost-sorted order[] are already on the device.
 cudaError_t launch_fused64(int dtype, bool wave, const void* a, void* c,

@@ -216,6 +216,26 @@ def test_cluster_kernel_many_turns(cuda):
     assert (rep.s == 0).any() and (rep.s > 3).any()
 
 
+def test_cluster_kernel_with_side_chain(cuda):
+    """A batch large enough that the tail runs on the concurrent side tiled
+    chain (the SMs K1c's 4-SM clusters leave idle): both parts correct,
+    float32 storage too."""
+    rng = np.random.default_rng(270)
+    a = cfg2_like(rng, 1100, n=100, lo=-3, hi=2.0)
+    rep = csm.cos_sin_batched(a)
+    for i in list(range(0, 1100, 97)) + list(range(1020, 1100, 9)) + [1099]:
+        c, s, k, sc = orc.cos_sin(a[i])
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc), i
+        assert rel1(rep.cos_part[i], c) <= TOL64, i
+        assert rel1(rep.sin_part[i], s) <= TOL64, i
+    a32 = cfg3_like(rng, 1030, n=128)
+    rep = csm.cos_sin_batched(a32, csm.Precision.SINGLE)
+    for i in (0, 500, 1000, 1029):
+        c, s, k, sc = orc.cos_sin(a32[i], "single")
+        assert rel1(rep.cos_part[i], c) <= TOL32, i
+        assert rel1(rep.sin_part[i], s) <= TOL32, i
+
+
 @pytest.mark.parametrize("n", [64, 99, 128, 256])
 def test_batched_float32(cuda, n):
     """configs[2] variant: float32 storage, float64 compute, SINGLE table."""
