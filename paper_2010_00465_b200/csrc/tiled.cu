@@ -43,6 +43,10 @@ constexpr int NSLOT = 9;
 constexpr int MAXT = 8;
 constexpr int MAXSEG = 8;
 
+#ifndef CSM_TILED_PB
+#define CSM_TILED_PB 4  // epilogue pairs in flight per thread
+#endif
+
 // Term sources
 constexpr int SRC_ACC = -1, SRC_I = -2, SRC_OUT0 = -3;  // OUTj = -3 - j
 // Output scale modes
@@ -109,7 +113,10 @@ struct LaunchArgs {
 // One 64x64 output tile of one matrix: acc = L R over the full NP-deep
 // contraction, then the op's linear combinations from the staged
 // accumulator tile with row-contiguous (coalesced) global reads and writes.
-__global__ void __launch_bounds__(THREADS, 4) gemm_epi_kernel(const LaunchArgs args) {
+#ifndef CSM_TILED_MINB
+#define CSM_TILED_MINB 4  // resident CTAs per SM the register budget targets
+#endif
+__global__ void __launch_bounds__(THREADS, CSM_TILED_MINB) gemm_epi_kernel(const LaunchArgs args) {
   extern __shared__ __align__(16) double sm[];
   __shared__ Op op;
   __shared__ int sh_b;
@@ -225,59 +232,96 @@ __global__ void __launch_bounds__(THREADS, 4) gemm_epi_kernel(const LaunchArgs a
     const bool final_now = args.dbl_step < 0 ? (s_b == 0) : (s_b == args.dbl_step + 1);
     const int nout = op.nout;
     const int r0 = tm * BM, c0 = tn * BN;
-#pragma unroll 2
-    for (int p = tid; p < BM * BN / 2; p += THREADS) {
-      const int rr = p >> 5, cc = (p & 31) * 2;  // 32 pairs per tile row
-      const int r = r0 + rr, c = c0 + cc;
-      const size_t off = static_cast<size_t>(r) * NP + c;
-      const double2 av = *reinterpret_cast<const double2*>(E + rr * LDE + cc);
-      const int rg = r + args.row0;  // global row (slab mode)
-      const double i0 = (rg == c) ? 1.0 : 0.0, i1 = (rg == c + 1) ? 1.0 : 0.0;
-      double o0[2] = {0.0, 0.0}, o1[2] = {0.0, 0.0};  // outputs 0 and 1 of this pair
+    // PB pairs per thread at a time: every slot-sourced term issues PB
+    // independent loads before its FMAs, so the workspace reads (HBM for
+    // large batches) overlap instead of exposing one latency per term.
+    constexpr int PB = CSM_TILED_PB;
+    static_assert((BM * BN / 2) % (PB * THREADS) == 0, "pair groups tile the output");
+    for (int p0 = tid; p0 < BM * BN / 2; p0 += PB * THREADS) {
+      size_t off[PB];
+      int ecol[PB];
+      double o0[PB][2], o1[PB][2];  // outputs 0 and 1 (OUTj terms of later outputs)
+#pragma unroll
+      for (int m = 0; m < PB; ++m) {
+        const int p = p0 + m * THREADS;
+        const int rr = p >> 5, cc = (p & 31) * 2;  // 32 pairs per tile row
+        off[m] = static_cast<size_t>(r0 + rr) * NP + c0 + cc;
+        ecol[m] = rr * LDE + cc;
+        o0[m][0] = o0[m][1] = o1[m][0] = o1[m][1] = 0.0;
+      }
       for (int q = 0; q < nout; ++q) {
         const OutSpec& os = op.out[q];
-        double v0 = 0.0, v1 = 0.0;
+        double v[PB][2];
+#pragma unroll
+        for (int m = 0; m < PB; ++m) v[m][0] = v[m][1] = 0.0;
         for (int tt = 0; tt < os.nterms; ++tt) {
           const int src = os.t[tt].src;
           const double cf = os.t[tt].c;
-          double x0, x1;
           if (src >= 0) {
-            const double2 v = *reinterpret_cast<const double2*>(slot(src) + off);
-            x0 = v.x; x1 = v.y;
-          } else if (src == SRC_ACC) {
-            x0 = av.x; x1 = av.y;
-          } else if (src == SRC_I) {
-            x0 = i0; x1 = i1;
-          } else if (src == SRC_OUT0) {
-            x0 = o0[0]; x1 = o0[1];
+            const double* sp = slot(src);
+            double2 x[PB];
+#pragma unroll
+            for (int m = 0; m < PB; ++m) x[m] = *reinterpret_cast<const double2*>(sp + off[m]);
+#pragma unroll
+            for (int m = 0; m < PB; ++m) {
+              v[m][0] = fma(cf, x[m].x, v[m][0]);
+              v[m][1] = fma(cf, x[m].y, v[m][1]);
+            }
           } else {
-            x0 = o1[0]; x1 = o1[1];
+#pragma unroll
+            for (int m = 0; m < PB; ++m) {
+              double x0, x1;
+              if (src == SRC_ACC) {
+                const double2 av = *reinterpret_cast<const double2*>(E + ecol[m]);
+                x0 = av.x; x1 = av.y;
+              } else if (src == SRC_I) {
+                const int p = p0 + m * THREADS;
+                const int rg = r0 + (p >> 5) + args.row0, c = c0 + (p & 31) * 2;
+                x0 = (rg == c) ? 1.0 : 0.0;
+                x1 = (rg == c + 1) ? 1.0 : 0.0;
+              } else if (src == SRC_OUT0) {
+                x0 = o0[m][0]; x1 = o0[m][1];
+              } else {
+                x0 = o1[m][0]; x1 = o1[m][1];
+              }
+              v[m][0] = fma(cf, x0, v[m][0]);
+              v[m][1] = fma(cf, x1, v[m][1]);
+            }
           }
-          v0 = fma(cf, x0, v0);
-          v1 = fma(cf, x1, v1);
         }
         if (os.scale != SC_NONE) {
           const double sc = os.scale == SC_TP ? sc_tp : (os.scale == SC_F ? sc_f : sc_f2);
-          v0 *= sc;
-          v1 *= sc;
+#pragma unroll
+          for (int m = 0; m < PB; ++m) { v[m][0] *= sc; v[m][1] *= sc; }
         }
-        if (q == 0) { o0[0] = v0; o0[1] = v1; }
-        if (q == 1) { o1[0] = v0; o1[1] = v1; }
-        *reinterpret_cast<double2*>(base + os.slot * slotsz + off) = make_double2(v0, v1);
-        if (os.final != FIN_NONE && final_now && r < n) {
+#pragma unroll
+        for (int m = 0; m < PB; ++m) {
+          if (q == 0) { o0[m][0] = v[m][0]; o0[m][1] = v[m][1]; }
+          if (q == 1) { o1[m][0] = v[m][0]; o1[m][1] = v[m][1]; }
+          *reinterpret_cast<double2*>(base + os.slot * slotsz + off[m]) =
+              make_double2(v[m][0], v[m][1]);
+        }
+        if (os.final != FIN_NONE && final_now) {
           void* dst = os.final == FIN_COS ? args.cout : args.sout;
-          const size_t o = static_cast<size_t>(b) * nn + static_cast<size_t>(r) * n + c;
-          if (args.out_f32) {
-            float* d = static_cast<float*>(dst);
-            if (c < n) d[o] = static_cast<float>(v0);
-            if (c + 1 < n) d[o + 1] = static_cast<float>(v1);
-          } else {
-            double* d = static_cast<double*>(dst);
-            if (c + 1 < n && ((o & 1) == 0)) {
-              *reinterpret_cast<double2*>(d + o) = make_double2(v0, v1);
+#pragma unroll
+          for (int m = 0; m < PB; ++m) {
+            const int p = p0 + m * THREADS;
+            const int r = r0 + (p >> 5), c = c0 + (p & 31) * 2;
+            if (r >= n) continue;
+            const double v0 = v[m][0], v1 = v[m][1];
+            const size_t o = static_cast<size_t>(b) * nn + static_cast<size_t>(r) * n + c;
+            if (args.out_f32) {
+              float* d = static_cast<float*>(dst);
+              if (c < n) d[o] = static_cast<float>(v0);
+              if (c + 1 < n) d[o + 1] = static_cast<float>(v1);
             } else {
-              if (c < n) d[o] = v0;
-              if (c + 1 < n) d[o + 1] = v1;
+              double* d = static_cast<double*>(dst);
+              if (c + 1 < n && ((o & 1) == 0)) {
+                *reinterpret_cast<double2*>(d + o) = make_double2(v0, v1);
+              } else {
+                if (c < n) d[o] = v0;
+                if (c + 1 < n) d[o + 1] = v1;
+              }
             }
           }
         }
