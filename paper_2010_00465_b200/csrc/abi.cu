@@ -178,7 +178,7 @@ int fused_max() {
 int64_t side_count(int64_t batch) {
   static const double share = [] {
     const char* e = std::getenv("CSM_SIDE_SHARE");
-    const double x = e ? std::atof(e) : 0.08;
+    const double x = e ? std::atof(e) : 0.12;
     return x < 0.0 ? 0.0 : (x > 0.5 ? 0.5 : x);
   }();
   int dev = 0, sms = 0;
@@ -208,7 +208,7 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
   if (n <= fused_max()) {
     // K1c leaves the SMs outside whole 4-SM clusters idle (GPC boundaries):
     // a share of the batch sized to them runs the tiled chain concurrently
-    // on a side stream (CSM_SIDE_SHARE, default 0.08; 0 disables).
+    // on a side stream (CSM_SIDE_SHARE, default 0.12; 0 disables).
     int64_t bf = batch;
     if (n > 64) bf = batch - side_count(batch);
     cudaEvent_t ev_sel = nullptr, ev_done = nullptr;
