@@ -296,6 +296,32 @@ def test_input_errors(cuda):
     assert np.all(np.isnan(rep.cos_part[1]))
 
 
+@pytest.mark.parametrize("n,count", [(100, 40), (128, 1200), (300, 12)])
+def test_bad_statuses_on_every_path(cuda, n, count):
+    """Non-finite entries, infinite norms and norm/theta overflow inside a
+    batch on K1c, K1c + side chain and the tiled chain: those matrices get
+    their status and NaN outputs, their neighbours stay exact."""
+    rng = np.random.default_rng(600 + n)
+    a = cfg2_like(rng, count, n=n, lo=-2, hi=1.0)
+    bad = {1: 1, count - 2: 1, count // 2: 2, count - 1: 3}
+    a[1, 3, 5] = math.nan
+    a[count - 2, 0, 0] = math.inf
+    a[count // 2, :, 0] = 1e308  # column sum overflows: non-finite norm
+    a[count - 1] = 0.0
+    a[count - 1, 0, 0] = 1.7e308  # finite norm, norm / theta overflows
+    rep = csm.cos_sin_batched(a, raise_on_error=False)
+    st = np.asarray(rep.status)
+    for i, code in bad.items():
+        assert st[i] == code, (i, st[i])
+        assert np.all(np.isnan(rep.cos_part[i])) and np.all(np.isnan(rep.sin_part[i]))
+    good = [i for i in range(count) if i not in bad]
+    assert np.all(st[good] == 0)
+    for i in good[:: max(1, len(good) // 6)]:
+        c, s, k, sc = orc.cos_sin(a[i])
+        assert rel1(rep.cos_part[i], c) <= TOL64, i
+        assert rel1(rep.sin_part[i], s) <= TOL64, i
+
+
 def test_empty_inputs(cuda):
     rep = csm.cos_sin(np.zeros((0, 0)))
     assert rep.result.cos_part.shape == (0, 0)
