@@ -466,21 +466,31 @@ __global__ void __launch_bounds__(256) pade_lu_solve_kernel(
     if (tid == 0) status[b] = kSingular;
     return;
   }
-  // getrs: unit-lower then upper triangular solve, one thread per column
+  // getrs: unit-lower then upper triangular solve, one thread per column;
+  // each dot product runs in 4 independent partial sums (the serial FMA
+  // chain, not memory, bounds this loop)
+  auto dot = [&](const double* row, const double* col, int q0, int q1) {
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+    int q = q0;
+    for (; q + 3 < q1; q += 4) {
+      p0 = fma(row[q], col[static_cast<size_t>(q) * NP], p0);
+      p1 = fma(row[q + 1], col[static_cast<size_t>(q + 1) * NP], p1);
+      p2 = fma(row[q + 2], col[static_cast<size_t>(q + 2) * NP], p2);
+      p3 = fma(row[q + 3], col[static_cast<size_t>(q + 3) * NP], p3);
+    }
+    for (; q < q1; ++q) p0 = fma(row[q], col[static_cast<size_t>(q) * NP], p0);
+    return (p0 + p1) + (p2 + p3);
+  };
   for (int j = tid; j < 2 * n; j += 256) {
     double* M = X[j / n];
     const int c = j % n;
-    for (int i = 1; i < n; ++i) {
-      double acc = M[static_cast<size_t>(i) * NP + c];
-      const double* lrow = D + static_cast<size_t>(i) * NP;
-      for (int q = 0; q < i; ++q) acc = fma(-lrow[q], M[static_cast<size_t>(q) * NP + c], acc);
-      M[static_cast<size_t>(i) * NP + c] = acc;
-    }
+    double* col = M + c;
+    for (int i = 1; i < n; ++i)
+      col[static_cast<size_t>(i) * NP] -= dot(D + static_cast<size_t>(i) * NP, col, 0, i);
     for (int i = n - 1; i >= 0; --i) {
-      double acc = M[static_cast<size_t>(i) * NP + c];
       const double* urow = D + static_cast<size_t>(i) * NP;
-      for (int q = i + 1; q < n; ++q) acc = fma(-urow[q], M[static_cast<size_t>(q) * NP + c], acc);
-      M[static_cast<size_t>(i) * NP + c] = acc / urow[i];
+      col[static_cast<size_t>(i) * NP] =
+          (col[static_cast<size_t>(i) * NP] - dot(urow, col, i + 1, n)) / urow[i];
     }
   }
   if (S[b] != 0) return;

@@ -10,6 +10,7 @@ import paper_2010_00465_b200 as csm
 from tests._util import cfg2_like, cfg3_like
 
 which = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
+method = sys.argv[2] if len(sys.argv) > 2 else "taylor"
 rng = np.random.default_rng(0)
 if which == "cfg3":
     a = torch.from_numpy(cfg3_like(rng, 4096)).cuda(); prec = csm.Precision.SINGLE
@@ -17,12 +18,13 @@ elif which == "cfg2":
     a = torch.from_numpy(cfg2_like(rng, 16384)).cuda(); prec = csm.Precision.DOUBLE
 else:
     n = int(which); a = torch.from_numpy(cfg2_like(rng, max(1, 2 ** 21 // n ** 2 * 8), n=n)).cuda(); prec = csm.Precision.DOUBLE
+run = csm.cos_sin_batched if method == "taylor" else csm.pade_cos_sin_batched
 for _ in range(2):
-    csm.cos_sin_batched(a, prec, raise_on_error=False)
+    run(a, prec, raise_on_error=False)
 torch.cuda.synchronize()
 from torch.profiler import profile, ProfilerActivity
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-    csm.cos_sin_batched(a, prec, raise_on_error=False)
+    run(a, prec, raise_on_error=False)
     torch.cuda.synchronize()
 ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
 ev.sort(key=lambda e: e.time_range.start)
