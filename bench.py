@@ -203,6 +203,7 @@ def run_reference(args, cfg):
             if i >= args.warmup:
                 times.append(time.perf_counter() - t0)
         rate = 1.0 / statistics.mean(times)
+        ms_step = 1e3 * statistics.mean(times)
         cores, sample = os.cpu_count(), f"{args.steps} full calls"
     else:
         per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))
@@ -212,6 +213,7 @@ def run_reference(args, cfg):
             if i >= args.warmup:
                 rates.append(rate_i)
         rate = statistics.mean(rates)
+        ms_step = 1e3 * batch / rate  # one step's batch at the measured rate
         cores = workers
         sample = (f"{workers} processes x 1 BLAS thread, each re-running "
                   f"{pw} seeded {desc.split(',')[0]} matrices for >= "
@@ -219,7 +221,7 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": rate,
         "unit": "matrices/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": None,
+        "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64" if dt == "f64" else "f32->f64", "data": "synthetic",
         "config": {"workload": args.config, "description": desc},
