@@ -232,6 +232,12 @@ int csm_slab_op_peer(const void* op, double* slab, int M, int NP, int row0,
                      void* cos_out, void* sin_out, int out_f32, void* scratch,
                      void* stream);
 
+/* 1 when csm_cos_sin / csm_wave for (dtype, batch, n) never synchronises
+ * the host (K1, or K1c without the side chain), so the call can be
+ * captured in a CUDA graph; 0 for the tiled chain (it reads (k, s) back to
+ * plan its launches). */
+int csm_graph_safe(int dtype, int64_t batch, int n);
+
 /* ---- Measurement helpers (not part of the reference surface) ------------
  * csm_fp64_peak: time a DMMA (mma.sync m8n8k4 f64) throughput loop on the
  * current device for ~`iters` iterations; returns TFLOP/s in *tflops.

@@ -64,6 +64,7 @@ SIGNATURES = {
                            _i32, _vp, _vp]),
     "csm_slab_op_peer": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _dp, _i32,
                                 _vp, _vp, _i32, _vp, _vp]),
+    "csm_graph_safe": (_i32, [_i32, _i64, _i32]),
     "csm_profile_enable": (_i32, [_i32]),
     "csm_profile_collect": (_i32, [_vp, _vp]),
 }

@@ -739,6 +739,13 @@ int csm_pade_cos_sin(int dtype, int precision, const void* a, void* cos_out, voi
   return CSM_SUCCESS;
 }
 
+int csm_graph_safe(int dtype, int64_t batch, int n) {
+  (void)dtype;
+  if (batch < 0 || n < 0) return 0;
+  if (n <= 64) return 1;
+  return (n <= fused_max() && side_count(batch) == 0) ? 1 : 0;
+}
+
 int csm_profile_enable(int on) {
   prof_clear();
   g_prof = on != 0;

@@ -3,7 +3,10 @@
 ``BatchPlan`` is the serving/benchmark form of cos_sin_batched /
 wave_cos_sin_batched: it owns the device outputs, the (k, s, status) arrays
 and the C-ABI workspace, so a run is one C call with no allocation and no
-host synchronisation (n <= 64).  ``run_host`` streams a batch from pinned
+host synchronisation (n <= 64, and n <= 128 below the side-chain batch).
+Such plans can also be captured once into a CUDA graph (``capture`` /
+``replay``): the norm, selection, schedule and fused kernels then launch
+as one graph, which is what small batches (launch-latency bound) want.  ``run_host`` streams a batch from pinned
 host memory through the device and back in chunks on three CUDA streams
 (H2D, compute, D2H), so the two PCIe directions and the kernels overlap.
 """
@@ -93,6 +96,35 @@ class BatchPlan:
             hi = min(self.batch, lo + self.chunk)
             self._call(a.data_ptr() + lo * nn * esz, lo, hi, h,
                        None if tp is None else tp + lo * tsz)
+        return self.cos, self.sin, self.k, self.s, self.status
+
+    @property
+    def graph_safe(self) -> bool:
+        return bool(_lib.lib().csm_graph_safe(self.code, self.chunk, self.n))
+
+    def capture(self, a, t=None):
+        """Capture run(a, t) into a CUDA graph; `a` (and t) become the
+        graph's static inputs -- copy new data into them, then replay()."""
+        torch = self.torch
+        if not self.graph_safe:
+            raise RuntimeError("this plan synchronises the host (tiled chain); "
+                               "it cannot be captured in a CUDA graph")
+        self._g_a = a.contiguous()
+        self._g_t = None if t is None else t.contiguous()
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up outside the capture
+            self.run(self._g_a, self._g_t)
+        torch.cuda.current_stream().wait_stream(side)
+        self._graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._graph):
+            self.run(self._g_a, self._g_t)
+        return self._g_a
+
+    def replay(self):
+        """Replay the captured run on the current stream; returns the same
+        (cos, sin, k, s, status) tensors as run()."""
+        self._graph.replay()
         return self.cos, self.sin, self.k, self.s, self.status
 
     def run_host(self, a_host, cos_host, sin_host, t_host=None,

@@ -1,0 +1,61 @@
+"""BatchPlan: device runs, the chunked host pipeline and CUDA-graph replay
+agree with the one-shot batched API (same kernels, same bits)."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2010_00465_b200 as csm
+from paper_2010_00465_b200.plan import BatchPlan
+from tests._util import cfg2_like, laplacian_wave
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n,batch", [(64, 96), (100, 40)])
+def test_plan_run_and_graph_replay_bitwise(cuda, n, batch):
+    rng = np.random.default_rng(700 + n)
+    a0 = torch.from_numpy(cfg2_like(rng, batch, n=n)).cuda()
+    a1 = torch.from_numpy(cfg2_like(rng, batch, n=n)).cuda()
+    plan = BatchPlan(batch, n)
+    assert plan.graph_safe
+    cos, sin, k, s, st = plan.run(a0)
+    ref = csm.cos_sin_batched(a0)
+    assert torch.equal(cos, ref.cos_part) and torch.equal(sin, ref.sin_part)
+    static = plan.capture(a0)
+    static.copy_(a1)  # new data into the graph's static input
+    cos, sin, k, s, st = plan.replay()
+    torch.cuda.synchronize()
+    ref = csm.cos_sin_batched(a1)
+    assert torch.equal(cos, ref.cos_part) and torch.equal(sin, ref.sin_part)
+    assert torch.equal(k, ref.k) and torch.equal(s, ref.s)
+
+
+def test_plan_graph_wave(cuda):
+    rng = np.random.default_rng(710)
+    a, t = laplacian_wave(rng, 8, 48)
+    a = torch.from_numpy(a).cuda()
+    t = torch.from_numpy(t).cuda()
+    plan = BatchPlan(8, 48, wave=True)
+    plan.capture(a, t)
+    c, s_, k, s, st = plan.replay()
+    ref = csm.wave_cos_sin_batched(a, t)
+    assert torch.equal(c, ref.cos_part) and torch.equal(s_, ref.sin_part)
+
+
+def test_plan_tiled_is_not_graph_safe(cuda):
+    plan = BatchPlan(4, 200)
+    assert not plan.graph_safe
+    with pytest.raises(RuntimeError):
+        plan.capture(torch.zeros((4, 200, 200), dtype=torch.float64, device="cuda"))
+
+
+def test_plan_run_host_matches(cuda):
+    rng = np.random.default_rng(720)
+    a = torch.from_numpy(cfg2_like(rng, 256, n=64)).pin_memory()
+    c = torch.empty_like(a).pin_memory()
+    s = torch.empty_like(a).pin_memory()
+    plan = BatchPlan(256, 64, chunk=64)
+    plan.run_host(a, c, s, chunks=4)
+    torch.cuda.synchronize()
+    ref = csm.cos_sin_batched(a.numpy())
+    assert np.array_equal(c.numpy(), ref.cos_part) and np.array_equal(s.numpy(), ref.sin_part)
