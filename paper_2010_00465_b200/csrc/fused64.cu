@@ -919,8 +919,12 @@ static cudaError_t launch_fused(int dtype, bool wave, const void* a, void* c, vo
 // SMs the K1c grid occupies (4 x co-resident clusters; the rest of the GPU
 // is free for concurrent work).
 int k1c_resident_sms() {
-  static int cached = -1;
-  if (cached >= 0) return cached;
+  static int cached[32] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1,
+                           -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev = dev < 32 ? dev : 31;
+  if (cached[dev] >= 0) return cached[dev];
   auto kern = f64k::fused64_kernel<4, double, double, false>;
   const size_t smem = fused64_smem_bytes();
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -939,8 +943,8 @@ int k1c_resident_sms() {
   cfg.gridDim = dim3(4 * 32);
   int active = 0;
   if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) != cudaSuccess) return 0;
-  cached = 4 * active;
-  return cached;
+  cached[dev] = 4 * active;
+  return cached[dev];
 }
 
 // Launch K1 (n <= 64) or K1c (64 < n <= 128) for a batch whose (k, s,

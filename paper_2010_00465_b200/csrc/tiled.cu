@@ -376,6 +376,19 @@ __global__ void nan_fill_kernel(TOut* __restrict__ Cout, TOut* __restrict__ Sout
   }
 }
 
+// Opt the tiled kernel into its dynamic shared memory, once per device.
+inline cudaError_t ensure_smem_attr() {
+  static unsigned done_mask = 0;  // bit per device ordinal (< 32)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 32 && ((done_mask >> dev) & 1u)) return cudaSuccess;
+  e = cudaFuncSetAttribute(gemm_epi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(SMEM));
+  if (e == cudaSuccess && dev < 32) done_mask |= 1u << dev;
+  return e;
+}
+
 // Order-8 Pade: LU with partial pivoting of the shared denominator (slot 5)
 // and the two solves for the numerators (slots 6 and 7, in place), one CTA
 // per matrix on its n x n block (the padding of den / num_cos is I and of
@@ -873,13 +886,7 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // host vectors die here
     if (e != cudaSuccess) return e;
 
-    static bool attr_done = false;
-    if (!attr_done) {
-      e = cudaFuncSetAttribute(tk::gemm_epi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(tk::SMEM));
-      if (e != cudaSuccess) return e;
-      attr_done = true;
-    }
+    if ((e = tk::ensure_smem_attr()) != cudaSuccess) return e;
     const unsigned tiles = static_cast<unsigned>((NP / tk::BM) * (NP / tk::BN));
     tk::LaunchArgs A{};
     A.ws = w.slots;
@@ -1012,13 +1019,7 @@ cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
   if (e != cudaSuccess) return e;
   e = cudaStreamSynchronize(stream);  // h lives on this stack frame
   if (e != cudaSuccess) return e;
-  static bool attr_done = false;
-  if (!attr_done) {
-    e = cudaFuncSetAttribute(tk::gemm_epi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(tk::SMEM));
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  if ((e = tk::ensure_smem_attr()) != cudaSuccess) return e;
   Staged* d = static_cast<Staged*>(scratch);
   tk::LaunchArgs A{};
   A.ws = slab;
