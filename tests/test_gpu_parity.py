@@ -515,6 +515,48 @@ def test_large_symmetric_against_oracle_noise_floor(cuda, n):
     gate = max(TOL64, 4.0 * noise)
     assert rel1(rep.result.cos_part, c) <= gate, (rel1(rep.result.cos_part, c), noise)
     assert rel1(rep.result.sin_part, s) <= gate, (rel1(rep.result.sin_part, s), noise)
+    # third number: both against the double-double truth
+    from paper_2010_00465_b200 import verify
+    tr = verify.reference_cos_sin(a)
+    for got, ref, t in ((rep.result.cos_part, c, tr.cos_part),
+                        (rep.result.sin_part, s, tr.sin_part)):
+        assert rel1(got, t) <= 4.0 * rel1(ref, t) + 1e-15, (rel1(got, t), rel1(ref, t))
+
+
+@pytest.mark.timeout(600)
+def test_wave_cfg4_analogue_three_numbers(cuda):
+    """configs[3] analogue (SPD Laplacian + potential, n = 256, large s):
+    GPU vs reference gated at max(1e-12, 4 x the reference's own
+    permuted-order noise), and both against the eigendecomposition answer
+    c = V cos(t sqrt(L)) V^T, s = V sin(t sqrt(L))/sqrt(L) V^T."""
+    rng = np.random.default_rng(4)
+    a, _ = laplacian_wave(rng, 1, 256)
+    a = a[0]
+    t = 1e-1
+    c, s, k, sc = orc.wave_cos_sin(a, t)
+    assert sc >= 9
+    rep = csm.wave_cos_sin(a, t)
+    assert (rep.scheme_used.k_products, rep.scaling_exponent) == (k, sc)
+
+    class _T(np.ndarray):
+        def __matmul__(self, other):
+            x, y = np.asarray(self), np.asarray(other)
+            h = x.shape[1] // 2 + 1
+            return (x[:, :h] @ y[:h] + x[:, h:] @ y[h:]).view(_T)
+
+    tp = t / 2.0 ** sc
+    cp, spp = orc.wave_core(a.view(_T), tp, k)
+    cp, spp = orc.double_angle(np.asarray(cp).view(_T), np.asarray(spp).view(_T), sc)
+    noise = max(rel1(np.asarray(cp), c), rel1(np.asarray(spp), s))
+    gate = max(TOL64, 4.0 * noise)
+    assert rel1(rep.result.c_part, c) <= gate
+    assert rel1(rep.result.s_part, s) <= gate
+    lam, v = np.linalg.eigh(a)
+    w = np.sqrt(lam)
+    ce = (v * np.cos(t * w)) @ v.T
+    se = (v * (np.sin(t * w) / w)) @ v.T
+    for got, ref, ex in ((rep.result.c_part, c, ce), (rep.result.s_part, s, se)):
+        assert rel1(got, ex) <= 4.0 * rel1(ref, ex) + 1e-14, (rel1(got, ex), rel1(ref, ex))
 
 
 def _pade_tol(s, prec="double"):
