@@ -216,6 +216,13 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
       cudaEventCreateWithFlags(&ev_sel, cudaEventDisableTiming);
       cudaEventRecord(ev_sel, stream);  // (k, s, status) are final here
     }
+    struct EventGuard {  // events are released on every exit path
+      cudaEvent_t* ev[2];
+      ~EventGuard() {
+        for (auto* p : ev)
+          if (*p) cudaEventDestroy(*p);
+      }
+    } guard{{&ev_sel, &ev_done}};
     e = csm::launch_schedule(K, S, st, bf, w.bins, w.order, stream, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "schedule kernels");
     csm::prof_begin(stream);
@@ -237,8 +244,6 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
       cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
       cudaEventRecord(ev_done, side);
       cudaStreamWaitEvent(stream, ev_done, 0);
-      cudaEventDestroy(ev_sel);
-      cudaEventDestroy(ev_done);
     }
     csm::prof_end(stream);
   } else {
