@@ -432,8 +432,9 @@ def run_ours(args, cfg):
     s_host = torch.empty_like(c_host).pin_memory()
     t_host = torch.from_numpy(t_np).pin_memory() if wave else None
     e2e_steps = max(1, min(args.steps, 10))
+    chunks = int(os.environ.get("CSM_E2E_CHUNKS", "16"))
     for _ in range(2):
-        plan.run_host(a_host, c_host, s_host, t_host)
+        plan.run_host(a_host, c_host, s_host, t_host, chunks=chunks)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -441,7 +442,7 @@ def run_ours(args, cfg):
     e3 = torch.cuda.Event(enable_timing=True)
     e2.record()
     for _ in range(e2e_steps):
-        plan.run_host(a_host, c_host, s_host, t_host)
+        plan.run_host(a_host, c_host, s_host, t_host, chunks=chunks)
         _ = float(c_host[batch - 1, n - 1, n - 1])  # host read of the result
     e3.record()
     torch.cuda.synchronize()

@@ -131,7 +131,9 @@ class BatchPlan:
                  chunks: int = 8) -> None:
         """Host->device->host run: pinned CPU tensors in and out, chunked
         over H2D / compute / D2H streams.  Ends with the current stream
-        waiting on the last D2H copy (call synchronize to read results)."""
+        waiting on the last D2H copy (call synchronize to read results).
+        The host input buffer is read asynchronously: do not overwrite it
+        until the current stream has passed this call."""
         torch = self.torch
         if self._a_dev is None:
             self._a_dev = torch.empty((self.batch, self.n, self.n),
@@ -145,13 +147,23 @@ class BatchPlan:
             chunks = (self.batch + self.chunk - 1) // self.chunk
         s_h2d, s_cmp, s_d2h = self._streams
         cur = torch.cuda.current_stream()
-        for s in self._streams:
-            s.wait_stream(cur)
         step = (self.batch + chunks - 1) // chunks
+        # Back-to-back calls pipeline across the call boundary: the next
+        # call's H2D of chunk j only waits for THIS call's compute of chunk j
+        # (the one reader of that input slice), so it overlaps this call's
+        # remaining D2H -- the two PCIe directions stay busy together.
+        prev = self._cmp_done if getattr(self, "_pipe_step", None) == step else None
+        s_cmp.wait_stream(cur)  # outputs are rewritten: after the caller's work
+        if prev is None:
+            s_h2d.wait_stream(cur)
+        self._pipe_step = step
+        self._cmp_done = []
         nn = self.n * self.n
         esz = self._a_dev.element_size()
-        for lo in range(0, self.batch, step):
+        for j, lo in enumerate(range(0, self.batch, step)):
             hi = min(self.batch, lo + step)
+            if prev is not None:
+                s_h2d.wait_event(prev[j])
             with torch.cuda.stream(s_h2d):
                 self._a_dev[lo:hi].copy_(a_host[lo:hi], non_blocking=True)
                 if self.wave:
@@ -167,10 +179,10 @@ class BatchPlan:
                            else self._t_dev.data_ptr() + 8 * clo)
             ev_out = torch.cuda.Event()
             ev_out.record(s_cmp)
+            self._cmp_done.append(ev_out)
             s_d2h.wait_event(ev_out)
             with torch.cuda.stream(s_d2h):
                 cos_host[lo:hi].copy_(self.cos[lo:hi], non_blocking=True)
                 sin_host[lo:hi].copy_(self.sin[lo:hi], non_blocking=True)
         cur.wait_stream(s_d2h)
         cur.wait_stream(s_cmp)
-        cur.wait_stream(s_h2d)
