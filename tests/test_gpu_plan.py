@@ -59,3 +59,22 @@ def test_plan_run_host_matches(cuda):
     torch.cuda.synchronize()
     ref = csm.cos_sin_batched(a.numpy())
     assert np.array_equal(c.numpy(), ref.cos_part) and np.array_equal(s.numpy(), ref.sin_part)
+
+
+def test_plan_run_host_back_to_back_calls(cuda):
+    """Consecutive run_host calls overlap across the call boundary; each
+    call's results still belong to its own input."""
+    rng = np.random.default_rng(730)
+    a1 = torch.from_numpy(cfg2_like(rng, 512, n=64)).pin_memory()
+    a2 = torch.from_numpy(cfg2_like(rng, 512, n=64)).pin_memory()
+    c1, s1 = torch.empty_like(a1).pin_memory(), torch.empty_like(a1).pin_memory()
+    c2, s2 = torch.empty_like(a1).pin_memory(), torch.empty_like(a1).pin_memory()
+    plan = BatchPlan(512, 64)
+    for _ in range(3):
+        plan.run_host(a1, c1, s1, chunks=16)
+        plan.run_host(a2, c2, s2, chunks=16)
+    torch.cuda.synchronize()
+    r1 = csm.cos_sin_batched(a1.numpy())
+    r2 = csm.cos_sin_batched(a2.numpy())
+    assert np.array_equal(c1.numpy(), r1.cos_part) and np.array_equal(s1.numpy(), r1.sin_part)
+    assert np.array_equal(c2.numpy(), r2.cos_part) and np.array_equal(s2.numpy(), r2.sin_part)
