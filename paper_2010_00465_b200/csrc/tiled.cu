@@ -479,9 +479,12 @@ __global__ void __launch_bounds__(256) pade_lu_solve_kernel(
     if (tid == 0) status[b] = kSingular;
     return;
   }
-  // getrs: unit-lower then upper triangular solve, one thread per column;
-  // each dot product runs in 4 independent partial sums (the serial FMA
-  // chain, not memory, bounds this loop)
+  // getrs, blocked by 64 rows: per block a short triangular solve down each
+  // right-hand-side column (one thread per column), then the rank-64
+  // update of the remaining rows as a register-tiled (4 x 4 per thread)
+  // product, so every loaded L / U / X element feeds 4 FMAs instead of 1.
+  constexpr int BSZ = 64;
+  // dot product in 4 independent partial sums (breaks the serial FMA chain)
   auto dot = [&](const double* row, const double* col, int q0, int q1) {
     double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
     int q = q0;
@@ -494,17 +497,59 @@ __global__ void __launch_bounds__(256) pade_lu_solve_kernel(
     for (; q < q1; ++q) p0 = fma(row[q], col[static_cast<size_t>(q) * NP], p0);
     return (p0 + p1) + (p2 + p3);
   };
-  for (int j = tid; j < 2 * n; j += 256) {
-    double* M = X[j / n];
-    const int c = j % n;
-    double* col = M + c;
-    for (int i = 1; i < n; ++i)
-      col[static_cast<size_t>(i) * NP] -= dot(D + static_cast<size_t>(i) * NP, col, 0, i);
-    for (int i = n - 1; i >= 0; --i) {
-      const double* urow = D + static_cast<size_t>(i) * NP;
-      col[static_cast<size_t>(i) * NP] =
-          (col[static_cast<size_t>(i) * NP] - dot(urow, col, i + 1, n)) / urow[i];
+  auto xat = [&](int r, int c) -> double& {  // column c of [X1 | X2]
+    return c < n ? X[0][static_cast<size_t>(r) * NP + c] : X[1][static_cast<size_t>(r) * NP + c - n];
+  };
+  auto dat = [&](int r, int c) -> double { return D[static_cast<size_t>(r) * NP + c]; };
+  // rows [u0, u1) -= F[u0:u1, q0:q1] * X[q0:q1, :], F = the L or U part of D
+  auto update = [&](int u0, int u1, int q0, int q1) {
+    const int rt = (u1 - u0 + 3) / 4, ct = (2 * n + 3) / 4;
+    for (int tile = tid; tile < rt * ct; tile += 256) {
+      const int r = u0 + 4 * (tile / ct), c = 4 * (tile % ct);
+      double acc[4][4] = {};
+      for (int q = q0; q < q1; ++q) {
+        double a[4], x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = r + i < u1 ? dat(r + i, q) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = c + j < 2 * n ? xat(q, c + j) : 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], x[j], acc[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (r + i < u1 && c + j < 2 * n) xat(r + i, c + j) -= acc[i][j];
     }
+  };
+  const int nb = (n + BSZ - 1) / BSZ;
+  for (int bi = 0; bi < nb; ++bi) {  // forward: unit-lower L
+    const int r0 = bi * BSZ, r1 = min(n, r0 + BSZ);
+    for (int c = tid; c < 2 * n; c += 256) {
+      double* col = &xat(0, c);
+      for (int i = r0 + 1; i < r1; ++i)
+        col[static_cast<size_t>(i) * NP] -= dot(D + static_cast<size_t>(i) * NP, col, r0, i);
+    }
+    __syncthreads();
+    if (r1 < n) update(r1, n, r0, r1);
+    __syncthreads();
+  }
+  for (int bi = nb - 1; bi >= 0; --bi) {  // backward: upper U
+    const int r0 = bi * BSZ, r1 = min(n, r0 + BSZ);
+    for (int c = tid; c < 2 * n; c += 256) {
+      double* col = &xat(0, c);
+      for (int i = r1 - 1; i >= r0; --i) {
+        const double* urow = D + static_cast<size_t>(i) * NP;
+        col[static_cast<size_t>(i) * NP] =
+            (col[static_cast<size_t>(i) * NP] - dot(urow, col, i + 1, r1)) / urow[i];
+      }
+    }
+    __syncthreads();
+    if (r0 > 0) update(0, r0, r0, r1);
+    __syncthreads();
   }
   if (S[b] != 0) return;
   __syncthreads();
