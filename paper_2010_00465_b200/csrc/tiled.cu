@@ -428,62 +428,6 @@ __global__ void __launch_bounds__(256) pade_lu_solve_kernel(
   }
   __syncthreads();
 
-  for (int k = 0; k < n; ++k) {
-    // pivot: first row of max |a_ik|, i >= k (idamax)
-    double bv = -1.0;
-    int bi = n;
-    for (int i = k + tid; i < n; i += 256) {
-      const double v = fabs(D[static_cast<size_t>(i) * NP + k]);
-      if (v > bv) { bv = v; bi = i; }
-    }
-    for (int o = 16; o; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
-    if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
-    __syncthreads();
-    if (tid == 0) {
-      double v = red_v[0];
-      int p = red_i[0];
-      for (int w = 1; w < 8; ++w)
-        if (red_v[w] > v || (red_v[w] == v && red_i[w] < p)) { v = red_v[w]; p = red_i[w]; }
-      sh_p = p < n ? p : k;
-    }
-    __syncthreads();
-    const int p = sh_p;
-    if (p != k) {  // swap rows k, p of den (whole row) and of both right-hand sides
-      for (int j = tid; j < 3 * n; j += 256) {
-        double* M = j < n ? D : X[j / n - 1];
-        const int c = j % n;
-        const double t = M[static_cast<size_t>(k) * NP + c];
-        M[static_cast<size_t>(k) * NP + c] = M[static_cast<size_t>(p) * NP + c];
-        M[static_cast<size_t>(p) * NP + c] = t;
-      }
-      __syncthreads();
-    }
-    const double piv = D[static_cast<size_t>(k) * NP + k];
-    if (tid == 0) sh_umin = fmin(sh_umin, fabs(piv));
-    const double rcp = 1.0 / piv;
-    for (int i = k + 1 + tid; i < n; i += 256) D[static_cast<size_t>(i) * NP + k] *= rcp;
-    __syncthreads();
-    for (int i = k + 1 + warp; i < n; i += 8) {
-      const double l = D[static_cast<size_t>(i) * NP + k];
-      double* row = D + static_cast<size_t>(i) * NP;
-      const double* urow = D + static_cast<size_t>(k) * NP;
-      for (int j = k + 1 + lane; j < n; j += 32) row[j] = fma(-l, urow[j], row[j]);
-    }
-    __syncthreads();
-  }
-  if (sh_umin <= 1e3 * 0x1p-52 * sh_norm || !(sh_umin == sh_umin)) {
-    if (tid == 0) status[b] = kSingular;
-    return;
-  }
-  // getrs, blocked by 64 rows: per block a short triangular solve down each
-  // right-hand-side column (one thread per column), then the rank-64
-  // update of the remaining rows as a register-tiled (4 x 4 per thread)
-  // product, so every loaded L / U / X element feeds 4 FMAs instead of 1.
-  constexpr int BSZ = 64;
   // dot product in 4 independent partial sums (breaks the serial FMA chain)
   auto dot = [&](const double* row, const double* col, int q0, int q1) {
     double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
@@ -497,22 +441,20 @@ __global__ void __launch_bounds__(256) pade_lu_solve_kernel(
     for (; q < q1; ++q) p0 = fma(row[q], col[static_cast<size_t>(q) * NP], p0);
     return (p0 + p1) + (p2 + p3);
   };
-  auto xat = [&](int r, int c) -> double& {  // column c of [X1 | X2]
-    return c < n ? X[0][static_cast<size_t>(r) * NP + c] : X[1][static_cast<size_t>(r) * NP + c - n];
-  };
-  auto dat = [&](int r, int c) -> double { return D[static_cast<size_t>(r) * NP + c]; };
-  // rows [u0, u1) -= F[u0:u1, q0:q1] * X[q0:q1, :], F = the L or U part of D
-  auto update = [&](int u0, int u1, int q0, int q1) {
-    const int rt = (u1 - u0 + 3) / 4, ct = (2 * n + 3) / 4;
+  // M[u0:u1, v0:v1] -= A[u0:u1, q0:q1] * B[q0:q1, v0:v1], register-tiled
+  // 4 x 4 per thread (every loaded element feeds 4 FMAs)
+  auto rank_update = [&](auto&& Mat, auto&& Aat, auto&& Bat, int u0, int u1, int v0, int v1,
+                         int q0, int q1) {
+    const int rt = (u1 - u0 + 3) / 4, ct = (v1 - v0 + 3) / 4;
     for (int tile = tid; tile < rt * ct; tile += 256) {
-      const int r = u0 + 4 * (tile / ct), c = 4 * (tile % ct);
+      const int r = u0 + 4 * (tile / ct), c = v0 + 4 * (tile % ct);
       double acc[4][4] = {};
       for (int q = q0; q < q1; ++q) {
         double a[4], x[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = r + i < u1 ? dat(r + i, q) : 0.0;
+        for (int i = 0; i < 4; ++i) a[i] = r + i < u1 ? Aat(r + i, q) : 0.0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) x[j] = c + j < 2 * n ? xat(q, c + j) : 0.0;
+        for (int j = 0; j < 4; ++j) x[j] = c + j < v1 ? Bat(q, c + j) : 0.0;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -522,8 +464,94 @@ __global__ void __launch_bounds__(256) pade_lu_solve_kernel(
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (r + i < u1 && c + j < 2 * n) xat(r + i, c + j) -= acc[i][j];
+          if (r + i < u1 && c + j < v1) Mat(r + i, c + j) -= acc[i][j];
     }
+  };
+  auto dref = [&](int r, int c) -> double& { return D[static_cast<size_t>(r) * NP + c]; };
+  auto dval = [&](int r, int c) -> double { return D[static_cast<size_t>(r) * NP + c]; };
+  constexpr int PW = 64;  // panel width of the blocked getrf
+
+  // getrf, right-looking and blocked by 64-column panels: unblocked LU with
+  // partial pivoting inside the panel (whole-row swaps, as LAPACK's laswp
+  // on both sides), then U12 = L11^-1 A12 and the trailing update
+  // A22 -= L21 U12 -- one pass over the trailing matrix per panel instead
+  // of one per pivot.
+  for (int c0 = 0; c0 < n; c0 += PW) {
+    const int c1 = min(n, c0 + PW);
+    for (int k = c0; k < c1; ++k) {
+      // pivot: first row of max |a_ik|, i >= k (idamax)
+      double bv = -1.0;
+      int bi = n;
+      for (int i = k + tid; i < n; i += 256) {
+        const double v = fabs(D[static_cast<size_t>(i) * NP + k]);
+        if (v > bv) { bv = v; bi = i; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
+      __syncthreads();
+      if (tid == 0) {
+        double v = red_v[0];
+        int p = red_i[0];
+        for (int w = 1; w < 8; ++w)
+          if (red_v[w] > v || (red_v[w] == v && red_i[w] < p)) { v = red_v[w]; p = red_i[w]; }
+        sh_p = p < n ? p : k;
+      }
+      __syncthreads();
+      const int p = sh_p;
+      if (p != k) {  // swap rows k, p of den (whole row) and of both right-hand sides
+        for (int j = tid; j < 3 * n; j += 256) {
+          double* M = j < n ? D : X[j / n - 1];
+          const int c = j % n;
+          const double t = M[static_cast<size_t>(k) * NP + c];
+          M[static_cast<size_t>(k) * NP + c] = M[static_cast<size_t>(p) * NP + c];
+          M[static_cast<size_t>(p) * NP + c] = t;
+        }
+        __syncthreads();
+      }
+      const double piv = D[static_cast<size_t>(k) * NP + k];
+      if (tid == 0) sh_umin = fmin(sh_umin, fabs(piv));
+      const double rcp = 1.0 / piv;
+      for (int i = k + 1 + tid; i < n; i += 256) D[static_cast<size_t>(i) * NP + k] *= rcp;
+      __syncthreads();
+      for (int i = k + 1 + warp; i < n; i += 8) {  // rank-1 update inside the panel
+        const double l = D[static_cast<size_t>(i) * NP + k];
+        double* row = D + static_cast<size_t>(i) * NP;
+        const double* urow = D + static_cast<size_t>(k) * NP;
+        for (int j = k + 1 + lane; j < c1; j += 32) row[j] = fma(-l, urow[j], row[j]);
+      }
+      __syncthreads();
+    }
+    if (c1 < n) {
+      for (int j = c1 + tid; j < n; j += 256) {  // U12 = L11^-1 A12 (unit lower)
+        double* col = D + j;
+        for (int i = c0 + 1; i < c1; ++i)
+          col[static_cast<size_t>(i) * NP] -= dot(D + static_cast<size_t>(i) * NP, col, c0, i);
+      }
+      __syncthreads();
+      rank_update(dref, dval, dval, c1, n, c1, n, c0, c1);  // A22 -= L21 U12
+      __syncthreads();
+    }
+  }
+  if (sh_umin <= 1e3 * 0x1p-52 * sh_norm || !(sh_umin == sh_umin)) {
+    if (tid == 0) status[b] = kSingular;
+    return;
+  }
+  // getrs, blocked by 64 rows: per block a short triangular solve down each
+  // right-hand-side column (one thread per column), then the rank-64
+  // update of the remaining rows as a register-tiled (4 x 4 per thread)
+  // product, so every loaded L / U / X element feeds 4 FMAs instead of 1.
+  constexpr int BSZ = 64;
+  auto xat = [&](int r, int c) -> double& {  // column c of [X1 | X2]
+    return c < n ? X[0][static_cast<size_t>(r) * NP + c] : X[1][static_cast<size_t>(r) * NP + c - n];
+  };
+  auto dat = [&](int r, int c) -> double { return D[static_cast<size_t>(r) * NP + c]; };
+  // rows [u0, u1) of [X1 | X2] -= F[u0:u1, q0:q1] * X[q0:q1, :], F = L or U of D
+  auto update = [&](int u0, int u1, int q0, int q1) {
+    rank_update(xat, dval, xat, u0, u1, 0, 2 * n, q0, q1);
   };
   const int nb = (n + BSZ - 1) / BSZ;
   for (int bi = 0; bi < nb; ++bi) {  // forward: unit-lower L
