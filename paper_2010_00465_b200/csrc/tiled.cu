@@ -403,8 +403,21 @@ __global__ void __launch_bounds__(256) pade_lu_solve_kernel(
   const int b = idx[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t slotsz = static_cast<size_t>(NP) * NP;
-  double* D = ws + static_cast<size_t>(b) * mat_stride + 5 * slotsz;
-  double* X[2] = {D + slotsz, D + 2 * slotsz};
+  double* const Dg = ws + static_cast<size_t>(b) * mat_stride + 5 * slotsz;
+  double* D = Dg;
+  double* X[2] = {Dg + slotsz, Dg + 2 * slotsz};
+  // NP = 64: den and both right-hand sides (3 x 32 KiB) are staged in
+  // shared memory for the whole factorisation and solve
+  extern __shared__ __align__(16) double lu_sm[];
+  const bool staged = NP == 64;
+  if (staged) {
+    for (int e = tid; e < static_cast<int>(3 * slotsz / 2); e += 256)
+      reinterpret_cast<double2*>(lu_sm)[e] = reinterpret_cast<const double2*>(Dg)[e];
+    D = lu_sm;
+    X[0] = lu_sm + slotsz;
+    X[1] = lu_sm + 2 * slotsz;
+    __syncthreads();
+  }
   __shared__ double red_v[8];
   __shared__ int red_i[8];
   __shared__ int sh_p;
@@ -579,8 +592,12 @@ __global__ void __launch_bounds__(256) pade_lu_solve_kernel(
     if (r0 > 0) update(0, r0, r0, r1);
     __syncthreads();
   }
-  if (S[b] != 0) return;
   __syncthreads();
+  if (staged && S[b] != 0)  // the doubling launches read the solutions from the workspace
+    for (int e = tid; e < static_cast<int>(slotsz); e += 256) {
+      reinterpret_cast<double2*>(Dg + slotsz)[e] = reinterpret_cast<const double2*>(X[0])[e];
+    }
+  if (S[b] != 0) return;
   const size_t nn = static_cast<size_t>(n) * n;
   for (size_t e = tid; e < 2 * nn; e += 256) {
     const int w = static_cast<int>(e / nn);
@@ -978,12 +995,20 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     A.row0 = 0;
     A.rhs_full = nullptr;
     A.rhs_parts = nullptr;
+    size_t lu_smem = 0;
+    if (pade && NP == 64) {  // den + both right-hand sides staged in shared memory
+      lu_smem = 3 * static_cast<size_t>(NP) * NP * sizeof(double);
+      e = cudaFuncSetAttribute(tk::pade_lu_solve_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(lu_smem));
+      if (e != cudaSuccess) return e;
+    }
     prof_begin(stream);
     for (size_t pi = 0; pi < plans.size(); ++pi) {
       const LaunchPlan& L = plans[pi];
       if (pade && pi == max_steps) {  // chain done: factor and solve before doubling
         for (const Group& G : groups) {
-          tk::pade_lu_solve_kernel<<<static_cast<unsigned>(G.cnt), 256, 0, stream>>>(
+          tk::pade_lu_solve_kernel<<<static_cast<unsigned>(G.cnt), 256, lu_smem, stream>>>(
               w.slots, mat_stride, NP, n, w.idx + G.off, dS, const_cast<int32_t*>(dStatus),
               c_out, s_out, out_f32);
           ++*launches;
@@ -1005,7 +1030,7 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     }
     if (pade && plans.size() == max_steps) {  // no doubling at all
       for (const Group& G : groups) {
-        tk::pade_lu_solve_kernel<<<static_cast<unsigned>(G.cnt), 256, 0, stream>>>(
+        tk::pade_lu_solve_kernel<<<static_cast<unsigned>(G.cnt), 256, lu_smem, stream>>>(
             w.slots, mat_stride, NP, n, w.idx + G.off, dS, const_cast<int32_t*>(dStatus), c_out,
             s_out, out_f32);
         ++*launches;
