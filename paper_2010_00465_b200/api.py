@@ -273,6 +273,11 @@ def pade_cos_sin(a, precision: Precision = Precision.DOUBLE
     """Drop-in for driver.pade_cos_sin (driver.py:149-164); total_products
     is the reference's 22/3 + 2 s."""
     batch = _as_batch(a, batched=False, f32_out=False)
+    if int(batch.dev.shape[-1]) == 0:
+        # lu_solve_pair on a 0 x 0 denominator: min pivot 0 <= threshold 0
+        # (matcore.py:141-147), so the reference raises
+        raise SingularMatrixError(
+            "denominator singular to working precision (pivot 0.000e+00 <= 0.000e+00)")
     return _single(_pade(batch, precision, True))
 
 

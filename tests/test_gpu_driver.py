@@ -103,3 +103,18 @@ def test_wave_rejects_bad_input(cuda):
         csm.wave_cos_sin(np.zeros((2, 3)), 1.0)
     with pytest.raises(csm.MatrixInputError):
         csm.wave_cos_sin(np.array([[math.nan]]), 1.0)
+
+
+def test_empty_matrices_like_the_reference(cuda):
+    """0 x 0 inputs behave as in the reference: cos_sin / reference values /
+    taylor_sin9 return empty results, pade_cos_sin raises (its pivot test is
+    0 <= 0, matcore.py:141-147)."""
+    from paper_2010_00465_b200 import verify
+    e = np.zeros((0, 0))
+    r = csm.cos_sin(e)
+    assert r.result.cos_part.shape == (0, 0) and r.total_products == Fraction(3)
+    ref = verify.reference_cos_sin(e)
+    assert ref.cos_part.shape == (0, 0) and ref.cost.total_cost == 7
+    assert csm.taylor_sin9(e, csm.CostLedger()).shape == (0, 0)
+    with pytest.raises(csm.SingularMatrixError):
+        csm.pade_cos_sin(e)
