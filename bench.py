@@ -506,7 +506,10 @@ def run_ours(args, cfg):
                      "unit": "TFLOP/s",
                      "frac": (achieved / peak) if (achieved and peak) else None,
                      "traffic": traffic,
-                     "kernel": "fused64_kernel" if n <= 64 else "gemm_epi_kernel",
+                     "kernel": ("fused64_kernel (K1)" if n <= 64 else
+                                "fused64_kernel<4> (K1c, 4-CTA clusters) + side tiled chain, "
+                                "timed as one interval" if n <= 128 else
+                                "gemm_epi_kernel (tiled chain)"),
                      "peak_source": "csm_fp64_peak: DMMA m8n8k4 loop on this "
                                     "GPU in this run (MEASURED_PEAKS.json has "
                                     "no FP64 entry)",
