@@ -8,14 +8,17 @@
 //   slice_rows   A (M x K, fp64 row-major) -> S int8 planes [s][M][K]
 //                + per-row exponent; B is sliced the same way after a
 //                transpose (B^T rows = B columns), giving K-major operands.
-//   ozaki_gemm   128 x 64 output tile per CTA (128 threads).  Per 64-deep
-//                K block: cp.async stages the 8 A planes (128 x 64) and the
-//                8 B planes (64 x 64) into the canonical K-major no-swizzle
-//                UMMA layout; thread 0 issues 36 x 2 tcgen05.mma.kind::i8
-//                (K = 32 each) into the 8 level accumulators (8 x 64 TMEM
-//                columns = all 512); tcgen05.commit -> mbarrier frees the
-//                stage.  Epilogue: tcgen05.ld each level, combine in fp64
-//                with 2^-7L and the row / column scales.
+//   ozaki_gemm   128 x 64 output tile per CTA (128 threads).  Per 32-deep
+//                K block: cp.async stages the 8 A planes (128 x 32) and the
+//                8 B planes (64 x 32) into the canonical K-major no-swizzle
+//                UMMA layout (4-stage ring, 48 KiB per stage); thread 0
+//                issues 36 tcgen05.mma.kind::i8 into the 8 level
+//                accumulators (8 x 64 TMEM columns = all 512) and commits
+//                to the stage's mbarrier; the stage is refilled with K
+//                block kb + 3 once those MMAs are done, while the next
+//                block's MMAs are already queued.  Epilogue: tcgen05.ld
+//                each level, combine in fp64 with 2^-7L and the row /
+//                column scales.
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -24,11 +27,11 @@
 
 constexpr int S = 8;              // slices
 constexpr int TM = 128, TN = 64;  // CTA tile
-constexpr int BK = 64;            // K block (2 MMAs of K = 32)
+constexpr int BK = 32;            // K block (1 MMA of K = 32 per slice pair)
 constexpr int THREADS = 128;
 constexpr int A_PLANE = TM * BK, B_PLANE = TN * BK;      // bytes per plane per stage
-constexpr int STAGE = S * (A_PLANE + B_PLANE);           // 96 KiB
-constexpr int NSTAGE = 2;
+constexpr int STAGE = S * (A_PLANE + B_PLANE);           // 48 KiB
+constexpr int NSTAGE = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -46,9 +49,14 @@ __device__ __forceinline__ void cp16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
 }
 
-// rows of X (R x K fp64, row-major) -> S int8 planes [s][R][K], exponent e[r]
-// with |x| < 2^e[r] for the whole row.  One block per row.
-__global__ void slice_rows(const double* X, int R, int K, int8_t* planes, int* ex) {
+// rows of X (R x K fp64, row-major) -> S int8 planes, exponent e[r] with
+// |x| < 2^e[r] for the whole row.  Plane layout is tile-major and already
+// the canonical K-major no-swizzle UMMA layout: for a tile of TR rows and a
+// 32-deep K block, one contiguous 32 TR-byte block [chunk 0..1][row][16 B],
+// so the GEMM brings each (plane, tile, K block) with ONE bulk copy.
+//   offset(s, r, k) = (((s * (R / TR) + r / TR) * (K / 32) + k / 32) * 2
+//                      + (k % 32) / 16) * TR * 16 + (r % TR) * 16 + k % 16
+__global__ void slice_rows(const double* X, int R, int K, int TR, int8_t* planes, int* ex) {
   const int r = blockIdx.x;
   const double* row = X + static_cast<size_t>(r) * K;
   __shared__ double red[32];
@@ -67,13 +75,16 @@ __global__ void slice_rows(const double* X, int R, int K, int8_t* planes, int* e
   frexp(red[0], &e);  // max < 2^e
   if (red[0] == 0.0) e = 0;
   if (threadIdx.x == 0) ex[r] = e;
+  const size_t tiles = R / TR, kbs = K / 32;
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     // 56-bit fixed point relative to 2^e, split into 8 x 7-bit digits
     const long long q = llrint(ldexp(row[k], 7 * S - e));
     const long long a = q < 0 ? -q : q;
-    for (int s = 0; s < S; ++s) {
-      const int d = static_cast<int>((a >> (7 * (S - 1 - s))) & 127);
-      planes[(static_cast<size_t>(s) * R + r) * K + k] = static_cast<int8_t>(q < 0 ? -d : d);
+    const size_t in_tile = static_cast<size_t>((k % 32) / 16) * TR * 16 + (r % TR) * 16 + k % 16;
+    for (int s2 = 0; s2 < S; ++s2) {
+      const int d = static_cast<int>((a >> (7 * (S - 1 - s2))) & 127);
+      const size_t blk = (static_cast<size_t>(s2) * tiles + r / TR) * kbs + k / 32;
+      planes[blk * 32 * TR + in_tile] = static_cast<int8_t>(q < 0 ? -d : d);
     }
   }
 }
@@ -91,6 +102,7 @@ ozaki_gemm(const int8_t* Ap, const int8_t* Bp, const int* ea, const int* eb, dou
            int N, int K) {
   extern __shared__ __align__(1024) int8_t sm[];
   __shared__ __align__(8) uint64_t bar_free[NSTAGE];
+  __shared__ __align__(8) uint64_t bar_full[NSTAGE];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
@@ -98,86 +110,75 @@ ozaki_gemm(const int8_t* Ap, const int8_t* Bp, const int* ea, const int* eb, dou
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
-  if (tid == 0)
-    for (int i = 0; i < NSTAGE; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar_free[i])));
+  if (tid == 0) {
+    for (int i = 0; i < NSTAGE; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar_free[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar_full[i])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tmem = tmem_base;
 
-  // stage loader: canonical K-major layout, byte (r, k) of a plane at
-  // (k / 16) * ROWS * 16 + r * 16 + k % 16
-  auto load = [&](int stage, int k0) {
-    int8_t* base = sm + stage * STAGE;
-    {  // A: thread -> (row tid, all 4 chunks) of every plane
-      const int r = tid;  // TM == THREADS
-      const int8_t* src = Ap + (static_cast<size_t>(m0) + r) * K + k0;
-#pragma unroll
-      for (int s2 = 0; s2 < S; ++s2)
-#pragma unroll
-        for (int c = 0; c < BK / 16; ++c)
-          cp16(base + s2 * A_PLANE + c * TM * 16 + r * 16, src + static_cast<size_t>(s2) * M * K + c * 16);
-    }
-    int8_t* bb = base + S * A_PLANE;
-    {  // B: 64 rows x 4 chunks per plane = 256 copies -> 2 per thread per plane
-      const int r = tid & 63, c0 = (tid >> 6) * 2;
-      const int8_t* src = Bp + (static_cast<size_t>(n0) + r) * K + k0;
-#pragma unroll
-      for (int s2 = 0; s2 < S; ++s2)
-#pragma unroll
-        for (int c = c0; c < c0 + 2; ++c)
-          cp16(bb + s2 * B_PLANE + c * TN * 16 + r * 16, src + static_cast<size_t>(s2) * N * K + c * 16);
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-  };
-
   const int nk = K / BK;
   const uint32_t idesc = idesc_i8(TM, TN);
-  uint32_t phase[NSTAGE] = {0, 0};
-  load(0, 0);
-  for (int kb = 0; kb < nk; ++kb) {
-    const int st = kb % NSTAGE;
-    if (kb + 1 < nk) {
-      const int nst = (kb + 1) % NSTAGE;
-      if (kb + 1 >= NSTAGE) {  // the MMAs that read this stage must be done
-        asm volatile("{\n.reg .pred p;\nW1:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W1;\n}\n" ::"r"(smem_u32(&bar_free[nst])), "r"(phase[nst]));
-        phase[nst] ^= 1;
+  const size_t a_tiles = M / TM, b_tiles = N / TN;
+  // ONE thread runs the whole pipeline: bulk copies (TMA engine) fill a
+  // 4-stage ring, MMAs are queued as soon as a stage is full, and a stage is
+  // refilled once the tensor core has finished reading it.
+  if (tid == 0) {
+    auto fill = [&](int stage, int kb) {
+      const uint32_t bar = smem_u32(&bar_full[stage]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(STAGE));
+      int8_t* base = sm + stage * STAGE;
+      for (int s2 = 0; s2 < S; ++s2) {
+        const int8_t* a = Ap + ((static_cast<size_t>(s2) * a_tiles + blockIdx.y) * nk + kb) * A_PLANE;
+        const int8_t* b = Bp + ((static_cast<size_t>(s2) * b_tiles + blockIdx.x) * nk + kb) * B_PLANE;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     ::"r"(smem_u32(base + s2 * A_PLANE)), "l"(a), "r"(A_PLANE), "r"(bar) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     ::"r"(smem_u32(base + S * A_PLANE + s2 * B_PLANE)), "l"(b), "r"(B_PLANE), "r"(bar) : "memory");
       }
-      load(nst, (kb + 1) * BK);
-      asm volatile("cp.async.wait_group 1;\n" ::);
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-    }
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
+    };
+    uint32_t ph_full[NSTAGE] = {}, ph_free[NSTAGE] = {};
+    for (int p = 0; p < NSTAGE - 1 && p < nk; ++p) fill(p, p);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % NSTAGE;
+      asm volatile("{\n.reg .pred p;\nWF:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WF;\n}\n" ::"r"(smem_u32(&bar_full[st])), "r"(ph_full[st]));
+      ph_full[st] ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;\n");
-      // descriptors differ only in the start address (bits [0,14), 16-byte units)
       const uint64_t da0 = make_desc(smem_u32(sm + st * STAGE), TM * 16, 128);
       const uint64_t db0 = make_desc(smem_u32(sm + st * STAGE + S * A_PLANE), TN * 16, 128);
 #pragma unroll
       for (int i = 0; i < S; ++i)
 #pragma unroll
         for (int j = 0; j < S; ++j) {
-          const int lvl = i + j;  // 0-based level (i + j + 2 in 1-based digits)
+          const int lvl = i + j;
           if (lvl >= S) continue;
-#pragma unroll
-          for (int kk = 0; kk < BK / 32; ++kk) {
-            const uint64_t da = da0 + ((i * A_PLANE + kk * 2 * TM * 16) >> 4);
-            const uint64_t db = db0 + ((j * B_PLANE + kk * 2 * TN * 16) >> 4);
-            // first write of a level (kb 0, kk 0) is the (i = 0, j = lvl) pair
-            const uint32_t acc = (kb > 0 || kk > 0 || i > 0) ? 1u : 0u;
-            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + lvl * TN),
-                         "l"(da), "l"(db), "r"(idesc), "r"(acc));
-          }
+          const uint64_t da = da0 + ((i * A_PLANE) >> 4);
+          const uint64_t db = db0 + ((j * B_PLANE) >> 4);
+          const uint32_t acc = (kb > 0 || i > 0) ? 1u : 0u;  // first write: (0, lvl) in block 0
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem + lvl * TN),
+                       "l"(da), "l"(db), "r"(idesc), "r"(acc));
         }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&bar_free[st])));
+      const int nxt = kb + NSTAGE - 1;
+      if (nxt < nk) {
+        const int rst = nxt % NSTAGE;
+        if (kb >= 1) {  // K block kb-1 read this stage
+          asm volatile("{\n.reg .pred p;\nWR:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WR;\n}\n" ::"r"(smem_u32(&bar_free[rst])), "r"(ph_free[rst]));
+          ph_free[rst] ^= 1;
+        }
+        fill(rst, nxt);
+      }
     }
+    // tcgen05.commit tracks every earlier MMA of this thread
+    const int st = (nk - 1) % NSTAGE;
+    asm volatile("{\n.reg .pred p;\nW2:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W2;\n}\n" ::"r"(smem_u32(&bar_free[st])), "r"(ph_free[st]));
   }
-  // wait for the last commit of each stage
-  for (int st = 0; st < NSTAGE && st < nk; ++st) {
-    asm volatile("{\n.reg .pred p;\nW2:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W2;\n}\n" ::"r"(smem_u32(&bar_free[st])), "r"(phase[st]));
-  }
+  __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   // epilogue: row (warp*32 + lane) of the tile, 64 columns per level
   const int row = m0 + warp * 32 + lane;
@@ -235,9 +236,9 @@ int main(int argc, char** argv) {
   const int smem = NSTAGE * STAGE;
   cudaFuncSetAttribute(ozaki_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   auto run = [&]() {
-    slice_rows<<<N, 256>>>(A, N, N, Ap, ea);
+    slice_rows<<<N, 256>>>(A, N, N, TM, Ap, ea);
     transpose<<<dim3(N / 32, N / 32), dim3(32, 8)>>>(B, Bt, N, N);
-    slice_rows<<<N, 256>>>(Bt, N, N, Bp, eb);
+    slice_rows<<<N, 256>>>(Bt, N, N, TN, Bp, eb);
     ozaki_gemm<<<dim3(N / TN, N / TM), THREADS, smem>>>(Ap, Bp, ea, eb, C, N, N, N);
   };
   run();
