@@ -234,6 +234,13 @@ def test_cluster_kernel_with_side_chain(cuda):
         c, s, k, sc = orc.cos_sin(a32[i], "single")
         assert rel1(rep.cos_part[i], c) <= TOL32, i
         assert rel1(rep.sin_part[i], s) <= TOL32, i
+    aw, tw = laplacian_wave(rng, 1040, 112)
+    rep = csm.wave_cos_sin_batched(aw, tw)
+    for i in (0, 520, 1000, 1039):
+        c, s, k, sc = orc.wave_cos_sin(aw[i], tw[i])
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc), i
+        assert pair_close(rep.cos_part[i], c, s, TOL64)[0], i
+        assert pair_close(rep.sin_part[i], s, c, TOL64)[0], i
 
 
 @pytest.mark.parametrize("n", [64, 99, 128, 256])

@@ -78,3 +78,16 @@ def test_plan_run_host_back_to_back_calls(cuda):
     r2 = csm.cos_sin_batched(a2.numpy())
     assert np.array_equal(c1.numpy(), r1.cos_part) and np.array_equal(s1.numpy(), r1.sin_part)
     assert np.array_equal(c2.numpy(), r2.cos_part) and np.array_equal(s2.numpy(), r2.sin_part)
+
+
+def test_plan_run_host_wave(cuda):
+    rng = np.random.default_rng(740)
+    a, t = laplacian_wave(rng, 64, 48)
+    a_h = torch.from_numpy(a).pin_memory()
+    t_h = torch.from_numpy(t).pin_memory()
+    c_h, s_h = torch.empty_like(a_h).pin_memory(), torch.empty_like(a_h).pin_memory()
+    plan = BatchPlan(64, 48, wave=True, chunk=16)
+    plan.run_host(a_h, c_h, s_h, t_h, chunks=4)
+    torch.cuda.synchronize()
+    ref = csm.wave_cos_sin_batched(a, t)
+    assert np.array_equal(c_h.numpy(), ref.cos_part) and np.array_equal(s_h.numpy(), ref.sin_part)
