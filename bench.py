@@ -549,11 +549,17 @@ def main():
     ap.add_argument("--dist-mode", choices=["gather", "peer"], default="gather",
                     help="cfg5 only: NCCL all-gather per product, or the fused "
                          "peer-memory product (symmetric memory)")
+    ap.add_argument("--engine", choices=["dmma", "ozaki"], default="dmma",
+                    help="product engine of the tiled chain (n > 128) and the cfg5 slab "
+                         "products: FP64 DMMA, or Ozaki-II on the int8 tensor cores")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warm-up raised to 3 (timing rule)")
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    if args.impl != "reference" and args.engine != "dmma":
+        import paper_2010_00465_b200 as csm
+        csm.set_engine(args.engine)
     if args.impl == "reference":
         run_reference(args, cfg)
     elif cfg[0] == "cfg5":

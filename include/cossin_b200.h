@@ -206,10 +206,13 @@ int csm_theta_table(int family, int precision, double* theta_cos,
  *     input rows (slot 0 alias), s / tp = the matrix's s and t', dbl_step =
  *     -1 for chain ops or the doubling index; outputs that are final are
  *     also written to cos_out / sin_out (the caller's M x NP rows).
- *     scratch: device buffer of csm_slab_scratch_bytes(). */
+ *     scratch: device buffer of csm_slab_scratch_bytes()
+ *     + csm_slab_engine_bytes(M, NP) (the latter is the Ozaki engine's
+ *     scratch, 0 under the DMMA engine; csm_slab_op_peer always runs DMMA). */
 #define CSM_SLAB_SLOTS 9
 size_t csm_op_bytes(void);
 size_t csm_slab_scratch_bytes(void);
+size_t csm_slab_engine_bytes(int M, int NP);
 int csm_chain_program(int family, int k, int fold, void* ops_out, int max_ops,
                       int32_t* step_nops, int max_steps, int32_t* cos_slot,
                       int32_t* sin_slot);
@@ -237,6 +240,22 @@ int csm_slab_op_peer(const void* op, double* slab, int M, int NP, int row0,
  * captured in a CUDA graph; 0 for the tiled chain (it reads (k, s) back to
  * plan its launches). */
 int csm_graph_safe(int dtype, int64_t batch, int n);
+
+/* Product engine of the tiled chain (n > 128; also the Pade and standalone
+ * sine calls), process-wide.  CSM_ENGINE_DMMA (default): FP64 DMMA
+ * (mma.sync m8n8k4).  CSM_ENGINE_OZAKI: each product exactly on integers by
+ * the Ozaki-II scheme -- rows / columns scaled to P-bit integers, one
+ * tcgen05 int8 GEMM per modulus (15 moduli for float64 results, 9 for
+ * float32), Chinese-remainder reconstruction fused with the op's epilogue;
+ * used when the padded order is a multiple of 256, DMMA otherwise.  The
+ * chain, (k, s) and the reference interface are unchanged (the products of
+ * matcore.py:90-97 are computed differently).  csm_workspace_size depends on
+ * the engine: size workspaces after setting it.  Returns CSM_ERR_ARG for an
+ * unknown engine. */
+#define CSM_ENGINE_DMMA 0
+#define CSM_ENGINE_OZAKI 1
+int csm_set_engine(int engine);
+int csm_get_engine(void);
 
 /* ---- Measurement helpers (not part of the reference surface) ------------
  * csm_fp64_peak: time a DMMA (mma.sync m8n8k4 f64) throughput loop on the

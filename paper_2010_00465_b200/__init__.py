@@ -10,6 +10,8 @@ from .api import (
     BatchReport,
     cos_sin,
     cos_sin_batched,
+    get_engine,
+    set_engine,
     identity,
     matrix_from_rows,
     norm1,
@@ -71,6 +73,8 @@ __all__ = [
     "WaveResult",
     "cos_sin",
     "cos_sin_batched",
+    "get_engine",
+    "set_engine",
     "identity",
     "matrix_from_rows",
     "norm1",

@@ -58,6 +58,7 @@ SIGNATURES = {
     "csm_last_launch_count": (_i64, []),
     "csm_op_bytes": (_sz, []),
     "csm_slab_scratch_bytes": (_sz, []),
+    "csm_slab_engine_bytes": (_sz, [_i32, _i32]),
     "csm_chain_program": (_i32, [_i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _vp]),
     "csm_doubling_program": (_i32, [_i32, _i32, _i32, _i32, _vp]),
     "csm_slab_op": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _dp, _i32, _vp, _vp,
@@ -65,6 +66,8 @@ SIGNATURES = {
     "csm_slab_op_peer": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _dp, _i32,
                                 _vp, _vp, _i32, _vp, _vp]),
     "csm_graph_safe": (_i32, [_i32, _i64, _i32]),
+    "csm_set_engine": (_i32, [_i32]),
+    "csm_get_engine": (_i32, []),
     "csm_profile_enable": (_i32, [_i32]),
     "csm_profile_collect": (_i32, [_vp, _vp]),
 }

@@ -561,8 +561,26 @@ def write_matrix(path: str, a) -> None:
             fh.write(" ".join(repr(float(v)) for v in row) + "\n")
 
 
+_ENGINES = {"dmma": 0, "ozaki": 1}
+
+
+def set_engine(name: str) -> None:
+    """Select the product engine of the tiled chain (n > 128), process-wide
+    (csm_set_engine): "dmma" (FP64 DMMA, default) or "ozaki" (Ozaki-II:
+    exact int8 tensor-core GEMMs per modulus + CRT, for padded orders that
+    are multiples of 256).  Size workspaces (BatchPlan) after changing it."""
+    if name not in _ENGINES:
+        raise ValueError(f"engine must be one of {sorted(_ENGINES)}")
+    _lib.check(_lib.lib().csm_set_engine(_ENGINES[name]), "csm_set_engine")
+
+
+def get_engine() -> str:
+    code = int(_lib.lib().csm_get_engine())
+    return {v: k for k, v in _ENGINES.items()}[code]
+
+
 __all__ = [
-    "BatchReport", "cos_sin", "cos_sin_batched", "identity",
+    "BatchReport", "cos_sin", "get_engine", "set_engine", "cos_sin_batched", "identity",
     "pade_cos_sin", "pade_cos_sin_batched",
     "matrix_from_rows", "norm1", "read_matrix", "select_batch",
     "select_scheme", "taylor_cos_sin", "taylor_sin9", "wave_cos_sin",

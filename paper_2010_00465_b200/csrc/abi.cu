@@ -37,12 +37,15 @@ cudaError_t launch_schedule(const int32_t* K, const int32_t* S, const int32_t* s
                             int64_t batch, int* bins, int32_t* order, cudaStream_t stream,
                             int64_t* launches);
 size_t tiled_workspace_bytes(int64_t batch, int n);
+void set_engine(int e);
+int engine();
 int k1c_resident_sms();
 size_t op_bytes();
 int chain_program(bool wave, int k, bool fold, void* ops_out, int max_ops, int32_t* step_nops,
                   int max_steps, int32_t* cos_slot, int32_t* sin_slot);
 void doubling_program(int c0, int s0, int c1, int s1, void* ops_out);
 size_t slab_scratch_bytes();
+size_t slab_engine_bytes(int M, int NP);
 cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
                     const double* rhs_full, const double* in0, int s, double tp, int dbl_step,
                     void* cout, void* sout, int out_f32, void* scratch, cudaStream_t stream,
@@ -531,6 +534,11 @@ int csm_doubling_program(int c0, int s0, int c1, int s1, void* ops_out) {
   return CSM_SUCCESS;
 }
 
+size_t csm_slab_engine_bytes(int M, int NP) {
+  if (M <= 0 || NP <= 0) return 0;
+  return csm::slab_engine_bytes(M, NP);
+}
+
 int csm_slab_op(const void* op, double* slab, int M, int NP, int row0, const double* rhs_full,
                 const double* in0, int s, double tp, int dbl_step, void* cos_out, void* sin_out,
                 int out_f32, void* scratch, void* stream) {
@@ -772,6 +780,15 @@ int csm_profile_collect(double* total_ms, int64_t* intervals) {
   prof_clear();
   return CSM_SUCCESS;
 }
+
+int csm_set_engine(int engine) {
+  if (engine != CSM_ENGINE_DMMA && engine != CSM_ENGINE_OZAKI)
+    return fail(CSM_ERR_ARG, "engine must be CSM_ENGINE_DMMA or CSM_ENGINE_OZAKI");
+  csm::set_engine(engine);
+  return CSM_SUCCESS;
+}
+
+int csm_get_engine(void) { return csm::engine(); }
 
 int csm_fp64_peak(int iters, double* tflops, void* stream_v) {
   if (!tflops || iters <= 0) return fail(CSM_ERR_ARG, "bad arguments");

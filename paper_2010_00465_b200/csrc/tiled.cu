@@ -25,6 +25,7 @@
 // (trig / wave use), driver.py:91-98 (doubling), driver.py:115/:139
 // (scaling), matcore.py:107-121 (linear combinations, fused here).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -109,6 +110,129 @@ struct LaunchArgs {
   // tile, instead of reading an all-gathered copy.  Null otherwise.
   const double* const* rhs_parts;
 };
+
+// Slot sl of matrix b (slot 0 may alias the caller's input).
+__device__ __forceinline__ double* slot_ptr(const LaunchArgs& args, int b, int sl) {
+  const size_t slotsz = static_cast<size_t>(args.M) * args.NP;
+  if (sl == 0 && args.in0)
+    return const_cast<double*>(args.in0) + static_cast<size_t>(b) * slotsz;
+  return args.ws + static_cast<size_t>(b) * args.mat_stride + sl * slotsz;
+}
+
+// The op's linear combinations for output tile (tm, tn) of matrix b, from
+// the product tile E ([BM][LDE] in shared memory): row-contiguous
+// (coalesced) global reads of the slot terms and writes of the outputs.
+__device__ __forceinline__ void epilogue_tile(const LaunchArgs& args, const Op& op, int b,
+                                              int tm, int tn, const double* E) {
+  const int tid = threadIdx.x;
+  const int NP = args.NP;
+  const int n = args.n;
+  const size_t nn = static_cast<size_t>(n) * n;
+  const size_t slotsz = static_cast<size_t>(args.M) * NP;
+  double* base = args.ws + static_cast<size_t>(b) * args.mat_stride;
+  auto slot = [&](int sl) -> double* { return slot_ptr(args, b, sl); };
+  const int s_b = args.S[b];
+  const double sc_tp = args.tsc ? args.tsc[b] : 1.0;
+  const double sc_f = ldexp(1.0, -s_b), sc_f2 = ldexp(1.0, -2 * s_b);
+  const bool final_now = args.dbl_step < 0 ? (s_b == 0) : (s_b == args.dbl_step + 1);
+  const int nout = op.nout;
+  const int r0 = tm * BM, c0 = tn * BN;
+  // PB pairs per thread at a time: every slot-sourced term issues PB
+  // independent loads before its FMAs, so the workspace reads (HBM for
+  // large batches) overlap instead of exposing one latency per term.
+  constexpr int PB = CSM_TILED_PB;
+  static_assert((BM * BN / 2) % (PB * THREADS) == 0, "pair groups tile the output");
+  for (int p0 = tid; p0 < BM * BN / 2; p0 += PB * THREADS) {
+    size_t off[PB];
+    int ecol[PB];
+    double o0[PB][2], o1[PB][2];  // outputs 0 and 1 (OUTj terms of later outputs)
+#pragma unroll
+    for (int m = 0; m < PB; ++m) {
+      const int p = p0 + m * THREADS;
+      const int rr = p >> 5, cc = (p & 31) * 2;  // 32 pairs per tile row
+      off[m] = static_cast<size_t>(r0 + rr) * NP + c0 + cc;
+      ecol[m] = rr * LDE + cc;
+      o0[m][0] = o0[m][1] = o1[m][0] = o1[m][1] = 0.0;
+    }
+    for (int q = 0; q < nout; ++q) {
+      const OutSpec& os = op.out[q];
+      double v[PB][2];
+#pragma unroll
+      for (int m = 0; m < PB; ++m) v[m][0] = v[m][1] = 0.0;
+      for (int tt = 0; tt < os.nterms; ++tt) {
+        const int src = os.t[tt].src;
+        const double cf = os.t[tt].c;
+        if (src >= 0) {
+          const double* sp = slot(src);
+          double2 x[PB];
+#pragma unroll
+          for (int m = 0; m < PB; ++m) x[m] = *reinterpret_cast<const double2*>(sp + off[m]);
+#pragma unroll
+          for (int m = 0; m < PB; ++m) {
+            v[m][0] = fma(cf, x[m].x, v[m][0]);
+            v[m][1] = fma(cf, x[m].y, v[m][1]);
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < PB; ++m) {
+            double x0, x1;
+            if (src == SRC_ACC) {
+              const double2 av = *reinterpret_cast<const double2*>(E + ecol[m]);
+              x0 = av.x; x1 = av.y;
+            } else if (src == SRC_I) {
+              const int p = p0 + m * THREADS;
+              const int rg = r0 + (p >> 5) + args.row0, c = c0 + (p & 31) * 2;
+              x0 = (rg == c) ? 1.0 : 0.0;
+              x1 = (rg == c + 1) ? 1.0 : 0.0;
+            } else if (src == SRC_OUT0) {
+              x0 = o0[m][0]; x1 = o0[m][1];
+            } else {
+              x0 = o1[m][0]; x1 = o1[m][1];
+            }
+            v[m][0] = fma(cf, x0, v[m][0]);
+            v[m][1] = fma(cf, x1, v[m][1]);
+          }
+        }
+      }
+      if (os.scale != SC_NONE) {
+        const double sc = os.scale == SC_TP ? sc_tp : (os.scale == SC_F ? sc_f : sc_f2);
+#pragma unroll
+        for (int m = 0; m < PB; ++m) { v[m][0] *= sc; v[m][1] *= sc; }
+      }
+#pragma unroll
+      for (int m = 0; m < PB; ++m) {
+        if (q == 0) { o0[m][0] = v[m][0]; o0[m][1] = v[m][1]; }
+        if (q == 1) { o1[m][0] = v[m][0]; o1[m][1] = v[m][1]; }
+        *reinterpret_cast<double2*>(base + os.slot * slotsz + off[m]) =
+            make_double2(v[m][0], v[m][1]);
+      }
+      if (os.final != FIN_NONE && final_now) {
+        void* dst = os.final == FIN_COS ? args.cout : args.sout;
+#pragma unroll
+        for (int m = 0; m < PB; ++m) {
+          const int p = p0 + m * THREADS;
+          const int r = r0 + (p >> 5), c = c0 + (p & 31) * 2;
+          if (r >= n) continue;
+          const double v0 = v[m][0], v1 = v[m][1];
+          const size_t o = static_cast<size_t>(b) * nn + static_cast<size_t>(r) * n + c;
+          if (args.out_f32) {
+            float* d = static_cast<float*>(dst);
+            if (c < n) d[o] = static_cast<float>(v0);
+            if (c + 1 < n) d[o + 1] = static_cast<float>(v1);
+          } else {
+            double* d = static_cast<double*>(dst);
+            if (c + 1 < n && ((o & 1) == 0)) {
+              *reinterpret_cast<double2*>(d + o) = make_double2(v0, v1);
+            } else {
+              if (c < n) d[o] = v0;
+              if (c + 1 < n) d[o + 1] = v1;
+            }
+          }
+        }
+      }
+    }
+  }
+}
 
 // One 64x64 output tile of one matrix: acc = L R over the full NP-deep
 // contraction, then the op's linear combinations from the staged
@@ -226,109 +350,11 @@ __global__ void __launch_bounds__(THREADS, CSM_TILED_MINB) gemm_epi_kernel(const
             make_double2(acc[mi][ni][0], acc[mi][ni][1]);
     __syncthreads();
 
-    const int s_b = args.S[b];
-    const double sc_tp = args.tsc ? args.tsc[b] : 1.0;
-    const double sc_f = ldexp(1.0, -s_b), sc_f2 = ldexp(1.0, -2 * s_b);
-    const bool final_now = args.dbl_step < 0 ? (s_b == 0) : (s_b == args.dbl_step + 1);
-    const int nout = op.nout;
-    const int r0 = tm * BM, c0 = tn * BN;
-    // PB pairs per thread at a time: every slot-sourced term issues PB
-    // independent loads before its FMAs, so the workspace reads (HBM for
-    // large batches) overlap instead of exposing one latency per term.
-    constexpr int PB = CSM_TILED_PB;
-    static_assert((BM * BN / 2) % (PB * THREADS) == 0, "pair groups tile the output");
-    for (int p0 = tid; p0 < BM * BN / 2; p0 += PB * THREADS) {
-      size_t off[PB];
-      int ecol[PB];
-      double o0[PB][2], o1[PB][2];  // outputs 0 and 1 (OUTj terms of later outputs)
-#pragma unroll
-      for (int m = 0; m < PB; ++m) {
-        const int p = p0 + m * THREADS;
-        const int rr = p >> 5, cc = (p & 31) * 2;  // 32 pairs per tile row
-        off[m] = static_cast<size_t>(r0 + rr) * NP + c0 + cc;
-        ecol[m] = rr * LDE + cc;
-        o0[m][0] = o0[m][1] = o1[m][0] = o1[m][1] = 0.0;
-      }
-      for (int q = 0; q < nout; ++q) {
-        const OutSpec& os = op.out[q];
-        double v[PB][2];
-#pragma unroll
-        for (int m = 0; m < PB; ++m) v[m][0] = v[m][1] = 0.0;
-        for (int tt = 0; tt < os.nterms; ++tt) {
-          const int src = os.t[tt].src;
-          const double cf = os.t[tt].c;
-          if (src >= 0) {
-            const double* sp = slot(src);
-            double2 x[PB];
-#pragma unroll
-            for (int m = 0; m < PB; ++m) x[m] = *reinterpret_cast<const double2*>(sp + off[m]);
-#pragma unroll
-            for (int m = 0; m < PB; ++m) {
-              v[m][0] = fma(cf, x[m].x, v[m][0]);
-              v[m][1] = fma(cf, x[m].y, v[m][1]);
-            }
-          } else {
-#pragma unroll
-            for (int m = 0; m < PB; ++m) {
-              double x0, x1;
-              if (src == SRC_ACC) {
-                const double2 av = *reinterpret_cast<const double2*>(E + ecol[m]);
-                x0 = av.x; x1 = av.y;
-              } else if (src == SRC_I) {
-                const int p = p0 + m * THREADS;
-                const int rg = r0 + (p >> 5) + args.row0, c = c0 + (p & 31) * 2;
-                x0 = (rg == c) ? 1.0 : 0.0;
-                x1 = (rg == c + 1) ? 1.0 : 0.0;
-              } else if (src == SRC_OUT0) {
-                x0 = o0[m][0]; x1 = o0[m][1];
-              } else {
-                x0 = o1[m][0]; x1 = o1[m][1];
-              }
-              v[m][0] = fma(cf, x0, v[m][0]);
-              v[m][1] = fma(cf, x1, v[m][1]);
-            }
-          }
-        }
-        if (os.scale != SC_NONE) {
-          const double sc = os.scale == SC_TP ? sc_tp : (os.scale == SC_F ? sc_f : sc_f2);
-#pragma unroll
-          for (int m = 0; m < PB; ++m) { v[m][0] *= sc; v[m][1] *= sc; }
-        }
-#pragma unroll
-        for (int m = 0; m < PB; ++m) {
-          if (q == 0) { o0[m][0] = v[m][0]; o0[m][1] = v[m][1]; }
-          if (q == 1) { o1[m][0] = v[m][0]; o1[m][1] = v[m][1]; }
-          *reinterpret_cast<double2*>(base + os.slot * slotsz + off[m]) =
-              make_double2(v[m][0], v[m][1]);
-        }
-        if (os.final != FIN_NONE && final_now) {
-          void* dst = os.final == FIN_COS ? args.cout : args.sout;
-#pragma unroll
-          for (int m = 0; m < PB; ++m) {
-            const int p = p0 + m * THREADS;
-            const int r = r0 + (p >> 5), c = c0 + (p & 31) * 2;
-            if (r >= n) continue;
-            const double v0 = v[m][0], v1 = v[m][1];
-            const size_t o = static_cast<size_t>(b) * nn + static_cast<size_t>(r) * n + c;
-            if (args.out_f32) {
-              float* d = static_cast<float*>(dst);
-              if (c < n) d[o] = static_cast<float>(v0);
-              if (c + 1 < n) d[o + 1] = static_cast<float>(v1);
-            } else {
-              double* d = static_cast<double*>(dst);
-              if (c + 1 < n && ((o & 1) == 0)) {
-                *reinterpret_cast<double2*>(d + o) = make_double2(v0, v1);
-              } else {
-                if (c < n) d[o] = v0;
-                if (c + 1 < n) d[o + 1] = v1;
-              }
-            }
-          }
-        }
-      }
-    }
+    epilogue_tile(args, op, b, tm, tn, E);
   }
 }
+
+#include "ozaki.cuh"
 
 // slot0 <- f * A (zero padded).  Taylor: f = 2^-s; wave: t' = t/2^s,
 // f = t' * t', and tsc[b] = t'.  Only when slot 0 cannot alias the input.
@@ -385,6 +411,12 @@ inline cudaError_t ensure_smem_attr() {
   if (dev < 32 && ((done_mask >> dev) & 1u)) return cudaSuccess;
   e = cudaFuncSetAttribute(gemm_epi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(SMEM));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(oz_crt_epi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(SMEM));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(OZ_SMEM));
   if (e == cudaSuccess && dev < 32) done_mask |= 1u << dev;
   return e;
 }
@@ -800,6 +832,78 @@ void free_pair(int c0, int s0, int* c1, int* s1) {
 
 size_t tiled_np(int n) { return static_cast<size_t>((n + 63) / 64) * 64; }
 
+// Product engine (process-wide, csm_set_engine): 0 = FP64 DMMA, 1 = Ozaki-II
+// on the int8 tensor cores (ozaki.cuh) for the tiled chain when NP % 256 == 0.
+static int g_engine = 0;
+void set_engine(int e) { g_engine = e; }
+int engine() { return g_engine; }
+static bool oz_applies(int NP) { return g_engine == 1 && NP % tk::OZ_TN == 0; }
+// moduli: pairwise coprime, <= 256, largest first
+static const int kOzMods[tk::OZ_MAXM] = {256, 255, 253, 251, 247, 241, 239, 233,
+                                        229, 227, 223, 217, 211, 199, 197, 193};
+int oz_moduli(int out_f32) { return out_f32 ? 9 : 16; }
+
+// CRT constants for the first nm moduli and contraction depth K.
+tk::OzConst oz_const(int nm, int K) {
+  typedef unsigned __int128 u128;
+  tk::OzConst C{};
+  C.nm = nm;
+  u128 M = 1;
+  double log2M = 0.0;
+  for (int t = 0; t < nm; ++t) {
+    M *= static_cast<u128>(kOzMods[t]);
+    log2M += std::log2(static_cast<double>(kOzMods[t]));
+  }
+  // K 2^(2P) <= M / 4: the integer product is exact and |L'R'| < M / 4
+  C.P = static_cast<int>(std::floor((log2M - 2.0 - std::log2(static_cast<double>(K))) / 2.0));
+  const u128 mask = (static_cast<u128>(1) << tk::OZ_LVB) - 1;
+  for (int t = 0; t < nm; ++t) {
+    const int m = kOzMods[t];
+    C.mod[t] = m;
+    C.inv[t] = 1.0f / static_cast<float>(m);
+    const u128 Mt = M / static_cast<u128>(m);
+    const int a = static_cast<int>(Mt % static_cast<u128>(m));
+    int inv = 0;
+    for (int x = 1; x < m; ++x)
+      if ((a * x) % m == 1) { inv = x; break; }
+    const u128 W = (Mt * static_cast<u128>(inv)) % M;
+    for (int l = 0; l < tk::OZ_LV; ++l)
+      C.w[t][l] = static_cast<double>(
+          static_cast<uint64_t>((W >> (tk::OZ_LVB * (tk::OZ_LV - 1 - l))) & mask));
+  }
+  // groups of consecutive moduli whose product stays below 2^24
+  C.ng = 0;
+  double G = 1.0;
+  for (int t = 0; t < nm; ++t) {
+    if (G * kOzMods[t] >= 16777216.0) {
+      C.gmod[C.ng] = G;
+      C.gend[C.ng++] = t;
+      G = 1.0;
+    }
+    G *= kOzMods[t];
+  }
+  C.gmod[C.ng] = G;
+  C.gend[C.ng++] = nm;
+  for (int l = 0; l < tk::OZ_LV; ++l)
+    C.M[l] = static_cast<double>(
+        static_cast<uint64_t>((M >> (tk::OZ_LVB * (tk::OZ_LV - 1 - l))) & mask));
+  C.invM = 1.0 / (static_cast<double>(static_cast<uint64_t>(M >> 64)) * 18446744073709551616.0 +
+                  static_cast<double>(static_cast<uint64_t>(M)));
+  return C;
+}
+
+// Ozaki scratch per product item (M = NP rows): row / column maxima, the
+// residue planes of both operands and of the product.
+static size_t oz_item_bytes(size_t NP) {
+  return 2 * NP * sizeof(unsigned long long) + 3 * tk::OZ_MAXM * NP * NP + 256;
+}
+static int64_t oz_cap_items(int64_t batch, size_t NP) {
+  const size_t budget = static_cast<size_t>(4) << 30;
+  int64_t cap = static_cast<int64_t>(budget / oz_item_bytes(NP));
+  cap = std::max<int64_t>(1, std::min<int64_t>(cap, 2 * batch));
+  return std::min<int64_t>(cap, 65535 / tk::OZ_MAXM);
+}
+
 size_t tiled_workspace_bytes(int64_t batch, int n) {
   const size_t NP = tiled_np(n);
   size_t bytes = 0;
@@ -807,6 +911,8 @@ size_t tiled_workspace_bytes(int64_t batch, int n) {
   bytes += static_cast<size_t>(batch) * sizeof(double);                        // tsc
   bytes += static_cast<size_t>(batch) * 2 * sizeof(int32_t) + 256;             // idx
   bytes += 128 * sizeof(Op) + 256;                                             // op table
+  if (oz_applies(static_cast<int>(NP)))
+    bytes += static_cast<size_t>(oz_cap_items(batch, NP)) * oz_item_bytes(NP) + 1024;
   return bytes;
 }
 
@@ -815,12 +921,14 @@ struct TiledWs {
   double* tsc;
   int32_t* idx;
   Op* ops;
+  tk::OzArgs oz;  // Ozaki scratch (engine 1 only)
+  int64_t oz_cap;
 };
 
 static TiledWs carve(void* ws, int64_t batch, int n) {
   const size_t NP = tiled_np(n);
   char* p = static_cast<char*>(ws);
-  TiledWs w;
+  TiledWs w{};
   w.slots = reinterpret_cast<double*>(p);
   p += static_cast<size_t>(batch) * tk::NSLOT * NP * NP * sizeof(double);
   w.tsc = reinterpret_cast<double*>(p);
@@ -830,7 +938,50 @@ static TiledWs carve(void* ws, int64_t batch, int n) {
   p += static_cast<size_t>(batch) * 2 * sizeof(int32_t);
   p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
   w.ops = reinterpret_cast<Op*>(p);
+  p += 128 * sizeof(Op) + 256;
+  if (oz_applies(static_cast<int>(NP))) {
+    const int64_t cap = oz_cap_items(batch, NP);
+    p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+    w.oz_cap = cap;
+    w.oz.mxL = reinterpret_cast<unsigned long long*>(p);
+    p += static_cast<size_t>(cap) * NP * 8;
+    w.oz.mxR = reinterpret_cast<unsigned long long*>(p);
+    p += static_cast<size_t>(cap) * NP * 8;
+    p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+    w.oz.pL = reinterpret_cast<int8_t*>(p);
+    p += static_cast<size_t>(cap) * tk::OZ_MAXM * NP * NP;
+    w.oz.pR = reinterpret_cast<int8_t*>(p);
+    p += static_cast<size_t>(cap) * tk::OZ_MAXM * NP * NP;
+    w.oz.res = reinterpret_cast<int8_t*>(p);
+  }
   return w;
+}
+
+// One tiled launch (all items of plan A) through the Ozaki engine, in
+// chunks of at most cap items: maxima, residues, nm int8 GEMMs, CRT +
+// epilogue.  Seven launches per chunk.
+static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scratch, int64_t cap,
+                                 const tk::OzConst& C, cudaStream_t stream, int64_t* launches) {
+  const int NP = A.NP, M = A.M;
+  const unsigned tiles = static_cast<unsigned>((M / tk::BM) * (NP / tk::BN));
+  for (int done = 0; done < A.total; done += static_cast<int>(cap)) {
+    const int cnt = static_cast<int>(std::min<int64_t>(cap, A.total - done));
+    tk::OzArgs O = scratch;
+    O.item0 = done;
+    O.nitems = cnt;
+    cudaError_t e = cudaMemsetAsync(O.mxR, 0, static_cast<size_t>(cnt) * NP * 8, stream);
+    if (e != cudaSuccess) return e;
+    tk::oz_rowmax<<<dim3(M / 8, cnt), 256, 0, stream>>>(A, O);
+    tk::oz_colmax<<<dim3(NP / 256, NP / 256, cnt), 256, 0, stream>>>(A, O);
+    tk::oz_conv_rows<<<dim3(M / 128, NP / 16, cnt), 128, 0, stream>>>(A, O, C);
+    tk::oz_conv_cols<<<dim3(NP / 128, NP / 16, cnt), 128, 0, stream>>>(A, O, C);
+    tk::oz_gemm<<<dim3(NP / tk::OZ_TN, M / tk::OZ_TM, cnt * C.nm), tk::OZ_THREADS, tk::OZ_SMEM,
+                  stream>>>(A, O, C);
+    tk::oz_crt_epi<<<dim3(tiles, cnt), tk::THREADS, tk::SMEM, stream>>>(A, O, C);
+    *launches += 6;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // Run the tiled pipeline for a batch whose (k, s, status) are on the device.
@@ -995,6 +1146,8 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     A.row0 = 0;
     A.rhs_full = nullptr;
     A.rhs_parts = nullptr;
+    const bool use_oz = oz_applies(NP);
+    const tk::OzConst ozc = use_oz ? oz_const(oz_moduli(out_f32), NP) : tk::OzConst{};
     size_t lu_smem = 0;
     if (pade && NP == 64) {  // den + both right-hand sides staged in shared memory
       lu_smem = 3 * static_cast<size_t>(NP) * NP * sizeof(double);
@@ -1019,6 +1172,10 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
       A.nseg = static_cast<int>(L.seg.size());
       for (size_t i = 0; i < L.seg.size(); ++i) A.seg[i] = L.seg[i];
       A.total = L.total;
+      if (use_oz) {
+        if ((e = run_oz_launch(A, w.oz, w.oz_cap, ozc, stream, launches)) != cudaSuccess) return e;
+        continue;
+      }
       for (int done = 0; done < L.total; done += 65535) {
         A.item_base = done;
         const int cnt = std::min(65535, L.total - done);
@@ -1091,6 +1248,15 @@ void doubling_program(int c0, int s0, int c1, int s1, void* ops_out) {
 constexpr int kMaxParts = 64;
 size_t slab_scratch_bytes() { return sizeof(Op) + 64 + kMaxParts * sizeof(double*); }
 
+// Extra slab scratch the Ozaki engine needs for an M x NP slab (0 when the
+// DMMA engine runs it).
+static bool oz_slab_applies(int M, int NP) { return oz_applies(NP) && M % tk::OZ_TM == 0; }
+size_t slab_engine_bytes(int M, int NP) {
+  if (!oz_slab_applies(M, NP)) return 0;
+  const size_t m = static_cast<size_t>(M), np = static_cast<size_t>(NP);
+  return (m + np) * 8 + tk::OZ_MAXM * (2 * m * np + np * np) + 4 * 256;
+}
+
 // Run one Op on a block-row slab: out rows = L_rows * rhs_full (+ epilogue).
 // scratch: device buffer of slab_scratch_bytes() (op descriptor, s, t').
 cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
@@ -1141,6 +1307,24 @@ cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
   A.rhs_parts = nparts > 0 ? d->parts : nullptr;
   A.M = M;
   A.row0 = row0;
+  if (nparts == 0 && oz_slab_applies(M, NP)) {  // Ozaki engine (gathered right operand)
+    auto align = [](char* p) {
+      return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+    };
+    char* p = align(static_cast<char*>(scratch) + slab_scratch_bytes());
+    const size_t m = static_cast<size_t>(M), np = static_cast<size_t>(NP);
+    tk::OzArgs O{};
+    O.mxL = reinterpret_cast<unsigned long long*>(p);
+    p = align(p + m * 8);
+    O.mxR = reinterpret_cast<unsigned long long*>(p);
+    p = align(p + np * 8);
+    O.pL = reinterpret_cast<int8_t*>(p);
+    p = align(p + tk::OZ_MAXM * m * np);
+    O.pR = reinterpret_cast<int8_t*>(p);
+    p = align(p + tk::OZ_MAXM * np * np);
+    O.res = reinterpret_cast<int8_t*>(p);
+    return run_oz_launch(A, O, 1, oz_const(oz_moduli(out_f32), NP), stream, launches);
+  }
   dim3 grid(static_cast<unsigned>((M / tk::BM) * (NP / tk::BN)), 1, 1);
   tk::gemm_epi_kernel<<<grid, tk::THREADS, tk::SMEM, stream>>>(A);
   ++*launches;

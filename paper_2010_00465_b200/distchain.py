@@ -167,9 +167,10 @@ def cos_sin_distributed(a, precision: Precision = Precision.DOUBLE, *,
     cos_rows = torch.empty((M, n), dtype=torch.float64, device=dev)
     sin_rows = torch.empty_like(cos_rows)
     scratch = None
-    if dev.type == "cuda":
-        scratch = torch.empty(int(_lib.lib().csm_slab_scratch_bytes()), dtype=torch.uint8,
-                              device=dev)
+    if dev.type == "cuda":  # + the Ozaki engine's scratch when it runs the products
+        L = _lib.lib()
+        scratch = torch.empty(int(L.csm_slab_scratch_bytes()) + int(L.csm_slab_engine_bytes(M, n)),
+                              dtype=torch.uint8, device=dev)
     in0 = a[row0:row0 + M]
     cache: dict[int, object] = {}
     stats = DistStats(k, s, 0, 0)
