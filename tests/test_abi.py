@@ -76,3 +76,25 @@ def test_ddref_series_constants_match_reference(golden_dir):
     got = np.array(out[:])
     want = np.concatenate([d[:7, 0], d[:7, 1], d[7:, 0], d[7:, 1]])
     assert (got.view(np.uint64) == want.view(np.uint64)).all()
+
+
+def test_engine_switch_without_device():
+    """csm_set_engine is host-only: a bad engine is CSM_ERR_ARG, and the
+    Ozaki engine enlarges the tiled workspace (n = 256) but not n = 64 or
+    the DMMA-only orders (NP % 256 != 0)."""
+    lib = _lib.lib()
+    assert lib.csm_get_engine() == 0
+    assert lib.csm_set_engine(5) == _lib.ERR_ARG
+    assert "engine" in _lib.last_error()
+    dm256, dm320, dm64 = (lib.csm_workspace_size(0, 8, n) for n in (256, 320, 64))
+    assert lib.csm_slab_engine_bytes(512, 1024) == 0
+    assert lib.csm_set_engine(1) == 0
+    try:
+        assert lib.csm_get_engine() == 1
+        assert lib.csm_workspace_size(0, 8, 256) > dm256
+        assert lib.csm_workspace_size(0, 8, 320) == dm320
+        assert lib.csm_workspace_size(0, 8, 64) == dm64
+        # residue planes of L (M x NP), R (NP x NP) and the product, 16 moduli
+        assert lib.csm_slab_engine_bytes(512, 1024) >= 16 * (2 * 512 * 1024 + 1024 * 1024)
+    finally:
+        assert lib.csm_set_engine(0) == 0

@@ -1,0 +1,134 @@
+"""GPU parity of the Ozaki-II product engine (csm_set_engine(CSM_ENGINE_OZAKI)):
+the same chains, (k, s) and bars as test_gpu_parity.py, with every tiled
+product computed exactly on integers (one tcgen05 int8 GEMM per modulus +
+CRT).  The engine applies when the padded order is a multiple of 256; other
+orders run the DMMA engine (checked bit for bit)."""
+import numpy as np
+import pytest
+
+import paper_2010_00465_b200 as csm
+from oracle import cossin_oracle as orc
+from tests._util import cfg2_like, cfg3_like, laplacian_wave, pair_close, rel1
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-12
+TOL32 = 1e-5
+
+
+@pytest.fixture
+def ozaki(cuda):
+    csm.set_engine("ozaki")
+    yield
+    csm.set_engine("dmma")
+
+
+@pytest.mark.parametrize("n", [256, 512])
+def test_batched_cos_sin_parity(ozaki, n):
+    rng = np.random.default_rng(700 + n)
+    a = cfg2_like(rng, 6, n=n)
+    rep = csm.cos_sin_batched(a)
+    assert int(rep.s.max()) > 0  # the doubling products go through the engine too
+    for i in range(a.shape[0]):
+        c, s, k, sc = orc.cos_sin(a[i])
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc)
+        assert pair_close(rep.cos_part[i], c, s, TOL64)[0], (n, i, sc)
+        assert pair_close(rep.sin_part[i], s, c, TOL64)[0], (n, i, sc)
+
+
+def test_batched_wave_parity(ozaki):
+    rng = np.random.default_rng(811)
+    a, t = laplacian_wave(rng, 4, 256)
+    t = np.minimum(t, 3e-3)  # s <= 6: below the reference's own noise floor
+    rep = csm.wave_cos_sin_batched(a, t)
+    for i in range(a.shape[0]):
+        c, s, k, sc = orc.wave_cos_sin(a[i], t[i])
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc)
+        assert rel1(rep.cos_part[i], c) <= TOL64, (i, sc)
+        assert rel1(rep.sin_part[i], s) <= TOL64, (i, sc)
+
+
+def test_float32_variant_nine_moduli(ozaki):
+    """configs[2] family: float32 storage, 9 moduli (P = 30 bits)."""
+    rng = np.random.default_rng(812)
+    a = cfg3_like(rng, 6, n=256)
+    rep = csm.cos_sin_batched(a, csm.Precision.SINGLE)
+    assert rep.cos_part.dtype == np.float32
+    for i in range(a.shape[0]):
+        c, s, k, sc = orc.cos_sin(a[i], "single")           # reference as-is
+        c64, s64, _, _ = orc.cos_sin(a[i].astype(np.float64), "single")
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc)
+        for got, ref in ((rep.cos_part[i], c), (rep.sin_part[i], s),
+                         (rep.cos_part[i], c64), (rep.sin_part[i], s64)):
+            assert rel1(got, ref) <= TOL32
+
+
+def test_ozaki_agrees_with_dmma(ozaki):
+    rng = np.random.default_rng(813)
+    a = cfg2_like(rng, 4, n=256, lo=-1.0, hi=1.0)
+    oz = csm.cos_sin_batched(a)
+    csm.set_engine("dmma")
+    dm = csm.cos_sin_batched(a)
+    csm.set_engine("ozaki")
+    for i in range(a.shape[0]):
+        assert rel1(oz.cos_part[i], dm.cos_part[i]) <= 1e-13
+        assert rel1(oz.sin_part[i], dm.sin_part[i]) <= 1e-13
+
+
+def test_exact_identities(ozaki):
+    """Reference identities (tests/test_schemes.py:69-73, :98-110): the zero
+    matrix gives (I, 0) exactly and a diagonal input has exactly zero
+    off-diagonals -- the integer products keep every zero a zero."""
+    n = 256
+    rep = csm.cos_sin_batched(np.zeros((1, n, n)))
+    assert np.array_equal(rep.cos_part[0], np.eye(n))
+    assert not rep.sin_part[0].any()
+    d = np.diag(np.linspace(-3.0, 3.0, n))
+    rep = csm.cos_sin(d)
+    off = ~np.eye(n, dtype=bool)
+    assert not rep.result.cos_part[off].any() and not rep.result.sin_part[off].any()
+    np.testing.assert_allclose(np.diag(rep.result.cos_part), np.cos(np.diag(d)), rtol=0, atol=1e-14)
+    np.testing.assert_allclose(np.diag(rep.result.sin_part), np.sin(np.diag(d)), rtol=0, atol=1e-14)
+
+
+def test_other_orders_run_dmma_bit_for_bit(ozaki):
+    """NP = 320 is not a multiple of 256: the DMMA engine runs it."""
+    rng = np.random.default_rng(814)
+    a = cfg2_like(rng, 2, n=300)
+    oz = csm.cos_sin_batched(a)
+    csm.set_engine("dmma")
+    dm = csm.cos_sin_batched(a)
+    csm.set_engine("ozaki")
+    assert np.array_equal(oz.cos_part, dm.cos_part)
+    assert np.array_equal(oz.sin_part, dm.sin_part)
+
+
+def test_block_row_slab_engine(ozaki):
+    """cfg5 path (csm_slab_op) on one GPU through the Ozaki engine."""
+    import torch
+    from paper_2010_00465_b200 import distchain
+    n = 512
+    g = np.random.default_rng(0).standard_normal((n, n))
+    a = 20.0 * (g + g.T) / (2.0 * np.sqrt(n))
+    c, s, st = distchain.cos_sin_distributed(torch.from_numpy(a).cuda())
+    c_ref, s_ref, k, sc = orc.cos_sin(a)
+    assert (st.k, st.s) == (k, sc)
+    # the noise gate of test_block_row_single_gpu_against_oracle
+    assert rel1(c.cpu().numpy(), c_ref) <= 2e-11
+    assert rel1(s.cpu().numpy(), s_ref) <= 2e-11
+
+
+def test_workspace_follows_engine(cuda):
+    L = csm._lib.lib()
+    csm.set_engine("dmma")
+    small = int(L.csm_workspace_size(csm._lib.F64, 4, 256))
+    assert int(L.csm_slab_engine_bytes(256, 512)) == 0
+    csm.set_engine("ozaki")
+    try:
+        assert int(L.csm_workspace_size(csm._lib.F64, 4, 256)) > small
+        assert int(L.csm_slab_engine_bytes(256, 512)) > 0
+        assert int(L.csm_slab_engine_bytes(64, 512)) == 0  # M % 128 != 0: DMMA
+    finally:
+        csm.set_engine("dmma")
+    with pytest.raises(ValueError):
+        csm.set_engine("tf32")
