@@ -302,6 +302,138 @@ gemm_mod(const int8_t* Ap, const int8_t* Bp, int8_t* Rout, int M, int N, int K) 
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TN));
 }
 
+
+// 2-CTA variant (cta_group::2): a cluster pair computes a 256 x 256 tile;
+// CTA rank r holds A rows [128 r, +128) and B^T rows [128 r, +128) of the
+// pair's tile (planes with 128-row tiles for both operands) and receives
+// D rows [128 r, +128) x 256 in its own TMEM.  The leader (rank 0) issues
+// tcgen05.mma.cta_group::2 (M = 256, N = 256); each CTA's thread 0 fills its
+// own stages; the peer forwards "my stage landed" to the leader's full
+// barrier by a remote arrive; the leader's commit frees the stage in both
+// CTAs (multicast).
+constexpr int P_ST = 2 * 128 * KS;  // 32 KiB per stage per CTA
+template <int NST>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+gemm_mod2(const int8_t* Ap, const int8_t* Bp, int8_t* Rout, int M, int N, int K) {
+  extern __shared__ __align__(1024) int8_t sm[];
+  __shared__ __align__(8) uint64_t bar_free[NST];
+  __shared__ __align__(8) uint64_t bar_full[NST];
+  __shared__ __align__(8) uint64_t bar_done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  const int t = blockIdx.z;
+  const int nx = blockIdx.x >> 1, my = blockIdx.y;
+  const int atile = 2 * my + rank, btile = 2 * nx + rank;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar_free[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&bar_full[i])), "r"(rank == 0 ? 2 : 1));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar_done)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = tmem_base;
+  const int nk = K / KS;
+  const size_t kb32 = K / 32;
+  const int8_t* abase = Ap + (((size_t)t * (M / 128) + atile) * kb32) * 32 * 128;
+  const int8_t* bbase = Bp + (((size_t)t * (N / 128) + btile) * kb32) * 32 * 128;
+  // warp 0 / lane 0: producer (this CTA's halves of each stage)
+  // warp 1 / lane 0: leader -> MMA issuer; peer -> forwards "landed" to the leader
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % NST;
+      if (kb >= NST) {
+        const uint32_t par = ((kb / NST) - 1) & 1;
+        asm volatile("{\n.reg .pred p;\nWR:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WR;\n}\n" ::"r"(smem_u32(&bar_free[st])), "r"(par) : "memory");
+      }
+      const uint32_t bar = smem_u32(&bar_full[st]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(P_ST));
+      int8_t* base = sm + st * P_ST;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                   ::"r"(smem_u32(base)), "l"(abase + (size_t)kb * 128 * KS), "r"(128 * KS), "r"(bar) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                   ::"r"(smem_u32(base + 128 * KS)), "l"(bbase + (size_t)kb * 128 * KS), "r"(128 * KS), "r"(bar) : "memory");
+    }
+  } else if (warp == 1 && lane == 0) {
+    uint32_t leader_full0;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(leader_full0) : "r"(smem_u32(&bar_full[0])));
+    const uint32_t idesc = idesc_i8(256, 256);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % NST;
+      const uint32_t par = (kb / NST) & 1;
+      asm volatile("{\n.reg .pred p;\nWF:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WF;\n}\n" ::"r"(smem_u32(&bar_full[st])), "r"(par) : "memory");
+      if (rank != 0) {
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(leader_full0 + st * 8) : "memory");
+        continue;
+      }
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll
+      for (int j = 0; j < KS / 32; ++j) {
+        const uint64_t da = make_desc(smem_u32(sm + st * P_ST + j * 32 * 128), 128 * 16, 128);
+        const uint64_t db = make_desc(smem_u32(sm + st * P_ST + 128 * KS + j * 32 * 128), 128 * 16, 128);
+        const uint32_t acc = (kb > 0 || j > 0) ? 1u : 0u;
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                     "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                   ::"r"(smem_u32(&bar_free[st])), "h"((unsigned short)3));
+    }
+    if (rank == 0)
+      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                   ::"r"(smem_u32(&bar_done)), "h"((unsigned short)3));
+  }
+  __syncwarp();
+  // every thread: the pair's MMAs are complete (this CTA's TMEM is final)
+  asm volatile("{\n.reg .pred p;\nWD:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra WD;\n}\n" ::"r"(smem_u32(&bar_done)) : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const int row = 256 * my + 128 * rank + warp * 32 + lane;
+  const int n0 = 256 * nx;
+  const int mod = c_mod[t];
+  const float inv = c_inv[t];
+  int8_t* dst = Rout + ((size_t)t * M + row) * N + n0;
+#pragma unroll 1
+  for (int cb = 0; cb < 256; cb += 32) {
+    uint32_t v[32];
+    const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + cb;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+    uint32_t packed[8];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int x = (int)v[j];
+      int r = x - __float2int_rn(__int2float_rn(x) * inv) * mod;
+      if (r > 127) r -= mod;
+      if (r < -128) r += mod;
+      const uint32_t b = (uint32_t)(r & 0xff);
+      if ((j & 3) == 0) packed[j >> 2] = b;
+      else packed[j >> 2] |= b << (8 * (j & 3));
+    }
+    uint4* d4 = reinterpret_cast<uint4*>(dst + cb);
+    d4[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    d4[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
+}
+
 // residues -> C = (sum_t r_t W_t mod M) 2^-(sa_i + sb_j); 8 columns per thread
 __global__ void crt(const int8_t* Rr, int NM, int M, int N, const int* sa, const int* sb, double* C) {
   const size_t idx = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
@@ -408,6 +540,9 @@ int main(int argc, char** argv) {
   unsigned long long *mxa, *mxb;
   cudaMalloc(&mxa, N * 8); cudaMalloc(&mxb, N * 8);
   const bool slow = getenv("OZ_SLOWCONV") != nullptr;
+  const int pair = getenv("OZ_PAIR") ? atoi(getenv("OZ_PAIR")) : 0;
+  cudaFuncSetAttribute(gemm_mod2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * P_ST);
+  cudaFuncSetAttribute(gemm_mod2<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * P_ST);
   auto conv = [&]() {
     if (slow) {
       scale_rows<<<N, 256>>>(A, N, N, P, sa);
@@ -422,9 +557,13 @@ int main(int argc, char** argv) {
     shifts<<<(N + 255) / 256, 256>>>(mxa, N, P, sa);
     shifts<<<(N + 255) / 256, 256>>>(mxb, N, P, sb);
     conv_rows<<<dim3((N + 127) / 128, N / 16), 128>>>(A, N, N, sa, NM, Ap, TM);
-    conv_cols<<<dim3((N + 127) / 128, N / 16), 128>>>(B, N, N, sb, NM, Bp, TN);
+    conv_cols<<<dim3((N + 127) / 128, N / 16), 128>>>(B, N, N, sb, NM, Bp, pair ? 128 : TN);
   };
-  auto gemm = [&]() { gemm_mod<<<dim3(N / TN, N / TM, NM), THREADS, smem>>>(Ap, Bp, Rr, N, N, N); };
+  auto gemm = [&]() {
+    if (pair == 6) gemm_mod2<6><<<dim3(2 * (N / 256), N / 256, NM), THREADS, 6 * P_ST>>>(Ap, Bp, Rr, N, N, N);
+    else if (pair) gemm_mod2<4><<<dim3(2 * (N / 256), N / 256, NM), THREADS, 4 * P_ST>>>(Ap, Bp, Rr, N, N, N);
+    else gemm_mod<<<dim3(N / TN, N / TM, NM), THREADS, smem>>>(Ap, Bp, Rr, N, N, N);
+  };
   auto rec = [&]() { crt<<<(unsigned)((nn / 8 + 255) / 256), 256>>>(Rr, NM, N, N, sa, sb, C); };
   conv(); gemm(); rec();
   cudaError_t e = cudaDeviceSynchronize();
