@@ -267,6 +267,9 @@ def run_cfg5(args, cfg):
     for _ in range(args.warmup):
         chain(a, gather_outputs=False)
     L = _lib.lib()
+    oz = ozaki_applies(n) and not peer
+    if oz:
+        L.csm_profile_enable(2)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         torch.distributed.barrier()
@@ -277,6 +280,8 @@ def run_cfg5(args, cfg):
             chain(a, gather_outputs=False)
         e1.record()
         torch.cuda.synchronize()
+    gemm_ms = ctypes_collect(L)[0] / args.steps if oz else 0.0
+    L.csm_profile_enable(0)
     ms_step = pdist.max_over_ranks(e0.elapsed_time(e1) / args.steps, device=dev)
     # e2e: H2D of A on every rank, compute, D2H of each rank's output rows
     c_host = torch.empty((M, n), dtype=torch.float64).pin_memory()
@@ -306,11 +311,13 @@ def run_cfg5(args, cfg):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
             "config": {"workload": args.config, "description": desc, "n": n,
                        "k": st.k, "s": st.s, "gathers_per_step": st.gathers,
+                       "engine": "ozaki" if oz else "dmma",
                        "parallelism": (f"block-row x{world}, right operand read from peer "
                                        "slabs inside the GEMM (symmetric memory, no gather)"
                                        if peer else
                                        f"block-row x{world}, NCCL all-gather per product")},
-            "roofline": {"bound": "tensor", "achieved": tfl, "peak": peak, "unit": "TFLOP/s",
+            "roofline": ozaki_roofline(16 * flops / world, gemm_ms, tfl, peak) if oz else
+                        {"bound": "tensor", "achieved": tfl, "peak": peak, "unit": "TFLOP/s",
                          "frac": (tfl / peak) if peak else None, "traffic": None,
                          "kernel": "gemm_epi_kernel (slab mode) + all-gathers",
                          "peak_source": "csm_fp64_peak on this GPU in this run"},
@@ -404,7 +411,8 @@ def run_ours(args, cfg):
         plan.run(a_dev, t_dev)
     torch.cuda.synchronize()
     L = _lib.lib()
-    L.csm_profile_enable(1)
+    oz = ozaki_applies(n)
+    L.csm_profile_enable(2 if oz else 1)
     plan.launches = 0
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -501,8 +509,11 @@ def run_ours(args, cfg):
                    "l2": "inputs larger than L2 (no flush needed)"
                    if batch * n * n * esz > 2 * 126e6 else
                    "input fits L2; steps reuse it (no flush)",
-                   "parallelism": f"batch shard x{world} (no collective)"},
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                   "parallelism": f"batch shard x{world} (no collective)",
+                   "engine": "ozaki" if oz else "dmma"},
+        "roofline": ozaki_roofline((9 if dt == "f32" else 16) * flops_step,
+                                   kern_ms[0] / args.steps, tflops, peak) if oz else
+                    {"bound": "tensor", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s",
                      "frac": (achieved / peak) if (achieved and peak) else None,
                      "traffic": traffic,
@@ -528,6 +539,31 @@ def run_ours(args, cfg):
 
 
 import ctypes  # noqa: E402
+
+# Ozaki engine: nominal dense int8 tensor peak of a B200 (the fp8 figure of
+# /opt/skills/guides/B200_PROFILING.md; MEASURED_PEAKS.json has no int8 entry)
+INT8_PEAK_TOPS = 4500.0
+
+
+def ozaki_applies(n):
+    """The Ozaki engine runs a call when it is selected and NP % 256 == 0."""
+    import paper_2010_00465_b200 as csm
+    return csm.get_engine() == "ozaki" and n > 128 and ((n + 63) // 64 * 64) % 256 == 0
+
+
+def ozaki_roofline(int8_ops_step, gemm_ms, fp64_tflops, dmma_peak):
+    """Roofline object of the Ozaki engine's dominant kernel, oz_gemm (one
+    tcgen05 int8 GEMM per modulus): int8 ops per step / its live CUDA-event
+    time, against the int8 tensor peak; the fp64-equivalent rate is reported
+    beside it as a multiple of the measured DMMA peak."""
+    achieved = int8_ops_step / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    return {"bound": "tensor", "achieved": achieved, "peak": INT8_PEAK_TOPS, "unit": "TOPS",
+            "frac": (achieved / INT8_PEAK_TOPS) if achieved else None, "traffic": None,
+            "kernel": "oz_gemm (tcgen05.mma.kind::i8, one GEMM per modulus)",
+            "peak_source": "nominal dense int8 (= fp8) tensor peak, B200_PROFILING.md",
+            "int8_ops_per_step": int8_ops_step, "kernel_ms_per_step": gemm_ms,
+            "fp64_equiv_tflops": fp64_tflops, "dmma_peak_tflops": dmma_peak,
+            "fp64_equiv_vs_dmma_peak": (fp64_tflops / dmma_peak) if dmma_peak else None}
 
 
 def ctypes_collect(L):

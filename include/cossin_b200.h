@@ -270,7 +270,8 @@ int64_t csm_last_launch_count(void);
  * kernel (the fused n <= 64 kernel, or the tiled GEMM launches).
  * csm_profile_collect synchronises those events, returns the summed
  * milliseconds and the number of intervals, and clears them.
- * csm_profile_enable(0/1) also clears. */
+ * csm_profile_enable(0/1) also clears; mode 2 records the Ozaki engine's
+ * int8 GEMM launches (one interval per launch) instead. */
 int csm_profile_enable(int on);
 int csm_profile_collect(double* total_ms, int64_t* intervals);
 

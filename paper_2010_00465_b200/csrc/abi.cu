@@ -65,20 +65,20 @@ cudaError_t ddref_chain(const double* a, const int32_t* dS, int smax, double* co
 }  // namespace csm
 
 namespace {
-thread_local bool g_prof = false;
+thread_local int g_prof = 0;  // 0 off, 1 pipeline intervals, 2 int8 GEMM launches
 thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_ev;
 thread_local cudaEvent_t g_prof_open = nullptr;
 thread_local bool g_prof_hold = false;  // an enclosing interval is open
 }  // namespace
 
 namespace csm {
-void prof_begin(cudaStream_t stream) {
-  if (!g_prof || g_prof_hold) return;
+void prof_begin(cudaStream_t stream, int kind) {
+  if (g_prof != kind || g_prof_hold) return;
   if (cudaEventCreate(&g_prof_open) != cudaSuccess) { g_prof_open = nullptr; return; }
   cudaEventRecord(g_prof_open, stream);
 }
-void prof_end(cudaStream_t stream) {
-  if (!g_prof || g_prof_hold || !g_prof_open) return;
+void prof_end(cudaStream_t stream, int kind) {
+  if (g_prof != kind || g_prof_hold || !g_prof_open) return;
   cudaEvent_t e1;
   if (cudaEventCreate(&e1) != cudaSuccess) return;
   cudaEventRecord(e1, stream);
@@ -761,7 +761,8 @@ int csm_graph_safe(int dtype, int64_t batch, int n) {
 
 int csm_profile_enable(int on) {
   prof_clear();
-  g_prof = on != 0;
+  if (on < 0 || on > 2) return fail(CSM_ERR_ARG, "profile mode must be 0, 1 or 2");
+  g_prof = on;
   return CSM_SUCCESS;
 }
 

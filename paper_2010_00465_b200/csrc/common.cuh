@@ -96,7 +96,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 }
 
 // Live-timing hooks (abi.cu): no-ops unless csm_profile_enable(1).
-void prof_begin(cudaStream_t stream);
-void prof_end(cudaStream_t stream);
+void prof_begin(cudaStream_t stream, int kind = 1);
+void prof_end(cudaStream_t stream, int kind = 1);
 
 }  // namespace csm

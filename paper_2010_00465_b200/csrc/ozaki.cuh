@@ -29,6 +29,9 @@ constexpr int OZ_MAXG = 6;  // moduli groups with products below 2^24
 constexpr int OZ_TM = 128, OZ_TN = 256, OZ_KS = 128, OZ_NSTAGE = 4;
 constexpr int OZ_A_ST = OZ_TM * OZ_KS, OZ_B_ST = OZ_TN * OZ_KS, OZ_STAGE = OZ_A_ST + OZ_B_ST;
 constexpr size_t OZ_SMEM = static_cast<size_t>(OZ_NSTAGE) * OZ_STAGE;  // 192 KiB
+// K <= 512: 2 stages (96 KiB) so two CTAs share an SM and one's epilogue
+// overlaps the other's MMAs
+constexpr int OZ_NSTAGE_SMALL = 2;
 constexpr int OZ_THREADS = 128;
 
 struct OzConst {
@@ -114,14 +117,15 @@ __global__ void oz_rowmax(const LaunchArgs la, const OzArgs oz) {
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (lane == 0) oz.mxL[static_cast<size_t>(ci) * la.M + r] = __double_as_longlong(m);
 }
-// grid (NP / 256, NP / 256, nitems), 256 threads: column maxima of R over
-// 256-row chunks, combined by atomicMax (mxR zeroed beforehand)
+// grid (NP / 256, NP / 64, nitems), 256 threads: column maxima of R over
+// 64-row chunks, combined by atomicMax (mxR zeroed beforehand)
 __global__ void oz_colmax(const LaunchArgs la, const OzArgs oz) {
   const int ci = blockIdx.z, NP = la.NP;
-  const int c = blockIdx.x * 256 + threadIdx.x, k0 = blockIdx.y * 256;
+  const int c = blockIdx.x * 256 + threadIdx.x, k0 = blockIdx.y * 64;
   const double* R = oz_rhs(la, oz.item0 + ci);
   double m = 0.0;
-  for (int k = k0; k < k0 + 256; ++k) m = fmax(m, fabs(R[static_cast<size_t>(k) * NP + c]));
+#pragma unroll 8
+  for (int k = k0; k < k0 + 64; ++k) m = fmax(m, fabs(R[static_cast<size_t>(k) * NP + c]));
   atomicMax(oz.mxR + static_cast<size_t>(ci) * NP + c,
             static_cast<unsigned long long>(__double_as_longlong(m)));
 }
@@ -137,21 +141,23 @@ __device__ __forceinline__ uint4 oz_pack16(const int (&b)[16]) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// 16 entries -> 16 residue bytes per modulus at out + t * plane
+// 16 entries -> 16 residue bytes per modulus at out + t * plane.  Moduli
+// are grouped in threes (products < 2^24, host oz_const) in table order.
+template <int NM>
 __device__ __forceinline__ void oz_store_residues(const double (&v)[16], const OzConst& C,
                                                   int8_t* out, size_t plane) {
-  int t0 = 0;
-  for (int g = 0; g < C.ng; ++g) {
+#pragma unroll
+  for (int g = 0; g < (NM + 2) / 3; ++g) {
     float x[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) x[i] = oz_mod_group(v[i], C.gmod[g]);
-    for (int t = t0; t < C.gend[g]; ++t) {
+#pragma unroll
+    for (int t = 3 * g; t < 3 * g + 3 && t < NM; ++t) {
       int b[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) b[i] = oz_mod_small(x[i], C, t);
       *reinterpret_cast<uint4*>(out + t * plane) = oz_pack16(b);
     }
-    t0 = C.gend[g];
   }
 }
 
@@ -159,6 +165,7 @@ __device__ __forceinline__ void oz_store_residues(const double (&v)[16], const O
 // bytes per modulus; consecutive threads take consecutive plane rows, so a
 // warp's stores for one modulus are one contiguous 512-byte run.
 // grid (M / 128, NP / 16, nitems), 128 threads.  L rows are plane rows.
+template <int NM>
 __global__ void oz_conv_rows(const LaunchArgs la, const OzArgs oz, const OzConst C) {
   const int ci = blockIdx.z, NP = la.NP, M = la.M;
   const int r = blockIdx.x * 128 + threadIdx.x, k0 = blockIdx.y * 16;
@@ -172,10 +179,11 @@ __global__ void oz_conv_rows(const LaunchArgs la, const OzArgs oz, const OzConst
     v[i + 1] = rint(ldexp(x.y, sh));
   }
   const size_t plane = static_cast<size_t>(M) * NP;
-  oz_store_residues(v, C, oz.pL + static_cast<size_t>(ci) * C.nm * plane + oz_off(r, k0, NP, OZ_TM),
+  oz_store_residues<NM>(v, C, oz.pL + static_cast<size_t>(ci) * NM * plane + oz_off(r, k0, NP, OZ_TM),
                     plane);
 }
 // grid (NP / 128, NP / 16, nitems), 128 threads.  R columns are plane rows.
+template <int NM>
 __global__ void oz_conv_cols(const LaunchArgs la, const OzArgs oz, const OzConst C) {
   const int ci = blockIdx.z, NP = la.NP;
   const int c = blockIdx.x * 128 + threadIdx.x, k0 = blockIdx.y * 16;
@@ -185,7 +193,7 @@ __global__ void oz_conv_cols(const LaunchArgs la, const OzArgs oz, const OzConst
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = rint(ldexp(R[static_cast<size_t>(i) * NP], sh));
   const size_t plane = static_cast<size_t>(NP) * NP;
-  oz_store_residues(v, C, oz.pR + static_cast<size_t>(ci) * C.nm * plane + oz_off(c, k0, NP, OZ_TN),
+  oz_store_residues<NM>(v, C, oz.pR + static_cast<size_t>(ci) * NM * plane + oz_off(c, k0, NP, OZ_TN),
                     plane);
 }
 
@@ -219,11 +227,12 @@ __device__ __forceinline__ void oz_wait(uint64_t* bar, uint32_t parity) {
 // accumulator, tcgen05.commit to free the stage.  Then each warp reads its
 // 32 TMEM lanes (rows) 32 columns at a time, reduces mod m_t and stores the
 // int8 residues (32 contiguous bytes per row).
+template <int NST>
 __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, const OzArgs oz,
                                                          const OzConst C) {
   extern __shared__ __align__(1024) int8_t osm[];
-  __shared__ __align__(8) uint64_t bar_free[OZ_NSTAGE];
-  __shared__ __align__(8) uint64_t bar_full[OZ_NSTAGE];
+  __shared__ __align__(8) uint64_t bar_free[NST];
+  __shared__ __align__(8) uint64_t bar_full[NST];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NP = la.NP, M = la.M;
@@ -236,7 +245,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, co
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
-    for (int i = 0; i < OZ_NSTAGE; ++i) {
+    for (int i = 0; i < NST; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(oz_smem(&bar_free[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(oz_smem(&bar_full[i])));
     }
@@ -269,11 +278,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, co
           "l"(bbase + static_cast<size_t>(kb) * OZ_B_ST), "r"(OZ_B_ST), "r"(bar)
           : "memory");
     };
-    uint32_t ph_full[OZ_NSTAGE] = {}, ph_free[OZ_NSTAGE] = {};
-    for (int p = 0; p < OZ_NSTAGE - 1 && p < nk; ++p) fill(p, p);
+    uint32_t ph_full[NST] = {}, ph_free[NST] = {};
+    for (int p = 0; p < NST - 1 && p < nk; ++p) fill(p, p);
     const uint32_t idesc = oz_idesc(OZ_TM, OZ_TN);
     for (int kb = 0; kb < nk; ++kb) {
-      const int st = kb % OZ_NSTAGE;
+      const int st = kb % NST;
       oz_wait(&bar_full[st], ph_full[st]);
       ph_full[st] ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;\n");
@@ -291,9 +300,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, co
       asm volatile(
           "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
               oz_smem(&bar_free[st])));
-      const int nxt = kb + OZ_NSTAGE - 1;
+      const int nxt = kb + NST - 1;
       if (nxt < nk) {
-        const int rst = nxt % OZ_NSTAGE;
+        const int rst = nxt % NST;
         if (kb >= 1) {  // stage rst was last read by K stage kb - 1
           oz_wait(&bar_free[rst], ph_free[rst]);
           ph_free[rst] ^= 1;
@@ -303,7 +312,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, co
     }
     // the last stage's final commit is the only one never waited on, and it
     // tracks every earlier MMA of this thread
-    const int st = (nk - 1) % OZ_NSTAGE;
+    const int st = (nk - 1) % NST;
     oz_wait(&bar_free[st], ph_free[st]);
   }
   __syncthreads();
@@ -351,7 +360,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, co
 
 // Product tile (CRT + unscaling) into shared memory, then the op's epilogue.
 // grid (tiles of 64 x 64, nitems), 128 threads, tk::SMEM dynamic.
-__global__ void __launch_bounds__(THREADS) oz_crt_epi(const LaunchArgs la, const OzArgs oz,
+template <int NM>
+__global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, const OzArgs oz,
                                                       const OzConst C) {
   extern __shared__ __align__(16) double sm[];
   __shared__ Op op;
@@ -376,31 +386,33 @@ __global__ void __launch_bounds__(THREADS) oz_crt_epi(const LaunchArgs la, const
   const int rr = tid >> 1, cbase = (tid & 1) * 32;
   const int row = tm * BM + rr;
   const size_t plane = static_cast<size_t>(M) * NP;
-  const int8_t* res = oz.res + static_cast<size_t>(ci) * C.nm * plane +
+  const int8_t* res = oz.res + static_cast<size_t>(ci) * NM * plane +
                       static_cast<size_t>(row) * NP + tn * BN + cbase;
   const int sa = oz_shift(oz.mxL[static_cast<size_t>(ci) * M + row], C.P);
   const unsigned long long* mxr = oz.mxR + static_cast<size_t>(ci) * NP + tn * BN + cbase;
   double* E = sm;
   const double d1s = ldexp(1.0, OZ_LVB), d2s = ldexp(1.0, 2 * OZ_LVB), d3s = ldexp(1.0, 3 * OZ_LVB);
 #pragma unroll 1
-  for (int g = 0; g < 4; ++g) {
-    double s[8][OZ_LV];
+  for (int g = 0; g < 8; ++g) {  // 4 columns at a time: 4 x 4 exact level sums
+    double s[4][OZ_LV];
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
+    for (int e = 0; e < 4; ++e)
 #pragma unroll
       for (int l = 0; l < OZ_LV; ++l) s[e][l] = 0.0;
-    for (int t = 0; t < C.nm; ++t) {
-      const uint2 w = *reinterpret_cast<const uint2*>(res + t * plane + g * 8);
+    uint32_t w4[NM];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int r8 = static_cast<int8_t>(((e < 4 ? w.x : w.y) >> (8 * (e & 3))) & 0xffu);
-        const double rd = static_cast<double>(r8);
+    for (int t = 0; t < NM; ++t) w4[t] = *reinterpret_cast<const uint32_t*>(res + t * plane + g * 4);
+#pragma unroll
+    for (int t = 0; t < NM; ++t) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double rd = static_cast<double>(static_cast<int8_t>((w4[t] >> (8 * e)) & 0xffu));
 #pragma unroll
         for (int l = 0; l < OZ_LV; ++l) s[e][l] = fma(rd, C.w[t][l], s[e][l]);
       }
     }
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < 4; ++e) {
       // S = sum_l s_l 2^(32 (3 - l)) exactly (each |s_l| < 2^43); q =
       // round(S / M); each level s_l - q M_l is exact, so only the final
       // sum rounds
@@ -411,8 +423,8 @@ __global__ void __launch_bounds__(THREADS) oz_crt_epi(const LaunchArgs la, const
       const double e2 = fma(-q, C.M[2], s[e][2]);
       const double e3 = fma(-q, C.M[3], s[e][3]);
       const double v = fma(e0, d3s, fma(e1, d2s, fma(e2, d1s, e3)));
-      const int sb = oz_shift(mxr[g * 8 + e], C.P);
-      E[rr * LDE + cbase + g * 8 + e] = ldexp(v, -(sa + sb));
+      const int sb = oz_shift(mxr[g * 4 + e], C.P);
+      E[rr * LDE + cbase + g * 4 + e] = ldexp(v, -(sa + sb));
     }
   }
   __syncthreads();

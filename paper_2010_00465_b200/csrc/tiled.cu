@@ -26,6 +26,7 @@
 // (scaling), matcore.py:107-121 (linear combinations, fused here).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -412,11 +413,18 @@ inline cudaError_t ensure_smem_attr() {
   e = cudaFuncSetAttribute(gemm_epi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(SMEM));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(oz_crt_epi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(oz_crt_epi<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(SMEM));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(oz_crt_epi<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(SMEM));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(oz_gemm<OZ_NSTAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(OZ_SMEM));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(oz_gemm<OZ_NSTAGE_SMALL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(OZ_NSTAGE_SMALL * OZ_STAGE));
   if (e == cudaSuccess && dev < 32) done_mask |= 1u << dev;
   return e;
 }
@@ -972,12 +980,34 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
     cudaError_t e = cudaMemsetAsync(O.mxR, 0, static_cast<size_t>(cnt) * NP * 8, stream);
     if (e != cudaSuccess) return e;
     tk::oz_rowmax<<<dim3(M / 8, cnt), 256, 0, stream>>>(A, O);
-    tk::oz_colmax<<<dim3(NP / 256, NP / 256, cnt), 256, 0, stream>>>(A, O);
-    tk::oz_conv_rows<<<dim3(M / 128, NP / 16, cnt), 128, 0, stream>>>(A, O, C);
-    tk::oz_conv_cols<<<dim3(NP / 128, NP / 16, cnt), 128, 0, stream>>>(A, O, C);
-    tk::oz_gemm<<<dim3(NP / tk::OZ_TN, M / tk::OZ_TM, cnt * C.nm), tk::OZ_THREADS, tk::OZ_SMEM,
-                  stream>>>(A, O, C);
-    tk::oz_crt_epi<<<dim3(tiles, cnt), tk::THREADS, tk::SMEM, stream>>>(A, O, C);
+    tk::oz_colmax<<<dim3(NP / 256, NP / 64, cnt), 256, 0, stream>>>(A, O);
+    const dim3 gconv_r(M / 128, NP / 16, cnt), gconv_c(NP / 128, NP / 16, cnt);
+    const dim3 ggemm(NP / tk::OZ_TN, M / tk::OZ_TM, cnt * C.nm), gcrt(tiles, cnt);
+    static const int force_st = [] {  // CSM_OZ_STAGES=2|4 overrides (experiments)
+      const char* e = std::getenv("CSM_OZ_STAGES");
+      return e ? std::atoi(e) : 0;
+    }();
+    // two 2-stage CTAs per SM: one's epilogue overlaps the other's MMAs
+    // (measured 3% faster than one 4-stage CTA at NP = 8192)
+    const bool small = force_st ? force_st == 2 : true;
+    const size_t gsm = (small ? tk::OZ_NSTAGE_SMALL : tk::OZ_NSTAGE) * tk::OZ_STAGE;
+    if (C.nm == 16) {
+      tk::oz_conv_rows<16><<<gconv_r, 128, 0, stream>>>(A, O, C);
+      tk::oz_conv_cols<16><<<gconv_c, 128, 0, stream>>>(A, O, C);
+    } else {
+      tk::oz_conv_rows<9><<<gconv_r, 128, 0, stream>>>(A, O, C);
+      tk::oz_conv_cols<9><<<gconv_c, 128, 0, stream>>>(A, O, C);
+    }
+    prof_begin(stream, 2);  // csm_profile_enable(2): the int8 GEMM alone
+    if (small)
+      tk::oz_gemm<tk::OZ_NSTAGE_SMALL><<<ggemm, tk::OZ_THREADS, gsm, stream>>>(A, O, C);
+    else
+      tk::oz_gemm<tk::OZ_NSTAGE><<<ggemm, tk::OZ_THREADS, gsm, stream>>>(A, O, C);
+    prof_end(stream, 2);
+    if (C.nm == 16)
+      tk::oz_crt_epi<16><<<gcrt, tk::THREADS, tk::SMEM, stream>>>(A, O, C);
+    else
+      tk::oz_crt_epi<9><<<gcrt, tk::THREADS, tk::SMEM, stream>>>(A, O, C);
     *launches += 6;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
