@@ -987,9 +987,9 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
       const char* e = std::getenv("CSM_OZ_STAGES");
       return e ? std::atoi(e) : 0;
     }();
-    // two 2-stage CTAs per SM: one's epilogue overlaps the other's MMAs
-    // (measured 3% faster than one 4-stage CTA at NP = 8192)
-    const bool small = force_st ? force_st == 2 : true;
+    // NP <= 512 (K <= 4 stages anyway): two 2-stage CTAs per SM, one's
+    // epilogue overlapping the other's MMAs; larger: one 4-stage CTA per SM
+    const bool small = force_st ? force_st == 2 : NP <= 512;
     const size_t gsm = (small ? tk::OZ_NSTAGE_SMALL : tk::OZ_NSTAGE) * tk::OZ_STAGE;
     if (C.nm == 16) {
       tk::oz_conv_rows<16><<<gconv_r, 128, 0, stream>>>(A, O, C);
@@ -998,12 +998,23 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
       tk::oz_conv_rows<9><<<gconv_r, 128, 0, stream>>>(A, O, C);
       tk::oz_conv_cols<9><<<gconv_c, 128, 0, stream>>>(A, O, C);
     }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;  // pairs of M tiles share B
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 2;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = ggemm;
+    cfg.blockDim = dim3(tk::OZ_THREADS);
+    cfg.dynamicSmemBytes = gsm;
+    cfg.stream = stream;
     prof_begin(stream, 2);  // csm_profile_enable(2): the int8 GEMM alone
-    if (small)
-      tk::oz_gemm<tk::OZ_NSTAGE_SMALL><<<ggemm, tk::OZ_THREADS, gsm, stream>>>(A, O, C);
-    else
-      tk::oz_gemm<tk::OZ_NSTAGE><<<ggemm, tk::OZ_THREADS, gsm, stream>>>(A, O, C);
+    e = small ? cudaLaunchKernelEx(&cfg, tk::oz_gemm<tk::OZ_NSTAGE_SMALL>, A, O, C)
+              : cudaLaunchKernelEx(&cfg, tk::oz_gemm<tk::OZ_NSTAGE>, A, O, C);
     prof_end(stream, 2);
+    if (e != cudaSuccess) return e;
     if (C.nm == 16)
       tk::oz_crt_epi<16><<<gcrt, tk::THREADS, tk::SMEM, stream>>>(A, O, C);
     else
@@ -1280,7 +1291,7 @@ size_t slab_scratch_bytes() { return sizeof(Op) + 64 + kMaxParts * sizeof(double
 
 // Extra slab scratch the Ozaki engine needs for an M x NP slab (0 when the
 // DMMA engine runs it).
-static bool oz_slab_applies(int M, int NP) { return oz_applies(NP) && M % tk::OZ_TM == 0; }
+static bool oz_slab_applies(int M, int NP) { return oz_applies(NP) && M % (2 * tk::OZ_TM) == 0; }
 size_t slab_engine_bytes(int M, int NP) {
   if (!oz_slab_applies(M, NP)) return 0;
   const size_t m = static_cast<size_t>(M), np = static_cast<size_t>(NP);

@@ -127,7 +127,7 @@ def test_workspace_follows_engine(cuda):
     try:
         assert int(L.csm_workspace_size(csm._lib.F64, 4, 256)) > small
         assert int(L.csm_slab_engine_bytes(256, 512)) > 0
-        assert int(L.csm_slab_engine_bytes(64, 512)) == 0  # M % 128 != 0: DMMA
+        assert int(L.csm_slab_engine_bytes(128, 512)) == 0  # M % 256 != 0: DMMA
     finally:
         csm.set_engine("dmma")
     with pytest.raises(ValueError):

@@ -303,6 +303,124 @@ gemm_mod(const int8_t* Ap, const int8_t* Bp, int8_t* Rout, int M, int N, int K) 
 }
 
 
+// Cluster (1, 2, 1) variant: the two CTAs of a cluster take vertically
+// adjacent 128 x 256 tiles, so they need the same B stage; each loads its
+// own A stage and HALF of the B stage, multicast into both CTAs' shared
+// memory (cp.async.bulk ... .multicast::cluster).  A stage is refilled only
+// when both CTAs' MMAs have read it: each MMA commit is multicast to both
+// CTAs' free barriers (count 2).  Producer and MMA issuer are separate
+// warps.
+template <int CM>
+__global__ void __launch_bounds__(THREADS, 1)
+gemm_mod_mc(const int8_t* Ap, const int8_t* Bp, int8_t* Rout, int M, int N, int K) {
+  extern __shared__ __align__(1024) int8_t sm[];
+  __shared__ __align__(8) uint64_t bar_free[NSTAGE];
+  __shared__ __align__(8) uint64_t bar_full[NSTAGE];
+  __shared__ __align__(8) uint64_t bar_done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  const int t = blockIdx.z;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "r"(TN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NSTAGE; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(&bar_free[i])), "r"(CM));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar_full[i])));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar_done)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = tmem_base;
+  const int nk = K / KS;
+  const size_t kb32 = K / 32;
+  const int8_t* abase = Ap + (((size_t)t * (M / TM) + blockIdx.y) * kb32) * 32 * TM;
+  const int8_t* bbase = Bp + (((size_t)t * (N / TN) + blockIdx.x) * kb32) * 32 * TN;
+  constexpr int BH = B_ST / CM;
+  const unsigned short cmask = (unsigned short)((1 << CM) - 1);
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % NSTAGE;
+      if (kb >= NSTAGE) {
+        const uint32_t par = ((kb / NSTAGE) - 1) & 1;
+        asm volatile("{\n.reg .pred p;\nWR:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WR;\n}\n" ::"r"(smem_u32(&bar_free[st])), "r"(par) : "memory");
+      }
+      const uint32_t bar = smem_u32(&bar_full[st]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(STAGE));
+      int8_t* base = sm + st * STAGE;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                   ::"r"(smem_u32(base)), "l"(abase + (size_t)kb * A_ST), "r"(A_ST), "r"(bar) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n"
+                   ::"r"(smem_u32(base + A_ST + rank * BH)), "l"(bbase + (size_t)kb * B_ST + rank * BH), "r"(BH), "r"(bar), "h"(cmask) : "memory");
+    }
+  } else if (warp == 1 && lane == 0) {
+    const uint32_t idesc = idesc_i8(TM, TN);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int st = kb % NSTAGE;
+      const uint32_t par = (kb / NSTAGE) & 1;
+      asm volatile("{\n.reg .pred p;\nWF:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WF;\n}\n" ::"r"(smem_u32(&bar_full[st])), "r"(par) : "memory");
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll
+      for (int j = 0; j < KS / 32; ++j) {
+        const uint64_t da = make_desc(smem_u32(sm + st * STAGE + j * 32 * TM), TM * 16, 128);
+        const uint64_t db = make_desc(smem_u32(sm + st * STAGE + A_ST + j * 32 * TN), TN * 16, 128);
+        const uint32_t acc = (kb > 0 || j > 0) ? 1u : 0u;
+        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                     "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                   ::"r"(smem_u32(&bar_free[st])), "h"(cmask));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&bar_done)));
+  }
+  __syncwarp();
+  asm volatile("{\n.reg .pred p;\nWD:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra WD;\n}\n" ::"r"(smem_u32(&bar_done)) : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const int row = m0 + warp * 32 + lane;
+  const int mod = c_mod[t];
+  const float inv = c_inv[t];
+  int8_t* dst = Rout + ((size_t)t * M + row) * N + n0;
+#pragma unroll 1
+  for (int cb = 0; cb < TN; cb += 32) {
+    uint32_t v[32];
+    const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + cb;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+    uint32_t packed[8];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int x = (int)v[j];
+      int r = x - __float2int_rn(__int2float_rn(x) * inv) * mod;
+      if (r > 127) r -= mod;
+      if (r < -128) r += mod;
+      const uint32_t b = (uint32_t)(r & 0xff);
+      if ((j & 3) == 0) packed[j >> 2] = b;
+      else packed[j >> 2] |= b << (8 * (j & 3));
+    }
+    uint4* d4 = reinterpret_cast<uint4*>(dst + cb);
+    d4[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    d4[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TN));
+}
+
 // 2-CTA variant (cta_group::2): a cluster pair computes a 256 x 256 tile;
 // CTA rank r holds A rows [128 r, +128) and B^T rows [128 r, +128) of the
 // pair's tile (planes with 128-row tiles for both operands) and receives
@@ -542,6 +660,9 @@ int main(int argc, char** argv) {
   const bool slow = getenv("OZ_SLOWCONV") != nullptr;
   const int pair = getenv("OZ_PAIR") ? atoi(getenv("OZ_PAIR")) : 0;
   cudaFuncSetAttribute(gemm_mod2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * P_ST);
+  cudaFuncSetAttribute(gemm_mod_mc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gemm_mod_mc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int mc = getenv("OZ_MC") ? atoi(getenv("OZ_MC")) : 0;
   cudaFuncSetAttribute(gemm_mod2<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * P_ST);
   auto conv = [&]() {
     if (slow) {
@@ -560,7 +681,18 @@ int main(int argc, char** argv) {
     conv_cols<<<dim3((N + 127) / 128, N / 16), 128>>>(B, N, N, sb, NM, Bp, pair ? 128 : TN);
   };
   auto gemm = [&]() {
-    if (pair == 6) gemm_mod2<6><<<dim3(2 * (N / 256), N / 256, NM), THREADS, 6 * P_ST>>>(Ap, Bp, Rr, N, N, N);
+    if (mc) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 1; at[0].val.clusterDim.y = mc; at[0].val.clusterDim.z = 1;
+      cfg.attrs = at; cfg.numAttrs = 1;
+      cfg.gridDim = dim3(N / TN, N / TM, NM); cfg.blockDim = dim3(THREADS); cfg.dynamicSmemBytes = smem;
+      cudaError_t le = mc == 4 ? cudaLaunchKernelEx(&cfg, gemm_mod_mc<4>, (const int8_t*)Ap, (const int8_t*)Bp, Rr, N, N, N)
+                              : cudaLaunchKernelEx(&cfg, gemm_mod_mc<2>, (const int8_t*)Ap, (const int8_t*)Bp, Rr, N, N, N);
+      if (le != cudaSuccess) printf("launch: %s\n", cudaGetErrorString(le));
+    }
+    else if (pair == 6) gemm_mod2<6><<<dim3(2 * (N / 256), N / 256, NM), THREADS, 6 * P_ST>>>(Ap, Bp, Rr, N, N, N);
     else if (pair) gemm_mod2<4><<<dim3(2 * (N / 256), N / 256, NM), THREADS, 4 * P_ST>>>(Ap, Bp, Rr, N, N, N);
     else gemm_mod<<<dim3(N / TN, N / TM, NM), THREADS, smem>>>(Ap, Bp, Rr, N, N, N);
   };
