@@ -236,7 +236,7 @@ __device__ __forceinline__ void oz_wait(uint64_t* bar, uint32_t parity) {
 template <int NST>
 __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, const OzArgs oz,
                                                          const OzConst C) {
-  extern __shared__ __align__(1024) int8_t osm[];
+  extern __shared__ __align__(128) int8_t osm[];
   __shared__ __align__(8) uint64_t bar_free[NST];
   __shared__ __align__(8) uint64_t bar_full[NST];
   __shared__ __align__(8) uint64_t bar_done;
