@@ -546,9 +546,12 @@ INT8_PEAK_TOPS = 4500.0
 
 
 def ozaki_applies(n):
-    """The Ozaki engine runs a call when it is selected and NP % 256 == 0."""
+    """The Ozaki engine runs a call when NP % 256 == 0 and it is selected
+    (or auto and NP >= 4096)."""
     import paper_2010_00465_b200 as csm
-    return csm.get_engine() == "ozaki" and n > 128 and ((n + 63) // 64 * 64) % 256 == 0
+    np_ = (n + 63) // 64 * 64
+    eng = csm.get_engine()
+    return n > 128 and np_ % 256 == 0 and (eng == "ozaki" or (eng == "auto" and np_ >= 4096))
 
 
 def ozaki_roofline(int8_ops_step, gemm_ms, fp64_tflops, dmma_peak):
@@ -585,15 +588,16 @@ def main():
     ap.add_argument("--dist-mode", choices=["gather", "peer"], default="gather",
                     help="cfg5 only: NCCL all-gather per product, or the fused "
                          "peer-memory product (symmetric memory)")
-    ap.add_argument("--engine", choices=["dmma", "ozaki"], default="dmma",
+    ap.add_argument("--engine", choices=["auto", "dmma", "ozaki"], default="auto",
                     help="product engine of the tiled chain (n > 128) and the cfg5 slab "
-                         "products: FP64 DMMA, or Ozaki-II on the int8 tensor cores")
+                         "products: FP64 DMMA, Ozaki-II on the int8 tensor cores, or auto "
+                         "(the library default: Ozaki from padded order 4096 up)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warm-up raised to 3 (timing rule)")
         args.warmup = 3
     cfg = CONFIGS[args.config]
-    if args.impl != "reference" and args.engine != "dmma":
+    if args.impl != "reference":
         import paper_2010_00465_b200 as csm
         csm.set_engine(args.engine)
     if args.impl == "reference":

@@ -242,18 +242,21 @@ int csm_slab_op_peer(const void* op, double* slab, int M, int NP, int row0,
 int csm_graph_safe(int dtype, int64_t batch, int n);
 
 /* Product engine of the tiled chain (n > 128; also the Pade and standalone
- * sine calls), process-wide.  CSM_ENGINE_DMMA (default): FP64 DMMA
+ * sine calls) and of csm_slab_op, process-wide.  CSM_ENGINE_DMMA: FP64 DMMA
  * (mma.sync m8n8k4).  CSM_ENGINE_OZAKI: each product exactly on integers by
  * the Ozaki-II scheme -- rows / columns scaled to P-bit integers, one
- * tcgen05 int8 GEMM per modulus (15 moduli for float64 results, 9 for
- * float32), Chinese-remainder reconstruction fused with the op's epilogue;
- * used when the padded order is a multiple of 256, DMMA otherwise.  The
- * chain, (k, s) and the reference interface are unchanged (the products of
- * matcore.py:90-97 are computed differently).  csm_workspace_size depends on
- * the engine: size workspaces after setting it.  Returns CSM_ERR_ARG for an
- * unknown engine. */
+ * tcgen05 int8 GEMM per modulus (16 moduli for float64 results, 9 for
+ * float32), Chinese-remainder reconstruction fused with the op's epilogue --
+ * whenever the padded order is a multiple of 256 (DMMA otherwise).
+ * CSM_ENGINE_AUTO (default): Ozaki for padded orders >= 4096 that are
+ * multiples of 256, where it is faster; DMMA below.  The chain, (k, s) and
+ * the reference interface are unchanged (the products of matcore.py:90-97
+ * are computed differently).  csm_workspace_size depends on the engine:
+ * size workspaces after setting it.  Returns CSM_ERR_ARG for an unknown
+ * engine. */
 #define CSM_ENGINE_DMMA 0
 #define CSM_ENGINE_OZAKI 1
+#define CSM_ENGINE_AUTO 2
 int csm_set_engine(int engine);
 int csm_get_engine(void);
 

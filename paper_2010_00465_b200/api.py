@@ -561,14 +561,16 @@ def write_matrix(path: str, a) -> None:
             fh.write(" ".join(repr(float(v)) for v in row) + "\n")
 
 
-_ENGINES = {"dmma": 0, "ozaki": 1}
+_ENGINES = {"dmma": 0, "ozaki": 1, "auto": 2}
 
 
 def set_engine(name: str) -> None:
-    """Select the product engine of the tiled chain (n > 128), process-wide
-    (csm_set_engine): "dmma" (FP64 DMMA, default) or "ozaki" (Ozaki-II:
-    exact int8 tensor-core GEMMs per modulus + CRT, for padded orders that
-    are multiples of 256).  Size workspaces (BatchPlan) after changing it."""
+    """Select the product engine of the tiled chain (n > 128) and the
+    block-row chain, process-wide (csm_set_engine): "dmma" (FP64 DMMA),
+    "ozaki" (Ozaki-II: exact int8 tensor-core GEMMs per modulus + CRT, for
+    padded orders that are multiples of 256) or "auto" (default: Ozaki from
+    padded order 4096 up, DMMA below).  Size workspaces (BatchPlan) after
+    changing it."""
     if name not in _ENGINES:
         raise ValueError(f"engine must be one of {sorted(_ENGINES)}")
     _lib.check(_lib.lib().csm_set_engine(_ENGINES[name]), "csm_set_engine")

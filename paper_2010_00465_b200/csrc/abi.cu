@@ -783,8 +783,8 @@ int csm_profile_collect(double* total_ms, int64_t* intervals) {
 }
 
 int csm_set_engine(int engine) {
-  if (engine != CSM_ENGINE_DMMA && engine != CSM_ENGINE_OZAKI)
-    return fail(CSM_ERR_ARG, "engine must be CSM_ENGINE_DMMA or CSM_ENGINE_OZAKI");
+  if (engine != CSM_ENGINE_DMMA && engine != CSM_ENGINE_OZAKI && engine != CSM_ENGINE_AUTO)
+    return fail(CSM_ERR_ARG, "engine must be CSM_ENGINE_DMMA, CSM_ENGINE_OZAKI or CSM_ENGINE_AUTO");
   csm::set_engine(engine);
   return CSM_SUCCESS;
 }

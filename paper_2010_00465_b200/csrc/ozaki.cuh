@@ -391,18 +391,25 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
   const int NP = la.NP, M = la.M;
   const int tiles_n = NP / BN;
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x - tm * tiles_n;
-  // 64 rows x 64 columns: thread -> row tid / 2, columns 32 (tid & 1) .. +32
-  const int rr = tid >> 1, cbase = (tid & 1) * 32;
-  const int row = tm * BM + rr;
+  // 64 x 64 tile: thread -> columns 4 (tid & 15) .. +4 of rows (tid >> 4) + 8 g,
+  // g = 0..7, so a warp's residue loads are two contiguous 64-byte row runs
+  const int c4 = (tid & 15) * 4, rbase = tid >> 4;
   const size_t plane = static_cast<size_t>(M) * NP;
   const int8_t* res = oz.res + static_cast<size_t>(ci) * NM * plane +
-                      static_cast<size_t>(row) * NP + tn * BN + cbase;
-  const int sa = oz_shift(oz.mxL[static_cast<size_t>(ci) * M + row], C.P);
-  const unsigned long long* mxr = oz.mxR + static_cast<size_t>(ci) * NP + tn * BN + cbase;
+                      static_cast<size_t>(tm * BM) * NP + tn * BN + c4;
+  int sb[4];
+  {
+    const unsigned long long* mxr = oz.mxR + static_cast<size_t>(ci) * NP + tn * BN + c4;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sb[e] = oz_shift(mxr[e], C.P);
+  }
+  const unsigned long long* mxl = oz.mxL + static_cast<size_t>(ci) * M + tm * BM;
   double* E = sm;
   const double d1s = ldexp(1.0, OZ_LVB), d2s = ldexp(1.0, 2 * OZ_LVB), d3s = ldexp(1.0, 3 * OZ_LVB);
 #pragma unroll 1
-  for (int g = 0; g < 8; ++g) {  // 4 columns at a time: 4 x 4 exact level sums
+  for (int g = 0; g < 8; ++g) {
+    const int rr = rbase + 8 * g;
+    const int sa = oz_shift(mxl[rr], C.P);
     double s[4][OZ_LV];
 #pragma unroll
     for (int e = 0; e < 4; ++e)
@@ -410,7 +417,8 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
       for (int l = 0; l < OZ_LV; ++l) s[e][l] = 0.0;
     uint32_t w4[NM];
 #pragma unroll
-    for (int t = 0; t < NM; ++t) w4[t] = *reinterpret_cast<const uint32_t*>(res + t * plane + g * 4);
+    for (int t = 0; t < NM; ++t)
+      w4[t] = *reinterpret_cast<const uint32_t*>(res + t * plane + static_cast<size_t>(rr) * NP);
 #pragma unroll
     for (int t = 0; t < NM; ++t) {
 #pragma unroll
@@ -432,8 +440,7 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
       const double e2 = fma(-q, C.M[2], s[e][2]);
       const double e3 = fma(-q, C.M[3], s[e][3]);
       const double v = fma(e0, d3s, fma(e1, d2s, fma(e2, d1s, e3)));
-      const int sb = oz_shift(mxr[g * 4 + e], C.P);
-      E[rr * LDE + cbase + g * 4 + e] = ldexp(v, -(sa + sb));
+      E[rr * LDE + c4 + e] = ldexp(v, -(sa + sb[e]));
     }
   }
   __syncthreads();

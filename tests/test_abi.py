@@ -83,8 +83,10 @@ def test_engine_switch_without_device():
     Ozaki engine enlarges the tiled workspace (n = 256) but not n = 64 or
     the DMMA-only orders (NP % 256 != 0)."""
     lib = _lib.lib()
-    assert lib.csm_get_engine() == 0
+    assert lib.csm_get_engine() == 2  # auto: Ozaki from padded order 4096 up
+    assert lib.csm_workspace_size(0, 1, 4096) > 9 * 4096 * 4096 * 8 + 16 * 3 * 4096 * 4096
     assert lib.csm_set_engine(5) == _lib.ERR_ARG
+    assert lib.csm_set_engine(0) == 0
     assert "engine" in _lib.last_error()
     dm256, dm320, dm64 = (lib.csm_workspace_size(0, 8, n) for n in (256, 320, 64))
     assert lib.csm_slab_engine_bytes(512, 1024) == 0
@@ -97,4 +99,4 @@ def test_engine_switch_without_device():
         # residue planes of L (M x NP), R (NP x NP) and the product, 16 moduli
         assert lib.csm_slab_engine_bytes(512, 1024) >= 16 * (2 * 512 * 1024 + 1024 * 1024)
     finally:
-        assert lib.csm_set_engine(0) == 0
+        assert lib.csm_set_engine(2) == 0

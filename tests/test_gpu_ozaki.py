@@ -20,7 +20,7 @@ TOL32 = 1e-5
 def ozaki(cuda):
     csm.set_engine("ozaki")
     yield
-    csm.set_engine("dmma")
+    csm.set_engine("auto")
 
 
 @pytest.mark.parametrize("n", [256, 512])
@@ -129,6 +129,6 @@ def test_workspace_follows_engine(cuda):
         assert int(L.csm_slab_engine_bytes(256, 512)) > 0
         assert int(L.csm_slab_engine_bytes(128, 512)) == 0  # M % 256 != 0: DMMA
     finally:
-        csm.set_engine("dmma")
+        csm.set_engine("auto")
     with pytest.raises(ValueError):
         csm.set_engine("tf32")
