@@ -132,3 +132,79 @@ def test_workspace_follows_engine(cuda):
         csm.set_engine("auto")
     with pytest.raises(ValueError):
         csm.set_engine("tf32")
+
+
+def test_bad_statuses_and_extreme_norms(ozaki):
+    """Non-finite inputs / norms and norm/theta overflow keep their status and
+    NaN outputs under the Ozaki engine; tiny (1e-150) and large (1e4, s = 13)
+    norms -- power-of-two shifts far from 0 -- agree with the DMMA engine."""
+    n, count = 256, 8
+    rng = np.random.default_rng(815)
+    a = cfg2_like(rng, count, n=n, lo=-2, hi=1.0)
+    a[0] *= 1e-150 / orc.norm1(a[0])
+    a[1] *= 1e4 / orc.norm1(a[1])
+    bad = {2: 1, 3: 2, 4: 3}
+    a[2, 3, 5] = np.nan
+    a[3, :, 0] = 1e308
+    a[4] = 0.0
+    a[4, 0, 0] = 1.7e308
+    rep = csm.cos_sin_batched(a, raise_on_error=False)
+    st = np.asarray(rep.status)
+    for i, code in bad.items():
+        assert st[i] == code
+        assert np.all(np.isnan(rep.cos_part[i])) and np.all(np.isnan(rep.sin_part[i]))
+    csm.set_engine("dmma")
+    dm = csm.cos_sin_batched(a, raise_on_error=False)
+    csm.set_engine("ozaki")
+    for i in (0, 1, 5, 6, 7):
+        assert st[i] == 0
+        assert (int(rep.k[i]), int(rep.s[i])) == (int(dm.k[i]), int(dm.s[i]))
+    for i in (0, 5, 6, 7):
+        c, s, k, sc = orc.cos_sin(a[i])
+        assert pair_close(rep.cos_part[i], c, s, TOL64)[0], i
+        assert pair_close(rep.sin_part[i], s, c, TOL64)[0], i
+    # norm 1e4, s = 13: the reference itself is ~1e-11 from the truth there
+    # (SURVEY 8a's noise-floor rule), so gate against the double-double
+    # reference values: the Ozaki result is as close to them as the oracle
+    assert int(rep.s[1]) >= 10
+    from paper_2010_00465_b200 import verify
+    tc, ts, _ = verify.reference_cos_sin_batched(a[1:2])
+    c, s, _, _ = orc.cos_sin(a[1])
+    for got, ref, tr in ((rep.cos_part[1], c, tc[0]), (rep.sin_part[1], s, ts[0])):
+        floor = rel1(ref, tr)
+        assert rel1(got, tr) <= 2.0 * floor + 1e-14
+        assert rel1(got, ref) <= max(TOL64, 2.0 * floor)
+
+
+def test_pade_and_standalone_sines(ozaki):
+    """pade_cos_sin (its five products), taylor_sin9 and wave_sin34 run on
+    the tiled chain, so on the Ozaki engine too."""
+    rng = np.random.default_rng(816)
+    a = cfg2_like(rng, 3, n=256, lo=-2, hi=0.5)
+    rep = csm.pade_cos_sin_batched(a)
+    for i in range(a.shape[0]):
+        c, s, sc = orc.pade_cos_sin(a[i])
+        assert int(rep.s[i]) == sc
+        tol = max(TOL64, 64 * 2.0 ** -53 * 4.0 ** sc)  # test_gpu_parity._pade_tol
+        assert pair_close(rep.cos_part[i], c, s, tol)[0], i
+        assert pair_close(rep.sin_part[i], s, c, tol)[0], i
+    b = a[0] * (0.5 / orc.norm1(a[0]))
+    assert rel1(csm.taylor_sin9(b, csm.CostLedger()), orc.taylor_sin9(b)) <= TOL64
+    assert rel1(csm.wave_sin34(b, 0.3, csm.CostLedger()), orc.wave_sin34(b, 0.3)) <= TOL64
+
+
+def test_auto_engine_picks_by_size(cuda):
+    """auto (the default): DMMA below padded order 4096 -- bit-identical to
+    the forced DMMA engine."""
+    csm.set_engine("auto")
+    assert csm.get_engine() == "auto"
+    rng = np.random.default_rng(817)
+    a = cfg2_like(rng, 2, n=512)
+    au = csm.cos_sin_batched(a)
+    csm.set_engine("dmma")
+    try:
+        dm = csm.cos_sin_batched(a)
+    finally:
+        csm.set_engine("auto")
+    assert np.array_equal(au.cos_part, dm.cos_part)
+    assert np.array_equal(au.sin_part, dm.sin_part)
