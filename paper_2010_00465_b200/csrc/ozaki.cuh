@@ -11,20 +11,20 @@
 //   * each modulus is ONE int8 GEMM on the 5th-generation tensor cores
 //     (oz_gemm: tcgen05.mma.kind::i8, int32 accumulators in TMEM, exact
 //     because |sum| <= K 2^14 < 2^31), reduced mod m_t to an int8 residue;
-//   * oz_crt_epi rebuilds L'R' = sum_t r_t W_t mod M (M = prod m_t) in four
-//     exact 32-bit fp64 levels, undoes the scaling, and runs the op's
+//   * oz_crt_epi rebuilds L'R' = sum_t r_t W_t mod M (M = prod m_t) in three
+//     42-bit fp64 levels, undoes the scaling, and runs the op's
 //     epilogue (the same epilogue_tile as the DMMA kernel).
 // P is the largest value with K 2^(2P) <= M / 4, so the integer product is
 // exact and the only error is the rounding of L and R to P bits relative to
 // their row / column maxima: P = 55..57 for nm = 16 (fp64 results), 30 for
 // nm = 9 (float32 results).  Tensor work per product: nm int8 GEMMs.
-// Residues: v mod G for groups of moduli with G < 2^24 (fp64, 3 ops), then
-// each modulus in fp32.
+// Residues: v mod G for groups of moduli with G < 2^24 (fp64 FMA pipe),
+// then each modulus by integer multiply-high (no conversion instructions).
 //
 // Reference: the products are matcore.py:90-97 (`a @ b`, ledger +1); the
 // engine changes how each product is computed, not the chain.
 
-constexpr int OZ_MAXM = 16, OZ_LV = 4, OZ_LVB = 32;
+constexpr int OZ_MAXM = 16, OZ_LV = 3, OZ_LVB = 42;
 constexpr int OZ_MAXG = 6;  // moduli groups with products below 2^24
 constexpr int OZ_TM = 128, OZ_TN = 256, OZ_KS = 128, OZ_NSTAGE = 4;
 constexpr int OZ_A_ST = OZ_TM * OZ_KS, OZ_B_ST = OZ_TN * OZ_KS, OZ_STAGE = OZ_A_ST + OZ_B_ST;
@@ -38,9 +38,11 @@ struct OzConst {
   int nm, P, ng;
   int mod[OZ_MAXM];
   float inv[OZ_MAXM];
+  uint32_t cdiv[OZ_MAXM];    // floor(2^32 / m_t): x / m_t by multiply-high
   int gend[OZ_MAXG];         // group g = moduli [gend[g-1], gend[g])
   double gmod[OZ_MAXG];      // product of the group's moduli (< 2^24)
-  double w[OZ_MAXM][OZ_LV];  // W_t = (M/m_t) ((M/m_t)^-1 mod m_t) in 32-bit digits, high first
+  double ginv[OZ_MAXG];      // 1 / gmod
+  double w[OZ_MAXM][OZ_LV];  // W_t = (M/m_t) ((M/m_t)^-1 mod m_t) in 42-bit digits, high first
   double M[OZ_LV];
   double invM;
 };
@@ -84,22 +86,24 @@ __device__ __forceinline__ size_t oz_off(int r, int k, int K, int TR) {
   return ((static_cast<size_t>(r / TR) * (K / 32) + k / 32) * 2 + (k % 32) / 16) * TR * 16 +
          (r % TR) * 16 + k % 16;
 }
-// v: an integer-valued double, |v| <= 2^57.  v mod G (G < 2^24, a group's
-// product of moduli) in three fp64 operations: the quotient estimate is
-// within 1/16 of v / G, the fma is exact.  Then each modulus of the group
-// from that 24-bit value in fp32 (exact below 2^24): a representative in
-// [-128, 127].
-__device__ __forceinline__ float oz_mod_group(double v, double G) {
-  const double q = rint(v * (1.0 / G));
-  return static_cast<float>(fma(-q, G, v));
+// v: an integer-valued double, |v| <= 2^57.  x = (v mod G) + G in [0, 2G)
+// for a group's product of moduli G < 2^24, without the conversion pipe:
+// the quotient is rounded by the 1.5 2^52 trick (|v / G| < 2^51), the fma
+// remainder is exact, and the same trick hands its integer bits over.
+// Then each modulus of the group: floor(x / m) by multiply-high with
+// floor(2^32 / m) (x < 2^25: at most one short), one correction, and a
+// representative in [-128, 127].  Integer / FMA pipes only.
+__device__ __forceinline__ uint32_t oz_mod_group(double v, double G, double invG) {
+  const double M52 = 6755399441055744.0;  // 1.5 * 2^52
+  const double q = fma(v, invG, M52) - M52;
+  const double r = fma(-q, G, v);  // |r| < G
+  return static_cast<uint32_t>(__double2loint(r + M52)) + static_cast<uint32_t>(G);
 }
-__device__ __forceinline__ int oz_mod_small(float x, const OzConst& C, int t) {
-  const float m = static_cast<float>(C.mod[t]);
-  const float q = rintf(x * C.inv[t]);
-  int r = static_cast<int>(fmaf(-q, m, x));
-  if (r > 127) r -= C.mod[t];
-  if (r < -128) r += C.mod[t];
-  return r;
+__device__ __forceinline__ int oz_mod_small(uint32_t x, const OzConst& C, int t) {
+  const uint32_t m = static_cast<uint32_t>(C.mod[t]);
+  uint32_t r = x - __umulhi(x, C.cdiv[t]) * m;  // in [0, 2m)
+  if (r >= m) r -= m;
+  return r > 127u ? static_cast<int>(r) - static_cast<int>(m) : static_cast<int>(r);
 }
 
 // grid (M / 8, nitems), 256 threads: one warp per row of L
@@ -148,9 +152,9 @@ __device__ __forceinline__ void oz_store_residues(const double (&v)[16], const O
                                                   int8_t* out, size_t plane) {
 #pragma unroll
   for (int g = 0; g < (NM + 2) / 3; ++g) {
-    float x[16];
+    uint32_t x[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) x[i] = oz_mod_group(v[i], C.gmod[g]);
+    for (int i = 0; i < 16; ++i) x[i] = oz_mod_group(v[i], C.gmod[g], C.ginv[g]);
 #pragma unroll
     for (int t = 3 * g; t < 3 * g + 3 && t < NM; ++t) {
       int b[16];
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
   }
   const unsigned long long* mxl = oz.mxL + static_cast<size_t>(ci) * M + tm * BM;
   double* E = sm;
-  const double d1s = ldexp(1.0, OZ_LVB), d2s = ldexp(1.0, 2 * OZ_LVB), d3s = ldexp(1.0, 3 * OZ_LVB);
+  const double d1s = ldexp(1.0, OZ_LVB), d2s = ldexp(1.0, 2 * OZ_LVB);
 #pragma unroll 1
   for (int g = 0; g < 8; ++g) {
     const int rr = rbase + 8 * g;
@@ -430,16 +434,16 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      // S = sum_l s_l 2^(32 (3 - l)) exactly (each |s_l| < 2^43); q =
-      // round(S / M); each level s_l - q M_l is exact, so only the final
-      // sum rounds
-      const double approx = fma(s[e][0], d3s, fma(s[e][1], d2s, fma(s[e][2], d1s, s[e][3])));
+      // S = s0 2^84 + s1 2^42 + s2 exactly (16 terms below 2^7 2^42: each
+      // |s_l| < 2^53); q = round(S / M); s0 - q M0 is exact (|result| <
+      // 2^40), the two lower levels may round by an ulp (<= 2^44 absolute,
+      // far below the P-bit truncation); only those and the final sum round
+      const double approx = fma(s[e][0], d2s, fma(s[e][1], d1s, s[e][2]));
       const double q = rint(approx * C.invM);
       const double e0 = fma(-q, C.M[0], s[e][0]);
       const double e1 = fma(-q, C.M[1], s[e][1]);
       const double e2 = fma(-q, C.M[2], s[e][2]);
-      const double e3 = fma(-q, C.M[3], s[e][3]);
-      const double v = fma(e0, d3s, fma(e1, d2s, fma(e2, d1s, e3)));
+      const double v = fma(e0, d2s, fma(e1, d1s, e2));
       E[rr * LDE + c4 + e] = ldexp(v, -(sa + sb[e]));
     }
   }

@@ -875,6 +875,7 @@ tk::OzConst oz_const(int nm, int K) {
     const int m = kOzMods[t];
     C.mod[t] = m;
     C.inv[t] = 1.0f / static_cast<float>(m);
+    C.cdiv[t] = static_cast<uint32_t>((static_cast<uint64_t>(1) << 32) / static_cast<uint64_t>(m));
     const u128 Mt = M / static_cast<u128>(m);
     const int a = static_cast<int>(Mt % static_cast<u128>(m));
     int inv = 0;
@@ -891,12 +892,14 @@ tk::OzConst oz_const(int nm, int K) {
   for (int t = 0; t < nm; ++t) {
     if (G * kOzMods[t] >= 16777216.0) {
       C.gmod[C.ng] = G;
+      C.ginv[C.ng] = 1.0 / G;
       C.gend[C.ng++] = t;
       G = 1.0;
     }
     G *= kOzMods[t];
   }
   C.gmod[C.ng] = G;
+  C.ginv[C.ng] = 1.0 / G;
   C.gend[C.ng++] = nm;
   for (int l = 0; l < tk::OZ_LV; ++l)
     C.M[l] = static_cast<double>(
@@ -993,9 +996,9 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
       const char* e = std::getenv("CSM_OZ_STAGES");
       return e ? std::atoi(e) : 0;
     }();
-    // NP <= 512 (K <= 4 stages anyway): two 2-stage CTAs per SM, one's
-    // epilogue overlapping the other's MMAs; larger: one 4-stage CTA per SM
-    const bool small = force_st ? force_st == 2 : NP <= 512;
+    // NP <= 1024: two 2-stage CTAs per SM, one's epilogue overlapping the
+    // other's MMAs (n = 1024: -25% GEMM time); larger: one 4-stage CTA per SM
+    const bool small = force_st ? force_st == 2 : NP <= 1024;
     const size_t gsm = (small ? tk::OZ_NSTAGE_SMALL : tk::OZ_NSTAGE) * tk::OZ_STAGE;
     if (C.nm == 16) {
       tk::oz_conv_rows<16><<<gconv_r, 128, 0, stream>>>(A, O, C);
