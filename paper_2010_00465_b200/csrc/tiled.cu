@@ -842,15 +842,15 @@ size_t tiled_np(int n) { return static_cast<size_t>((n + 63) / 64) * 64; }
 
 // Product engine (process-wide, csm_set_engine): 0 = FP64 DMMA, 1 = Ozaki-II
 // on the int8 tensor cores (ozaki.cuh) for the tiled chain when NP % 256 == 0.
-// 2 = auto (default): Ozaki from NP = 4096 up, where its O(n^2 nm) passes
-// are small next to the GEMM (cfg5, 8192^2: 2.98x the DMMA chain; batched
-// n <= 1024 is faster on DMMA, K7).
+// 2 = auto (default): Ozaki from NP = 2048 up, where its O(n^2 nm) passes
+// are small next to the GEMM (batched n = 2048: 1.61x the DMMA chain; cfg5,
+// 8192^2: 3.2x; n = 1024 is level, smaller n faster on DMMA, K7).
 static int g_engine = 2;
 void set_engine(int e) { g_engine = e; }
 int engine() { return g_engine; }
 static bool oz_applies(int NP) {
   if (NP % tk::OZ_TN != 0) return false;
-  return g_engine == 1 || (g_engine == 2 && NP >= 4096);
+  return g_engine == 1 || (g_engine == 2 && NP >= 2048);
 }
 // moduli: pairwise coprime, <= 256, largest first
 static const int kOzMods[tk::OZ_MAXM] = {256, 255, 253, 251, 247, 241, 239, 233,
