@@ -371,6 +371,190 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, co
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(OZ_TN));
 }
 
+// Persistent form of oz_gemm: one cluster pair per two SMs walks the pair
+// tiles (x, y pair, item x modulus) round-robin, with warp roles --
+// warp 0: producer (the stage ring runs on across tiles), warp 1: MMA
+// issuer, warps 2..5: epilogue -- and two 256-column TMEM accumulators, so
+// a tile's TMEM drain / residue epilogue overlaps the next tile's MMAs and
+// the set-up is paid once per CTA.  grid = 2 x clusters, 192 threads,
+// NST x 48 KiB dynamic shared memory.
+constexpr int OZ_PTHREADS = 192;
+template <int NST>
+__global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la, const OzArgs oz,
+                                                            const OzConst C, int pair_tiles) {
+  extern __shared__ __align__(128) int8_t osm[];
+  __shared__ __align__(8) uint64_t bar_free[NST];
+  __shared__ __align__(8) uint64_t bar_full[NST];
+  __shared__ __align__(8) uint64_t tm_full[2];
+  __shared__ __align__(8) uint64_t tm_empty[2];
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NP = la.NP, M = la.M;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int nx = NP / OZ_TN, nyp = M / (2 * OZ_TM);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     oz_smem(&tmem_base)),
+                 "r"(2 * OZ_TN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;\n" ::"r"(oz_smem(&bar_free[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(oz_smem(&bar_full[i])));
+    }
+    for (int i = 0; i < 2; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(oz_smem(&tm_full[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;\n" ::"r"(oz_smem(&tm_empty[i])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = tmem_base;
+  const int nk = NP / OZ_KS;
+  const size_t kb32 = NP / 32;
+  const size_t lplane = static_cast<size_t>(M) * NP, rplane = static_cast<size_t>(NP) * NP;
+  // pair tile T -> x fastest, then y pair, then item x modulus
+  auto decode = [&](int T, int& x, int& y, int& z) {
+    x = T % nx;
+    const int r = T / nx;
+    y = 2 * (r % nyp) + static_cast<int>(rank);
+    z = r / nyp;
+  };
+  constexpr int BH = OZ_B_ST / 2;
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0;  // k-block counter across tiles (the stage ring)
+      for (int T = cluster; T < pair_tiles; T += nclusters) {
+        int x, y, z;
+        decode(T, x, y, z);
+        const int ci = z / C.nm, t = z - ci * C.nm;
+        const int8_t* abase = oz.pL + (static_cast<size_t>(ci) * C.nm + t) * lplane +
+                              static_cast<size_t>(y) * kb32 * 32 * OZ_TM;
+        const int8_t* bbase = oz.pR + (static_cast<size_t>(ci) * C.nm + t) * rplane +
+                              static_cast<size_t>(x) * kb32 * 32 * OZ_TN;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int st = g % NST;
+          if (g >= NST) oz_wait(&bar_free[st], ((g / NST) - 1) & 1);
+          const uint32_t bar = oz_smem(&bar_full[st]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                       "r"(OZ_STAGE));
+          int8_t* base = osm + st * OZ_STAGE;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                  oz_smem(base)),
+              "l"(abase + static_cast<size_t>(kb) * OZ_A_ST), "r"(OZ_A_ST), "r"(bar)
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+              "[%0], [%1], %2, [%3], %4;\n" ::"r"(oz_smem(base + OZ_A_ST + rank * BH)),
+              "l"(bbase + static_cast<size_t>(kb) * OZ_B_ST + rank * BH), "r"(BH), "r"(bar),
+              "h"(static_cast<unsigned short>(3))
+              : "memory");
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = oz_idesc(OZ_TM, OZ_TN);
+      int g = 0, i = 0;
+      for (int T = cluster; T < pair_tiles; T += nclusters, ++i) {
+        const int acc_i = i & 1;
+        if (i >= 2) oz_wait(&tm_empty[acc_i], ((i >> 1) - 1) & 1);  // epilogue drained it
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const uint32_t dacc = tmem + acc_i * OZ_TN;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int st = g % NST;
+          oz_wait(&bar_full[st], (g / NST) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll
+          for (int j = 0; j < OZ_KS / 32; ++j) {
+            const uint64_t da =
+                oz_desc(oz_smem(osm + st * OZ_STAGE + j * 32 * OZ_TM), OZ_TM * 16, 128);
+            const uint64_t db =
+                oz_desc(oz_smem(osm + st * OZ_STAGE + OZ_A_ST + j * 32 * OZ_TN), OZ_TN * 16, 128);
+            const uint32_t acc = (kb > 0 || j > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(dacc),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+              "[%0], %1;\n" ::"r"(oz_smem(&bar_free[st])),
+              "h"(static_cast<unsigned short>(3)));
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                oz_smem(&tm_full[acc_i])));
+      }
+    }
+  } else {  // epilogue warps 2..5: TMEM lane quarter (warp % 4)
+    const int q = warp & 3;
+    int i = 0;
+    for (int T = cluster; T < pair_tiles; T += nclusters, ++i) {
+      int x, y, z;
+      decode(T, x, y, z);
+      const int ci = z / C.nm, t = z - ci * C.nm;
+      const int acc_i = i & 1;
+      oz_wait(&tm_full[acc_i], (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      const int row = y * OZ_TM + q * 32 + lane;
+      const int mod = C.mod[t];
+      const float inv = C.inv[t];
+      int8_t* dst = oz.res + (static_cast<size_t>(ci) * C.nm + t) * lplane +
+                    static_cast<size_t>(row) * NP + x * OZ_TN;
+#pragma unroll 1
+      for (int cb = 0; cb < OZ_TN; cb += 32) {
+        uint32_t v[32];
+        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc_i * OZ_TN + cb;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+              "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+              "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(ta));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+        uint32_t packed[8];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int xx = static_cast<int>(v[j]);
+          int r = xx - __float2int_rn(__int2float_rn(xx) * inv) * mod;
+          if (r > 127) r -= mod;
+          if (r < -128) r += mod;
+          const uint32_t bb = static_cast<uint32_t>(r) & 0xffu;
+          packed[j >> 2] = (j & 3) == 0 ? bb : (packed[j >> 2] | (bb << (8 * (j & 3))));
+        }
+        uint4* d4 = reinterpret_cast<uint4*>(dst + cb);
+        d4[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        d4[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(oz_smem(&tm_empty[acc_i]))
+                     : "memory");
+    }
+  }
+  __syncwarp();
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  // no CTA leaves while its cluster peer may still multicast into it or
+  // arrive on its barriers
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(2 * OZ_TN));
+}
+
 // Product tile (CRT + unscaling) into shared memory, then the op's epilogue.
 // grid (tiles of 64 x 64, nitems), 128 threads, tk::SMEM dynamic.
 template <int NM>

@@ -422,6 +422,9 @@ inline cudaError_t ensure_smem_attr() {
     e = cudaFuncSetAttribute(oz_gemm<OZ_NSTAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(OZ_SMEM));
   if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(oz_gemm_p<OZ_NSTAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(OZ_SMEM));
+  if (e == cudaSuccess)
     e = cudaFuncSetAttribute(oz_gemm<OZ_NSTAGE_SMALL>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(OZ_NSTAGE_SMALL * OZ_STAGE));
@@ -842,15 +845,16 @@ size_t tiled_np(int n) { return static_cast<size_t>((n + 63) / 64) * 64; }
 
 // Product engine (process-wide, csm_set_engine): 0 = FP64 DMMA, 1 = Ozaki-II
 // on the int8 tensor cores (ozaki.cuh) for the tiled chain when NP % 256 == 0.
-// 2 = auto (default): Ozaki from NP = 2048 up, where its O(n^2 nm) passes
-// are small next to the GEMM (batched n = 2048: 1.61x the DMMA chain; cfg5,
-// 8192^2: 3.2x; n = 1024 is level, smaller n faster on DMMA, K7).
+// 2 = auto (default): Ozaki from NP = 1024 up, where its O(n^2 nm) passes
+// are small enough next to the GEMM (batched n = 1024: 1.08x the DMMA chain,
+// n = 2048: 1.78x, cfg5 8192^2: 3.5x; smaller n is faster on DMMA,
+// DESIGN.md K7).
 static int g_engine = 2;
 void set_engine(int e) { g_engine = e; }
 int engine() { return g_engine; }
 static bool oz_applies(int NP) {
   if (NP % tk::OZ_TN != 0) return false;
-  return g_engine == 1 || (g_engine == 2 && NP >= 2048);
+  return g_engine == 1 || (g_engine == 2 && NP >= 1024);
 }
 // moduli: pairwise coprime, <= 256, largest first
 static const int kOzMods[tk::OZ_MAXM] = {256, 255, 253, 251, 247, 241, 239, 233,
@@ -974,6 +978,41 @@ static TiledWs carve(void* ws, int64_t batch, int n) {
   return w;
 }
 
+static bool persistent_layout() {
+  static const bool p = [] {
+    const char* e = std::getenv("CSM_OZ_GEMM");
+    return !(e && std::strcmp(e, "tile") == 0);
+  }();
+  return p;
+}
+
+// Co-resident 2-CTA clusters of the persistent int8 GEMM (one CTA per SM
+// by its shared memory), once per device.
+static int oz_resident_clusters() {
+  static int cached[32] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev = dev < 32 ? dev : 31;
+  if (cached[dev] > 0) return cached[dev];
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(tk::OZ_PTHREADS);
+  cfg.dynamicSmemBytes = tk::OZ_SMEM;
+  cfg.gridDim = dim3(2 * 64);
+  int active = 0;
+  if (cudaOccupancyMaxActiveClusters(&active, tk::oz_gemm_p<tk::OZ_NSTAGE>, &cfg) != cudaSuccess ||
+      active <= 0)
+    active = 64;
+  cached[dev] = active;
+  return active;
+}
+
 // One tiled launch (all items of plan A) through the Ozaki engine, in
 // chunks of at most cap items: maxima, residues, nm int8 GEMMs, CRT +
 // epilogue.  Seven launches per chunk.
@@ -1010,8 +1049,8 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;  // pairs of M tiles share B
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = 2;
+    attr[0].val.clusterDim.x = persistent_layout() ? 2 : 1;
+    attr[0].val.clusterDim.y = persistent_layout() ? 1 : 2;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
@@ -1019,9 +1058,23 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
     cfg.blockDim = dim3(tk::OZ_THREADS);
     cfg.dynamicSmemBytes = gsm;
     cfg.stream = stream;
+    static const bool persistent = [] {  // CSM_OZ_GEMM=tile: one CTA per tile
+      const char* e = std::getenv("CSM_OZ_GEMM");
+      return !(e && std::strcmp(e, "tile") == 0);
+    }();
     prof_begin(stream, 2);  // csm_profile_enable(2): the int8 GEMM alone
-    e = small ? cudaLaunchKernelEx(&cfg, tk::oz_gemm<tk::OZ_NSTAGE_SMALL>, A, O, C)
-              : cudaLaunchKernelEx(&cfg, tk::oz_gemm<tk::OZ_NSTAGE>, A, O, C);
+    if (persistent) {
+      const int pair_tiles = (NP / tk::OZ_TN) * (M / (2 * tk::OZ_TM)) * cnt * C.nm;
+      int clusters = oz_resident_clusters();
+      if (clusters > pair_tiles) clusters = pair_tiles;
+      cfg.gridDim = dim3(2 * clusters);
+      cfg.blockDim = dim3(tk::OZ_PTHREADS);
+      cfg.dynamicSmemBytes = tk::OZ_SMEM;
+      e = cudaLaunchKernelEx(&cfg, tk::oz_gemm_p<tk::OZ_NSTAGE>, A, O, C, pair_tiles);
+    } else {
+      e = small ? cudaLaunchKernelEx(&cfg, tk::oz_gemm<tk::OZ_NSTAGE_SMALL>, A, O, C)
+                : cudaLaunchKernelEx(&cfg, tk::oz_gemm<tk::OZ_NSTAGE>, A, O, C);
+    }
     prof_end(stream, 2);
     if (e != cudaSuccess) return e;
     if (C.nm == 16)
