@@ -8,9 +8,10 @@
 //     the per-row / per-column max, oz_conv_* the scaled integers' residues
 //     modulo nm pairwise coprime moduli m_t <= 256, as int8 planes in the
 //     canonical K-major UMMA layout, tile-major);
-//   * each modulus is ONE int8 GEMM on the 5th-generation tensor cores
-//     (oz_gemm: tcgen05.mma.kind::i8, int32 accumulators in TMEM, exact
-//     because |sum| <= K 2^14 < 2^31), reduced mod m_t to an int8 residue;
+//   * each modulus is ONE 8-bit GEMM on the 5th-generation tensor cores
+//     (oz_gemm_p: tcgen05.mma.kind::i8 on unsigned residues in [0, m_t),
+//     int32 accumulators in TMEM, exact because sum <= K 255^2 < 2^31 for
+//     K <= 33025), reduced mod m_t to an int8 residue in [-128, 127];
 //   * oz_crt_epi rebuilds L'R' = sum_t r_t W_t mod M (M = prod m_t) in three
 //     42-bit fp64 levels, undoes the scaling, and runs the op's
 //     epilogue (the same epilogue_tile as the DMMA kernel).
@@ -91,8 +92,9 @@ __device__ __forceinline__ size_t oz_off(int r, int k, int K, int TR) {
 // the quotient is rounded by the 1.5 2^52 trick (|v / G| < 2^51), the fma
 // remainder is exact, and the same trick hands its integer bits over.
 // Then each modulus of the group: floor(x / m) by multiply-high with
-// floor(2^32 / m) (x < 2^25: at most one short), one correction, and a
-// representative in [-128, 127].  Integer / FMA pipes only.
+// floor(2^32 / m) (x < 2^25: at most one short) and one correction: the
+// residue in [0, m) (the GEMM runs unsigned 8-bit operands).  Integer / FMA
+// pipes only.
 __device__ __forceinline__ uint32_t oz_mod_group(double v, double G, double invG) {
   const double M52 = 6755399441055744.0;  // 1.5 * 2^52
   const double q = fma(v, invG, M52) - M52;
@@ -102,6 +104,14 @@ __device__ __forceinline__ uint32_t oz_mod_group(double v, double G, double invG
 __device__ __forceinline__ int oz_mod_small(uint32_t x, const OzConst& C, int t) {
   const uint32_t m = static_cast<uint32_t>(C.mod[t]);
   uint32_t r = x - __umulhi(x, C.cdiv[t]) * m;  // in [0, 2m)
+  if (r >= m) r -= m;
+  return static_cast<int>(r);
+}
+// C_t (0 <= C_t <= K 255^2 < 2^31) mod m_t as a representative in
+// [-128, 127] for the CRT: multiply-high quotient (C_t < 2^32: at most one
+// short), one correction, then the symmetric range.
+__device__ __forceinline__ int oz_mod_acc(uint32_t x, uint32_t m, uint32_t cdiv) {
+  uint32_t r = x - __umulhi(x, cdiv) * m;
   if (r >= m) r -= m;
   return r > 127u ? static_cast<int>(r) - static_cast<int>(m) : static_cast<int>(r);
 }
@@ -211,10 +221,10 @@ __device__ __forceinline__ uint64_t oz_desc(uint32_t saddr, uint32_t lbo, uint32
          (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (static_cast<uint64_t>(1) << 46);
 }
-// instruction descriptor: kind::i8, s32 accumulator, signed A and B, K-major
+// instruction descriptor: kind::i8, s32 accumulator, unsigned 8-bit A and B
+// (residues in [0, m_t)), K-major
 __host__ __device__ constexpr uint32_t oz_idesc(int m, int n) {
-  return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
-         (static_cast<uint32_t>(m >> 4) << 24);
+  return (2u << 4) | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
 }
 __device__ __forceinline__ void oz_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -329,7 +339,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, co
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const int row = m0 + warp * 32 + lane;
   const int mod = C.mod[t];
-  const float inv = C.inv[t];
+  const uint32_t cdiv = C.cdiv[t];
   int8_t* dst = oz.res + (static_cast<size_t>(ci) * C.nm + t) * lplane +
                 static_cast<size_t>(row) * NP + n0;
 #pragma unroll 1
@@ -351,10 +361,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, co
     for (int j = 0; j < 32; ++j) {
       // |x| <= K 2^14 <= 2^27: the float quotient is within 0.1 of x / m, so
       // one correction lands in [-128, 127]
-      const int x = static_cast<int>(v[j]);
-      int r = x - __float2int_rn(__int2float_rn(x) * inv) * mod;
-      if (r > 127) r -= mod;
-      if (r < -128) r += mod;
+      const int r = oz_mod_acc(v[j], static_cast<uint32_t>(mod), cdiv);
       const uint32_t bb = static_cast<uint32_t>(r) & 0xffu;
       packed[j >> 2] = (j & 3) == 0 ? bb : (packed[j >> 2] | (bb << (8 * (j & 3))));
     }
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la,
       asm volatile("tcgen05.fence::after_thread_sync;\n");
       const int row = y * OZ_TM + q * 32 + lane;
       const int mod = C.mod[t];
-      const float inv = C.inv[t];
+      const uint32_t cdiv = C.cdiv[t];
       int8_t* dst = oz.res + (static_cast<size_t>(ci) * C.nm + t) * lplane +
                     static_cast<size_t>(row) * NP + x * OZ_TN;
 #pragma unroll 1
@@ -526,10 +533,7 @@ __global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la,
         uint32_t packed[8];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int xx = static_cast<int>(v[j]);
-          int r = xx - __float2int_rn(__int2float_rn(xx) * inv) * mod;
-          if (r > 127) r -= mod;
-          if (r < -128) r += mod;
+          const int r = oz_mod_acc(v[j], static_cast<uint32_t>(mod), cdiv);
           const uint32_t bb = static_cast<uint32_t>(r) & 0xffu;
           packed[j >> 2] = (j & 3) == 0 ? bb : (packed[j >> 2] | (bb << (8 * (j & 3))));
         }
