@@ -30,18 +30,16 @@ constexpr int OZ_MAXG = 6;  // moduli groups with products below 2^24
 constexpr int OZ_TM = 128, OZ_TN = 256, OZ_KS = 128, OZ_NSTAGE = 4;
 constexpr int OZ_A_ST = OZ_TM * OZ_KS, OZ_B_ST = OZ_TN * OZ_KS, OZ_STAGE = OZ_A_ST + OZ_B_ST;
 constexpr size_t OZ_SMEM = static_cast<size_t>(OZ_NSTAGE) * OZ_STAGE;  // 192 KiB
-// K <= 512: 2 stages (96 KiB) so two CTAs share an SM and one's epilogue
-// overlaps the other's MMAs
+// one-CTA-per-tile oz_gemm (CSM_OZ_GEMM=tile) for NP <= 1024: 2 stages
+// (96 KiB) so two CTAs share an SM and one's epilogue overlaps the other's
 constexpr int OZ_NSTAGE_SMALL = 2;
 constexpr int OZ_THREADS = 128;
 
 struct OzConst {
-  int nm, P, ng;
+  int nm, P;
   int mod[OZ_MAXM];
-  float inv[OZ_MAXM];
   uint32_t cdiv[OZ_MAXM];    // floor(2^32 / m_t): x / m_t by multiply-high
-  int gend[OZ_MAXG];         // group g = moduli [gend[g-1], gend[g])
-  double gmod[OZ_MAXG];      // product of the group's moduli (< 2^24)
+  double gmod[OZ_MAXG];      // product of moduli 3g .. 3g + 2 (< 2^24)
   double ginv[OZ_MAXG];      // 1 / gmod
   double w[OZ_MAXM][OZ_LV];  // W_t = (M/m_t) ((M/m_t)^-1 mod m_t) in 42-bit digits, high first
   double M[OZ_LV];

@@ -878,7 +878,6 @@ tk::OzConst oz_const(int nm, int K) {
   for (int t = 0; t < nm; ++t) {
     const int m = kOzMods[t];
     C.mod[t] = m;
-    C.inv[t] = 1.0f / static_cast<float>(m);
     C.cdiv[t] = static_cast<uint32_t>((static_cast<uint64_t>(1) << 32) / static_cast<uint64_t>(m));
     const u128 Mt = M / static_cast<u128>(m);
     const int a = static_cast<int>(Mt % static_cast<u128>(m));
@@ -890,21 +889,15 @@ tk::OzConst oz_const(int nm, int K) {
       C.w[t][l] = static_cast<double>(
           static_cast<uint64_t>((W >> (tk::OZ_LVB * (tk::OZ_LV - 1 - l))) & mask));
   }
-  // groups of consecutive moduli whose product stays below 2^24
-  C.ng = 0;
-  double G = 1.0;
-  for (int t = 0; t < nm; ++t) {
-    if (G * kOzMods[t] >= 16777216.0) {
-      C.gmod[C.ng] = G;
-      C.ginv[C.ng] = 1.0 / G;
-      C.gend[C.ng++] = t;
-      G = 1.0;
-    }
-    G *= kOzMods[t];
+  // residues go through groups of three consecutive moduli (the last one
+  // shorter), each product below 2^24 (oz_store_residues; checked in
+  // tests/test_ozaki_math.py)
+  for (int g = 0; 3 * g < nm; ++g) {
+    double G = 1.0;
+    for (int t = 3 * g; t < 3 * g + 3 && t < nm; ++t) G *= kOzMods[t];
+    C.gmod[g] = G;
+    C.ginv[g] = 1.0 / G;
   }
-  C.gmod[C.ng] = G;
-  C.ginv[C.ng] = 1.0 / G;
-  C.gend[C.ng++] = nm;
   for (int l = 0; l < tk::OZ_LV; ++l)
     C.M[l] = static_cast<double>(
         static_cast<uint64_t>((M >> (tk::OZ_LVB * (tk::OZ_LV - 1 - l))) & mask));
