@@ -208,3 +208,27 @@ def test_auto_engine_picks_by_size(cuda):
         csm.set_engine("auto")
     assert np.array_equal(au.cos_part, dm.cos_part)
     assert np.array_equal(au.sin_part, dm.sin_part)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("n", [768, 1000])
+def test_odd_tile_counts_and_padding(ozaki, n):
+    """NP = 768: three 256-wide column tiles and three 256-row tile pairs for
+    the persistent GEMM's cluster pairs; n = 1000: zero padding to NP = 1024
+    (block-diagonal, exact).  Trig and wave, against the oracle at the 1e-12
+    bar."""
+    rng = np.random.default_rng(818 + n)
+    a = cfg2_like(rng, 2, n=n, lo=-1.0, hi=1.5)
+    rep = csm.cos_sin_batched(a)
+    for i in range(a.shape[0]):
+        c, s, k, sc = orc.cos_sin(a[i])
+        assert (int(rep.k[i]), int(rep.s[i])) == (k, sc)
+        assert pair_close(rep.cos_part[i], c, s, TOL64)[0], (n, i)
+        assert pair_close(rep.sin_part[i], s, c, TOL64)[0], (n, i)
+    aw, tw = laplacian_wave(rng, 1, n)
+    tw = np.minimum(tw, 1e-3)
+    w = csm.wave_cos_sin_batched(aw, tw)
+    c, s, k, sc = orc.wave_cos_sin(aw[0], tw[0])
+    assert (int(w.k[0]), int(w.s[0])) == (k, sc)
+    assert rel1(w.cos_part[0], c) <= TOL64
+    assert rel1(w.sin_part[0], s) <= TOL64
