@@ -34,6 +34,8 @@ constexpr size_t OZ_SMEM = static_cast<size_t>(OZ_NSTAGE) * OZ_STAGE;  // 192 Ki
 // (96 KiB) so two CTAs share an SM and one's epilogue overlaps the other's
 constexpr int OZ_NSTAGE_SMALL = 2;
 constexpr int OZ_THREADS = 128;
+// oz_crt_epi: the 64 x 64 product tile in the epilogue's padded layout only
+constexpr size_t OZ_CRT_SMEM = static_cast<size_t>(BM) * LDE * sizeof(double);
 
 struct OzConst {
   int nm, P;
@@ -596,7 +598,12 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
   const unsigned long long* mxl = oz.mxL + static_cast<size_t>(ci) * M + tm * BM;
   double* E = sm;
   const double d1s = ldexp(1.0, OZ_LVB), d2s = ldexp(1.0, 2 * OZ_LVB);
-#pragma unroll 1
+  // residue loads run one group ahead of the reconstruction (the kernel is
+  // bound by their latency at 12 warps per SM)
+  uint32_t w4[NM];
+#pragma unroll
+  for (int t = 0; t < NM; ++t)
+    w4[t] = *reinterpret_cast<const uint32_t*>(res + t * plane + static_cast<size_t>(rbase) * NP);
   for (int g = 0; g < 8; ++g) {
     const int rr = rbase + 8 * g;
     const int sa = oz_shift(mxl[rr], C.P);
@@ -605,10 +612,11 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
     for (int e = 0; e < 4; ++e)
 #pragma unroll
       for (int l = 0; l < OZ_LV; ++l) s[e][l] = 0.0;
-    uint32_t w4[NM];
+    uint32_t wn[NM];
+    const int rn = g < 7 ? rr + 8 : rr;
 #pragma unroll
     for (int t = 0; t < NM; ++t)
-      w4[t] = *reinterpret_cast<const uint32_t*>(res + t * plane + static_cast<size_t>(rr) * NP);
+      wn[t] = *reinterpret_cast<const uint32_t*>(res + t * plane + static_cast<size_t>(rn) * NP);
 #pragma unroll
     for (int t = 0; t < NM; ++t) {
 #pragma unroll
@@ -632,6 +640,8 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
       const double v = fma(e0, d2s, fma(e1, d1s, e2));
       E[rr * LDE + c4 + e] = ldexp(v, -(sa + sb[e]));
     }
+#pragma unroll
+    for (int t = 0; t < NM; ++t) w4[t] = wn[t];
   }
   __syncthreads();
   epilogue_tile(la, op, sh_b, tm, tn, E);

@@ -1071,9 +1071,9 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
     prof_end(stream, 2);
     if (e != cudaSuccess) return e;
     if (C.nm == 16)
-      tk::oz_crt_epi<16><<<gcrt, tk::THREADS, tk::SMEM, stream>>>(A, O, C);
+      tk::oz_crt_epi<16><<<gcrt, tk::THREADS, tk::OZ_CRT_SMEM, stream>>>(A, O, C);
     else
-      tk::oz_crt_epi<9><<<gcrt, tk::THREADS, tk::SMEM, stream>>>(A, O, C);
+      tk::oz_crt_epi<9><<<gcrt, tk::THREADS, tk::OZ_CRT_SMEM, stream>>>(A, O, C);
     *launches += 6;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
