@@ -75,8 +75,17 @@ __device__ __forceinline__ const double* oz_rhs(const LaunchArgs& a, int item) {
   oz_item(a, item, opi, b);
   return a.rhs_full ? a.rhs_full : slot_ptr(a, b, a.ops[opi].rhs);
 }
+// |x| for the maxima, with NaN mapped to +Inf (fmax would drop it): a row or
+// column holding a non-finite entry gets max +Inf, and every product entry
+// it touches is NaN (oz_crt_epi), as an fp64 GEMM would make it non-finite
+__device__ __forceinline__ double oz_absmax(double m, double x) {
+  const double a = fabs(x);
+  return a <= 1.7976931348623157e308 ? fmax(m, a) : __longlong_as_double(0x7ff0000000000000ll);
+}
+constexpr unsigned long long OZ_INF_BITS = 0x7ff0000000000000ull;
 // 2^shift scales a row (column) whose max |x| has bits mx below 2^P
 __device__ __forceinline__ int oz_shift(unsigned long long mx, int P) {
+  if (mx >= OZ_INF_BITS) return 0;  // non-finite row / column: result is NaN anyway
   const double m = __longlong_as_double(static_cast<long long>(mx));
   int e = 0;
   frexp(m, &e);
@@ -125,7 +134,7 @@ __global__ void oz_rowmax(const LaunchArgs la, const OzArgs oz) {
   double m = 0.0;
   for (int k = lane * 2; k < NP; k += 64) {
     const double2 v = *reinterpret_cast<const double2*>(L + k);
-    m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+    m = oz_absmax(oz_absmax(m, v.x), v.y);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -139,7 +148,7 @@ __global__ void oz_colmax(const LaunchArgs la, const OzArgs oz) {
   const double* R = oz_rhs(la, oz.item0 + ci);
   double m = 0.0;
 #pragma unroll 8
-  for (int k = k0; k < k0 + 64; ++k) m = fmax(m, fabs(R[static_cast<size_t>(k) * NP + c]));
+  for (int k = k0; k < k0 + 64; ++k) m = oz_absmax(m, R[static_cast<size_t>(k) * NP + c]);
   atomicMax(oz.mxR + static_cast<size_t>(ci) * NP + c,
             static_cast<unsigned long long>(__double_as_longlong(m)));
 }
@@ -590,10 +599,14 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
   const int8_t* res = oz.res + static_cast<size_t>(ci) * NM * plane +
                       static_cast<size_t>(tm * BM) * NP + tn * BN + c4;
   int sb[4];
+  bool badc[4];
   {
     const unsigned long long* mxr = oz.mxR + static_cast<size_t>(ci) * NP + tn * BN + c4;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) sb[e] = oz_shift(mxr[e], C.P);
+    for (int e = 0; e < 4; ++e) {
+      sb[e] = oz_shift(mxr[e], C.P);
+      badc[e] = mxr[e] >= OZ_INF_BITS;
+    }
   }
   const unsigned long long* mxl = oz.mxL + static_cast<size_t>(ci) * M + tm * BM;
   double* E = sm;
@@ -607,6 +620,7 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
   for (int g = 0; g < 8; ++g) {
     const int rr = rbase + 8 * g;
     const int sa = oz_shift(mxl[rr], C.P);
+    const bool badr = mxl[rr] >= OZ_INF_BITS;
     double s[4][OZ_LV];
 #pragma unroll
     for (int e = 0; e < 4; ++e)
@@ -638,7 +652,8 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
       const double e1 = fma(-q, C.M[1], s[e][1]);
       const double e2 = fma(-q, C.M[2], s[e][2]);
       const double v = fma(e0, d2s, fma(e1, d1s, e2));
-      E[rr * LDE + c4 + e] = ldexp(v, -(sa + sb[e]));
+      E[rr * LDE + c4 + e] =
+          (badr || badc[e]) ? __longlong_as_double(0x7ff8000000000000ll) : ldexp(v, -(sa + sb[e]));
     }
 #pragma unroll
     for (int t = 0; t < NM; ++t) w4[t] = wn[t];

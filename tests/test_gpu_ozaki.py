@@ -232,3 +232,20 @@ def test_odd_tile_counts_and_padding(ozaki, n):
     assert (int(w.k[0]), int(w.s[0])) == (k, sc)
     assert rel1(w.cos_part[0], c) <= TOL64
     assert rel1(w.sin_part[0], s) <= TOL64
+
+
+def test_overflow_mid_chain_stays_non_finite(ozaki):
+    """A chain that overflows (norm 1e5: cos entries beyond 1e308 by the
+    doubling) must come out non-finite as on the DMMA engine (and in the
+    reference's numpy products), not as finite garbage reconstructed from
+    residues of Inf / NaN operands."""
+    rng = np.random.default_rng(819)
+    a = cfg2_like(rng, 1, n=256, lo=5.0, hi=5.0)
+    oz = csm.cos_sin_batched(a, raise_on_error=False)
+    csm.set_engine("dmma")
+    dm = csm.cos_sin_batched(a, raise_on_error=False)
+    csm.set_engine("ozaki")
+    assert int(oz.status[0]) == int(dm.status[0]) == 0
+    assert not np.isfinite(dm.cos_part[0]).all()  # the case overflows on DMMA
+    assert not np.isfinite(oz.cos_part[0]).all()
+    assert not np.isfinite(oz.sin_part[0]).all()
