@@ -55,6 +55,7 @@ struct OzArgs {
   int8_t* pL;               // [nitems][nm][M x NP]  residue planes of L'
   int8_t* pR;               // [nitems][nm][NP x NP] residue planes of R'^T
   int8_t* res;              // [nitems][nm][M x NP]  residues of L'R'
+  unsigned* bad;            // [nitems] nonzero: L or R holds a non-finite entry
 };
 
 __device__ __forceinline__ void oz_item(const LaunchArgs& a, int item, int& opi, int& b) {
@@ -138,7 +139,10 @@ __global__ void oz_rowmax(const LaunchArgs la, const OzArgs oz) {
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) oz.mxL[static_cast<size_t>(ci) * la.M + r] = __double_as_longlong(m);
+  if (lane == 0) {
+    oz.mxL[static_cast<size_t>(ci) * la.M + r] = __double_as_longlong(m);
+    if (!(m <= 1.7976931348623157e308)) atomicOr(oz.bad + ci, 1u);
+  }
 }
 // grid (NP / 256, NP / 64, nitems), 256 threads: column maxima of R over
 // 64-row chunks, combined by atomicMax (mxR zeroed beforehand)
@@ -151,6 +155,7 @@ __global__ void oz_colmax(const LaunchArgs la, const OzArgs oz) {
   for (int k = k0; k < k0 + 64; ++k) m = oz_absmax(m, R[static_cast<size_t>(k) * NP + c]);
   atomicMax(oz.mxR + static_cast<size_t>(ci) * NP + c,
             static_cast<unsigned long long>(__double_as_longlong(m)));
+  if (!(m <= 1.7976931348623157e308)) atomicOr(oz.bad + ci, 1u);
 }
 
 __device__ __forceinline__ uint4 oz_pack16(const int (&b)[16]) {
@@ -599,14 +604,10 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
   const int8_t* res = oz.res + static_cast<size_t>(ci) * NM * plane +
                       static_cast<size_t>(tm * BM) * NP + tn * BN + c4;
   int sb[4];
-  bool badc[4];
   {
     const unsigned long long* mxr = oz.mxR + static_cast<size_t>(ci) * NP + tn * BN + c4;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      sb[e] = oz_shift(mxr[e], C.P);
-      badc[e] = mxr[e] >= OZ_INF_BITS;
-    }
+    for (int e = 0; e < 4; ++e) sb[e] = oz_shift(mxr[e], C.P);
   }
   const unsigned long long* mxl = oz.mxL + static_cast<size_t>(ci) * M + tm * BM;
   double* E = sm;
@@ -620,7 +621,6 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
   for (int g = 0; g < 8; ++g) {
     const int rr = rbase + 8 * g;
     const int sa = oz_shift(mxl[rr], C.P);
-    const bool badr = mxl[rr] >= OZ_INF_BITS;
     double s[4][OZ_LV];
 #pragma unroll
     for (int e = 0; e < 4; ++e)
@@ -652,11 +652,24 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
       const double e1 = fma(-q, C.M[1], s[e][1]);
       const double e2 = fma(-q, C.M[2], s[e][2]);
       const double v = fma(e0, d2s, fma(e1, d1s, e2));
-      E[rr * LDE + c4 + e] =
-          (badr || badc[e]) ? __longlong_as_double(0x7ff8000000000000ll) : ldexp(v, -(sa + sb[e]));
+      E[rr * LDE + c4 + e] = ldexp(v, -(sa + sb[e]));
     }
 #pragma unroll
     for (int t = 0; t < NM; ++t) w4[t] = wn[t];
+  }
+  {
+    // a row of L or a column of R with a non-finite entry (max +Inf): the
+    // product entries it touches are NaN, as an fp64 GEMM would make them
+    // non-finite (rare: the max kernels flag the item, a fix-up pass then)
+    const unsigned long long* mxr = oz.mxR + static_cast<size_t>(ci) * NP + tn * BN;
+    __syncthreads();
+    if (oz.bad[ci]) {
+      for (int p = tid; p < BM * BN; p += THREADS) {
+        const int rr = p / BN, cc = p % BN;
+        if (mxl[rr] >= OZ_INF_BITS || mxr[cc] >= OZ_INF_BITS)
+          E[rr * LDE + cc] = __longlong_as_double(0x7ff8000000000000ll);
+      }
+    }
   }
   __syncthreads();
   epilogue_tile(la, op, sh_b, tm, tn, E);

@@ -909,7 +909,7 @@ tk::OzConst oz_const(int nm, int K) {
 // Ozaki scratch per product item (M = NP rows): row / column maxima, the
 // residue planes of both operands and of the product.
 static size_t oz_item_bytes(size_t NP) {
-  return 2 * NP * sizeof(unsigned long long) + 3 * tk::OZ_MAXM * NP * NP + 256;
+  return 2 * NP * sizeof(unsigned long long) + 3 * tk::OZ_MAXM * NP * NP + 256 + 8;
 }
 static int64_t oz_cap_items(int64_t batch, size_t NP) {
   const size_t budget = static_cast<size_t>(4) << 30;
@@ -961,6 +961,8 @@ static TiledWs carve(void* ws, int64_t batch, int n) {
     p += static_cast<size_t>(cap) * NP * 8;
     w.oz.mxR = reinterpret_cast<unsigned long long*>(p);
     p += static_cast<size_t>(cap) * NP * 8;
+    w.oz.bad = reinterpret_cast<unsigned*>(p);
+    p += static_cast<size_t>(cap) * 8;
     p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
     w.oz.pL = reinterpret_cast<int8_t*>(p);
     p += static_cast<size_t>(cap) * tk::OZ_MAXM * NP * NP;
@@ -1019,6 +1021,7 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
     O.item0 = done;
     O.nitems = cnt;
     cudaError_t e = cudaMemsetAsync(O.mxR, 0, static_cast<size_t>(cnt) * NP * 8, stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(O.bad, 0, static_cast<size_t>(cnt) * 4, stream);
     if (e != cudaSuccess) return e;
     tk::oz_rowmax<<<dim3(M / 8, cnt), 256, 0, stream>>>(A, O);
     tk::oz_colmax<<<dim3(NP / 256, NP / 64, cnt), 256, 0, stream>>>(A, O);
@@ -1350,7 +1353,7 @@ static bool oz_slab_applies(int M, int NP) { return oz_applies(NP) && M % (2 * t
 size_t slab_engine_bytes(int M, int NP) {
   if (!oz_slab_applies(M, NP)) return 0;
   const size_t m = static_cast<size_t>(M), np = static_cast<size_t>(NP);
-  return (m + np) * 8 + tk::OZ_MAXM * (2 * m * np + np * np) + 4 * 256;
+  return (m + np) * 8 + 8 + tk::OZ_MAXM * (2 * m * np + np * np) + 6 * 256;
 }
 
 // Run one Op on a block-row slab: out rows = L_rows * rhs_full (+ epilogue).
@@ -1414,6 +1417,8 @@ cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
     p = align(p + m * 8);
     O.mxR = reinterpret_cast<unsigned long long*>(p);
     p = align(p + np * 8);
+    O.bad = reinterpret_cast<unsigned*>(p);
+    p = align(p + 8);
     O.pL = reinterpret_cast<int8_t*>(p);
     p = align(p + tk::OZ_MAXM * m * np);
     O.pR = reinterpret_cast<int8_t*>(p);
