@@ -76,6 +76,21 @@ __device__ __forceinline__ const double* oz_rhs(const LaunchArgs& a, int item) {
   oz_item(a, item, opi, b);
   return a.rhs_full ? a.rhs_full : slot_ptr(a, b, a.ops[opi].rhs);
 }
+// Chunk-local item whose right-operand residues item ci uses.  A doubling
+// launch pairs S C and C C per group (consecutive segments with the same
+// matrices, doubling_ops): the second op's items take the first's planes of
+// C when those are in the same chunk, so C is converted once per step.
+__device__ __forceinline__ int oz_rsrc(const LaunchArgs& a, const OzArgs& oz, int ci) {
+  if (a.dbl_step < 0) return ci;
+  const int item = oz.item0 + ci;
+  int k = 0;
+#pragma unroll
+  for (int i = 1; i < MAXSEG; ++i)
+    if (i < a.nseg && item >= a.seg[i].start) k = i;
+  if ((k & 1) == 0) return ci;
+  const int partner = item - (a.seg[k].start - a.seg[k - 1].start);
+  return partner >= oz.item0 ? partner - oz.item0 : ci;
+}
 // |x| for the maxima, with NaN mapped to +Inf (fmax would drop it): a row or
 // column holding a non-finite entry gets max +Inf, and every product entry
 // it touches is NaN (oz_crt_epi), as an fp64 GEMM would make it non-finite
@@ -148,6 +163,7 @@ __global__ void oz_rowmax(const LaunchArgs la, const OzArgs oz) {
 // 64-row chunks, combined by atomicMax (mxR zeroed beforehand)
 __global__ void oz_colmax(const LaunchArgs la, const OzArgs oz) {
   const int ci = blockIdx.z, NP = la.NP;
+  if (oz_rsrc(la, oz, ci) != ci) return;  // shares an earlier item's right operand
   const int c = blockIdx.x * 256 + threadIdx.x, k0 = blockIdx.y * 64;
   const double* R = oz_rhs(la, oz.item0 + ci);
   double m = 0.0;
@@ -214,6 +230,7 @@ __global__ void oz_conv_rows(const LaunchArgs la, const OzArgs oz, const OzConst
 template <int NM>
 __global__ void oz_conv_cols(const LaunchArgs la, const OzArgs oz, const OzConst C) {
   const int ci = blockIdx.z, NP = la.NP;
+  if (oz_rsrc(la, oz, ci) != ci) return;
   const int c = blockIdx.x * 128 + threadIdx.x, k0 = blockIdx.y * 16;
   const double* R = oz_rhs(la, oz.item0 + ci) + static_cast<size_t>(k0) * NP + c;
   const int sh = oz_shift(oz.mxR[static_cast<size_t>(ci) * NP + c], C.P);
@@ -299,7 +316,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, co
   const size_t lplane = static_cast<size_t>(M) * NP, rplane = static_cast<size_t>(NP) * NP;
   const int8_t* abase = oz.pL + (static_cast<size_t>(ci) * C.nm + t) * lplane +
                         static_cast<size_t>(blockIdx.y) * kb32 * 32 * OZ_TM;
-  const int8_t* bbase = oz.pR + (static_cast<size_t>(ci) * C.nm + t) * rplane +
+  const int8_t* bbase = oz.pR + (static_cast<size_t>(oz_rsrc(la, oz, ci)) * C.nm + t) * rplane +
                         static_cast<size_t>(blockIdx.x) * kb32 * 32 * OZ_TN;
   constexpr int BH = OZ_B_ST / 2;
   if (warp == 0 && lane == 0) {
@@ -457,7 +474,7 @@ __global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la,
         const int ci = z / C.nm, t = z - ci * C.nm;
         const int8_t* abase = oz.pL + (static_cast<size_t>(ci) * C.nm + t) * lplane +
                               static_cast<size_t>(y) * kb32 * 32 * OZ_TM;
-        const int8_t* bbase = oz.pR + (static_cast<size_t>(ci) * C.nm + t) * rplane +
+        const int8_t* bbase = oz.pR + (static_cast<size_t>(oz_rsrc(la, oz, ci)) * C.nm + t) * rplane +
                               static_cast<size_t>(x) * kb32 * 32 * OZ_TN;
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const int st = g % NST;
@@ -597,6 +614,7 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
   const int NP = la.NP, M = la.M;
   const int tiles_n = NP / BN;
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x - tm * tiles_n;
+  const int rs = oz_rsrc(la, oz, ci);  // item holding this product's right operand
   // 64 x 64 tile: thread -> columns 4 (tid & 15) .. +4 of rows (tid >> 4) + 8 g,
   // g = 0..7, so a warp's residue loads are two contiguous 64-byte row runs
   const int c4 = (tid & 15) * 4, rbase = tid >> 4;
@@ -605,7 +623,7 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
                       static_cast<size_t>(tm * BM) * NP + tn * BN + c4;
   int sb[4];
   {
-    const unsigned long long* mxr = oz.mxR + static_cast<size_t>(ci) * NP + tn * BN + c4;
+    const unsigned long long* mxr = oz.mxR + static_cast<size_t>(rs) * NP + tn * BN + c4;
 #pragma unroll
     for (int e = 0; e < 4; ++e) sb[e] = oz_shift(mxr[e], C.P);
   }
@@ -661,9 +679,9 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
     // a row of L or a column of R with a non-finite entry (max +Inf): the
     // product entries it touches are NaN, as an fp64 GEMM would make them
     // non-finite (rare: the max kernels flag the item, a fix-up pass then)
-    const unsigned long long* mxr = oz.mxR + static_cast<size_t>(ci) * NP + tn * BN;
+    const unsigned long long* mxr = oz.mxR + static_cast<size_t>(rs) * NP + tn * BN;
     __syncthreads();
-    if (oz.bad[ci]) {
+    if (oz.bad[ci] | oz.bad[rs]) {
       for (int p = tid; p < BM * BN; p += THREADS) {
         const int rr = p / BN, cc = p % BN;
         if (mxl[rr] >= OZ_INF_BITS || mxr[cc] >= OZ_INF_BITS)
