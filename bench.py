@@ -324,7 +324,7 @@ def run_cfg5(args, cfg):
             "e2e": {"value": 1.0 / (e2e_ms * 1e-3), "unit": "matrices/s",
                     "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": 2 * M * n * 8,
                     "ms_per_step": e2e_ms},
-            "gpu_launches": (st.k + 2 * st.s) * args.steps,
+            "gpu_launches": st.launches * args.steps,
             "clocks": clk.summary(), "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)

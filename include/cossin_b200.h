@@ -221,6 +221,13 @@ int csm_slab_op(const void* op, double* slab, int M, int NP, int row0,
                 const double* rhs_full, const double* in0, int s, double tp,
                 int dbl_step, void* cos_out, void* sin_out, int out_f32,
                 void* scratch, void* stream);
+/* csm_slab_op_pair: the doubling step's two ops (csm_doubling_program: S C
+ * and C C, both with right operand C = rhs_full) in one launch; on the
+ * Ozaki engine C is converted once for both (dbl_step >= 0 required). */
+int csm_slab_op_pair(const void* op_a, const void* op_b, double* slab, int M, int NP,
+                     int row0, const double* rhs_full, const double* in0, int s,
+                     double tp, int dbl_step, void* cos_out, void* sin_out,
+                     int out_f32, void* scratch, void* stream);
 /* Fused all-gather + product: like csm_slab_op, but the right operand is
  * NOT gathered -- rhs_slabs (HOST array of nparts pointers) holds each
  * rank's slab base, peer pointers over NVLink (e.g. from torch symmetric

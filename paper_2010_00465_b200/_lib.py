@@ -65,6 +65,8 @@ SIGNATURES = {
                            _i32, _vp, _vp]),
     "csm_slab_op_peer": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _dp, _i32,
                                 _vp, _vp, _i32, _vp, _vp]),
+    "csm_slab_op_pair": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _dp, _i32,
+                                _vp, _vp, _i32, _vp, _vp]),
     "csm_graph_safe": (_i32, [_i32, _i64, _i32]),
     "csm_set_engine": (_i32, [_i32]),
     "csm_get_engine": (_i32, []),

@@ -46,7 +46,7 @@ int chain_program(bool wave, int k, bool fold, void* ops_out, int max_ops, int32
 void doubling_program(int c0, int s0, int c1, int s1, void* ops_out);
 size_t slab_scratch_bytes();
 size_t slab_engine_bytes(int M, int NP);
-cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
+cudaError_t slab_op(const void* const* op_host, int nops, double* slab, int M, int NP, int row0,
                     const double* rhs_full, const double* in0, int s, double tp, int dbl_step,
                     void* cout, void* sout, int out_f32, void* scratch, cudaStream_t stream,
                     int64_t* launches, const double* const* parts_host, int nparts);
@@ -548,10 +548,30 @@ int csm_slab_op(const void* op, double* slab, int M, int NP, int row0, const dou
     return fail(CSM_ERR_ARG, "slab shape must be M x NP with M, NP multiples of 64");
   int rc = check_device();
   if (rc) return rc;
-  cudaError_t e = csm::slab_op(op, slab, M, NP, row0, rhs_full, in0, s, tp, dbl_step, cos_out,
-                               sin_out, out_f32, scratch, static_cast<cudaStream_t>(stream),
-                               &g_launches, nullptr, 0);
+  const void* ops[1] = {op};
+  cudaError_t e = csm::slab_op(ops, 1, slab, M, NP, row0, rhs_full, in0, s, tp, dbl_step,
+                               cos_out, sin_out, out_f32, scratch,
+                               static_cast<cudaStream_t>(stream), &g_launches, nullptr, 0);
   if (e != cudaSuccess) return cuda_fail(e, "slab op");
+  return CSM_SUCCESS;
+}
+
+int csm_slab_op_pair(const void* op_a, const void* op_b, double* slab, int M, int NP, int row0,
+                     const double* rhs_full, const double* in0, int s, double tp, int dbl_step,
+                     void* cos_out, void* sin_out, int out_f32, void* scratch, void* stream) {
+  g_launches = 0;
+  if (!op_a || !op_b || !slab || !rhs_full || !scratch)
+    return fail(CSM_ERR_ARG, "null pointer argument");
+  if (M <= 0 || NP <= 0 || M % 64 || NP % 64 || row0 < 0 || row0 + M > NP)
+    return fail(CSM_ERR_ARG, "slab shape must be M x NP with M, NP multiples of 64");
+  if (dbl_step < 0) return fail(CSM_ERR_ARG, "csm_slab_op_pair runs a doubling step (dbl_step >= 0)");
+  int rc = check_device();
+  if (rc) return rc;
+  const void* ops[2] = {op_a, op_b};
+  cudaError_t e = csm::slab_op(ops, 2, slab, M, NP, row0, rhs_full, in0, s, tp, dbl_step,
+                               cos_out, sin_out, out_f32, scratch,
+                               static_cast<cudaStream_t>(stream), &g_launches, nullptr, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "slab op pair");
   return CSM_SUCCESS;
 }
 
@@ -567,7 +587,8 @@ int csm_slab_op_peer(const void* op, double* slab, int M, int NP, int row0,
     if (!rhs_slabs[i]) return fail(CSM_ERR_ARG, "null peer slab");
   int rc = check_device();
   if (rc) return rc;
-  cudaError_t e = csm::slab_op(op, slab, M, NP, row0, nullptr, in0, s, tp, dbl_step, cos_out,
+  const void* ops[1] = {op};
+  cudaError_t e = csm::slab_op(ops, 1, slab, M, NP, row0, nullptr, in0, s, tp, dbl_step, cos_out,
                                sin_out, out_f32, scratch, static_cast<cudaStream_t>(stream),
                                &g_launches, rhs_slabs, nparts);
   if (e != cudaSuccess) return cuda_fail(e, "peer slab op");

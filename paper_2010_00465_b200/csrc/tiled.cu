@@ -1345,35 +1345,42 @@ void doubling_program(int c0, int s0, int c1, int s1, void* ops_out) {
 }
 
 constexpr int kMaxParts = 64;
-size_t slab_scratch_bytes() { return sizeof(Op) + 64 + kMaxParts * sizeof(double*); }
+size_t slab_scratch_bytes() { return 2 * sizeof(Op) + 64 + kMaxParts * sizeof(double*); }
 
 // Extra slab scratch the Ozaki engine needs for an M x NP slab (0 when the
 // DMMA engine runs it).
 static bool oz_slab_applies(int M, int NP) { return oz_applies(NP) && M % (2 * tk::OZ_TM) == 0; }
+// Sized for csm_slab_op_pair: two left operands and products, one right
+// operand (the pair shares it).
 size_t slab_engine_bytes(int M, int NP) {
   if (!oz_slab_applies(M, NP)) return 0;
   const size_t m = static_cast<size_t>(M), np = static_cast<size_t>(NP);
-  return (m + np) * 8 + 8 + tk::OZ_MAXM * (2 * m * np + np * np) + 6 * 256;
+  return 2 * (m + np) * 8 + 16 + tk::OZ_MAXM * (4 * m * np + np * np) + 6 * 256;
 }
 
 // Run one Op on a block-row slab: out rows = L_rows * rhs_full (+ epilogue).
 // scratch: device buffer of slab_scratch_bytes() (op descriptor, s, t').
-cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
+// Run one op (nops = 1), or the doubling step's two ops sharing the
+// right operand (nops = 2: one launch; the Ozaki engine converts it once),
+// on a block-row slab.
+cudaError_t slab_op(const void* const* op_host, int nops, double* slab, int M, int NP, int row0,
                     const double* rhs_full, const double* in0, int s, double tp, int dbl_step,
                     void* cout, void* sout, int out_f32, void* scratch, cudaStream_t stream,
                     int64_t* launches, const double* const* parts_host, int nparts) {
   if (M % tk::BM != 0 || NP % tk::BN != 0) return cudaErrorInvalidValue;
   if (nparts < 0 || nparts > kMaxParts || (nparts > 0 && nparts * M != NP))
     return cudaErrorInvalidValue;
+  if (nops < 1 || nops > 2 || (nops == 2 && dbl_step < 0)) return cudaErrorInvalidValue;
   struct alignas(16) Staged {
-    Op op;
+    Op op[2];
     int32_t idx, s, pad0, pad1;
     double tp;
     const double* parts[kMaxParts];
   };
-  static_assert(sizeof(Staged) <= sizeof(Op) + 64 + kMaxParts * sizeof(double*), "scratch layout");
+  static_assert(sizeof(Staged) <= 2 * sizeof(Op) + 64 + kMaxParts * sizeof(double*),
+                "scratch layout");
   Staged h{};
-  std::memcpy(&h.op, op_host, sizeof(Op));
+  for (int i = 0; i < nops; ++i) std::memcpy(&h.op[i], op_host[i], sizeof(Op));
   h.idx = 0;
   h.s = s;
   h.tp = tp;
@@ -1388,7 +1395,7 @@ cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
   A.ws = slab;
   A.in0 = in0;
   A.idx = &d->idx;
-  A.ops = &d->op;
+  A.ops = d->op;
   A.tsc = &d->tp;
   A.S = &d->s;
   A.cout = cout;
@@ -1398,10 +1405,10 @@ cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
   A.n = NP;
   A.out_f32 = out_f32;
   A.dbl_step = dbl_step;
-  A.nseg = 1;
-  A.total = 1;
+  A.nseg = nops;
+  A.total = nops;
   A.item_base = 0;
-  A.seg[0] = {0, 0, 0};
+  for (int i = 0; i < nops; ++i) A.seg[i] = {i, 0, i};  // op i on matrix idx[0] = 0
   A.rhs_full = nparts > 0 ? nullptr : rhs_full;
   A.rhs_parts = nparts > 0 ? d->parts : nullptr;
   A.M = M;
@@ -1412,21 +1419,21 @@ cudaError_t slab_op(const void* op_host, double* slab, int M, int NP, int row0,
     };
     char* p = align(static_cast<char*>(scratch) + slab_scratch_bytes());
     const size_t m = static_cast<size_t>(M), np = static_cast<size_t>(NP);
-    tk::OzArgs O{};
+    tk::OzArgs O{};  // two items' L-side scratch; the pair's right operand once
     O.mxL = reinterpret_cast<unsigned long long*>(p);
-    p = align(p + m * 8);
+    p = align(p + 2 * m * 8);
     O.mxR = reinterpret_cast<unsigned long long*>(p);
-    p = align(p + np * 8);
+    p = align(p + 2 * np * 8);
     O.bad = reinterpret_cast<unsigned*>(p);
-    p = align(p + 8);
+    p = align(p + 16);
     O.pL = reinterpret_cast<int8_t*>(p);
-    p = align(p + tk::OZ_MAXM * m * np);
+    p = align(p + 2 * tk::OZ_MAXM * m * np);
     O.pR = reinterpret_cast<int8_t*>(p);
     p = align(p + tk::OZ_MAXM * np * np);
     O.res = reinterpret_cast<int8_t*>(p);
-    return run_oz_launch(A, O, 1, oz_const(oz_moduli(out_f32), NP), stream, launches);
+    return run_oz_launch(A, O, nops, oz_const(oz_moduli(out_f32), NP), stream, launches);
   }
-  dim3 grid(static_cast<unsigned>((M / tk::BM) * (NP / tk::BN)), 1, 1);
+  dim3 grid(static_cast<unsigned>((M / tk::BM) * (NP / tk::BN)), static_cast<unsigned>(nops), 1);
   tk::gemm_epi_kernel<<<grid, tk::THREADS, tk::SMEM, stream>>>(A);
   ++*launches;
   return cudaGetLastError();

@@ -107,6 +107,22 @@ def _device_slab_op(op: OpView, slab, M, n, row0, rhs_full, in0, s, dbl_step,
         vp(in0.data_ptr()), s, 0.0, dbl_step, vp(cos_rows.data_ptr()),
         vp(sin_rows.data_ptr()), 0, vp(scratch.data_ptr()),
         vp(int((stream or torch.cuda.current_stream()).cuda_stream))), "csm_slab_op")
+    return int(_lib.lib().csm_last_launch_count())
+
+
+def _device_slab_op_pair(ops, slab, M, n, row0, rhs_full, in0, s, dbl_step, cos_rows,
+                         sin_rows, scratch, stream):
+    """The doubling step's two ops (S C, C C) in one csm_slab_op_pair call:
+    one launch, and one conversion of C on the Ozaki engine."""
+    import torch
+    vp = ctypes.c_void_p
+    raw = [(ctypes.c_char * len(op.raw)).from_buffer(op.raw) for op in ops]
+    _lib.check(_lib.lib().csm_slab_op_pair(
+        raw[0], raw[1], vp(slab.data_ptr()), M, n, row0, vp(rhs_full.data_ptr()),
+        vp(in0.data_ptr()), s, 0.0, dbl_step, vp(cos_rows.data_ptr()),
+        vp(sin_rows.data_ptr()), 0, vp(scratch.data_ptr()),
+        vp(int((stream or torch.cuda.current_stream()).cuda_stream))), "csm_slab_op_pair")
+    return int(_lib.lib().csm_last_launch_count())
 
 
 def _device_select(a, precision: Precision):
@@ -129,9 +145,11 @@ def _device_slab_op_peer(op: OpView, slab, M, n, row0, rhs_slabs, in0, s, dbl_st
         0.0, dbl_step, vp(cos_rows.data_ptr()), vp(sin_rows.data_ptr()), 0,
         vp(scratch.data_ptr()),
         vp(int((stream or torch.cuda.current_stream()).cuda_stream))), "csm_slab_op_peer")
+    return int(_lib.lib().csm_last_launch_count())
 
 
 slab_op = _device_slab_op
+slab_op_pair = _device_slab_op_pair
 slab_op_peer = _device_slab_op_peer
 select = _device_select
 
@@ -142,6 +160,7 @@ class DistStats:
     s: int
     gathers: int
     products: int
+    launches: int = 0  # library kernels launched by the gather-mode products
 
 
 def cos_sin_distributed(a, precision: Precision = Precision.DOUBLE, *,
@@ -192,9 +211,10 @@ def cos_sin_distributed(a, precision: Precision = Precision.DOUBLE, *,
         if op.lhs == 0 and op.rhs != 0:  # A sc = sc A: keep A as the gathered side
             op = op.swapped()
         rf = full(op.rhs)
-        slab_op(op, slab, M, n, row0, rf, in0, s, dbl_step, cos_rows, sin_rows,
-                scratch, None)
+        launched = slab_op(op, slab, M, n, row0, rf, in0, s, dbl_step, cos_rows, sin_rows,
+                           scratch, None)
         stats.products += 1
+        stats.launches += launched or 0
         return [o[0] for o in op.outs]
 
     for step in steps:
@@ -208,10 +228,12 @@ def cos_sin_distributed(a, precision: Precision = Precision.DOUBLE, *,
     c1, s1 = free[0], free[1]
     for i in range(s):
         ops = doubling_program(c0, s0, c1, s1)
-        written = []
-        for op in ops:  # both products share the gathered C
-            written += run(op, i)
-        for w in written:
+        # both products share the gathered C: one paired call
+        launched = slab_op_pair(ops, slab, M, n, row0, full(c0), in0, s, i, cos_rows,
+                                sin_rows, scratch, None)
+        stats.products += 2
+        stats.launches += launched or 0
+        for w in [o[0] for op in ops for o in op.outs]:
             cache.pop(w, None)
         c0, s0, c1, s1 = c1, s1, c0, s0
     if not gather_outputs or world == 1:
@@ -243,13 +265,14 @@ def _peer_rank_program(a, precision, rank: int, world: int, slab, rhs_slabs,
         if op.lhs == 0 and op.rhs != 0:  # A X = X A: polynomials in A commute
             op = op.swapped()
         if op.rhs == 0:
-            slab_op(op, slab, M, n, row0, a, in0, s, dbl_step, cos_rows, sin_rows,
-                    scratch, None)
+            launched = slab_op(op, slab, M, n, row0, a, in0, s, dbl_step, cos_rows, sin_rows,
+                               scratch, None)
         else:
-            slab_op_peer(op, slab, M, n, row0, rhs_slabs, in0, s, dbl_step, cos_rows,
-                         sin_rows, scratch, None)
+            launched = slab_op_peer(op, slab, M, n, row0, rhs_slabs, in0, s, dbl_step,
+                                    cos_rows, sin_rows, scratch, None)
         if rank == 0:
             stats.products += 1
+            stats.launches += launched or 0
 
     for step in steps:
         for op in step:

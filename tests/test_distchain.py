@@ -43,6 +43,15 @@ def np_slab_op(op, slab, M, n, row0, rhs_full, in0, s, dbl_step, cos_rows,
             (cos_rows if final == 1 else sin_rows).copy_(v)
 
 
+def np_slab_op_pair(ops, slab, M, n, row0, rhs_full, in0, s, dbl_step, cos_rows, sin_rows,
+                    scratch, stream):
+    """Test double of csm_slab_op_pair: the two doubling ops in turn (they
+    read S and C and write other slots, so the order does not matter)."""
+    for op in ops:
+        np_slab_op(op, slab, M, n, row0, rhs_full, in0, s, dbl_step, cos_rows, sin_rows,
+                   scratch, stream)
+
+
 def np_slab_op_peer(op, slab, M, n, row0, rhs_slabs, in0, s, dbl_step, cos_rows,
                     sin_rows, scratch, stream):
     """Test double of csm_slab_op_peer: row block j of the right operand
@@ -92,6 +101,7 @@ def _worker(rank, world, port, n, q):
     try:
         from paper_2010_00465_b200 import distchain
         distchain.slab_op = np_slab_op
+        distchain.slab_op_pair = np_slab_op_pair
         distchain.select = _np_select
         g = np.random.default_rng(0).standard_normal((n, n))
         a = torch.from_numpy(20.0 * (g + g.T) / (2.0 * np.sqrt(n)))
