@@ -412,11 +412,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) oz_gemm(const LaunchArgs la, co
 // Persistent form of oz_gemm: one cluster pair per two SMs walks the pair
 // tiles (x, y pair, item x modulus) round-robin, with warp roles --
 // warp 0: producer (the stage ring runs on across tiles), warp 1: MMA
-// issuer, warps 2..5: epilogue -- and two 256-column TMEM accumulators, so
+// issuer, warps 2..9: epilogue, two per TMEM lane quarter -- and two
+// 256-column TMEM accumulators, so
 // a tile's TMEM drain / residue epilogue overlaps the next tile's MMAs and
-// the set-up is paid once per CTA.  grid = 2 x clusters, 192 threads,
+// the set-up is paid once per CTA.  grid = 2 x clusters, 320 threads,
 // NST x 48 KiB dynamic shared memory.
-constexpr int OZ_PTHREADS = 192;
+constexpr int OZ_PEPI = 8;  // epilogue warps: two per TMEM lane quarter, 128 columns each
+constexpr int OZ_PTHREADS = 32 * (2 + OZ_PEPI);
 template <int NST>
 __global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la, const OzArgs oz,
                                                             const OzConst C, int pair_tiles) {
@@ -445,7 +447,8 @@ __global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la,
     }
     for (int i = 0; i < 2; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(oz_smem(&tm_full[i])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;\n" ::"r"(oz_smem(&tm_empty[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(oz_smem(&tm_empty[i])),
+                   "r"(OZ_PEPI));
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n");
   }
@@ -532,8 +535,8 @@ __global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la,
                 oz_smem(&tm_full[acc_i])));
       }
     }
-  } else {  // epilogue warps 2..5: TMEM lane quarter (warp % 4)
-    const int q = warp & 3;
+  } else {  // epilogue warps 2..9: TMEM lane quarter (warp % 4), column half
+    const int q = warp & 3, half = (warp - 2) >> 2;  // lane quarter, column half
     int i = 0;
     for (int T = cluster; T < pair_tiles; T += nclusters, ++i) {
       int x, y, z;
@@ -548,7 +551,7 @@ __global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la,
       int8_t* dst = oz.res + (static_cast<size_t>(ci) * C.nm + t) * lplane +
                     static_cast<size_t>(row) * NP + x * OZ_TN;
 #pragma unroll 1
-      for (int cb = 0; cb < OZ_TN; cb += 32) {
+      for (int cb = half * (OZ_TN / 2); cb < (half + 1) * (OZ_TN / 2); cb += 32) {
         uint32_t v[32];
         const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc_i * OZ_TN + cb;
         asm volatile(
