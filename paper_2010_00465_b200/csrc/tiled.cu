@@ -973,6 +973,8 @@ static TiledWs carve(void* ws, int64_t batch, int n) {
   return w;
 }
 
+// The persistent int8 GEMM (default) or, with CSM_OZ_GEMM=tile, the one-CTA-
+// per-tile form (experiments); read once per process.
 static bool persistent_layout() {
   static const bool p = [] {
     const char* e = std::getenv("CSM_OZ_GEMM");
@@ -1054,12 +1056,8 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
     cfg.blockDim = dim3(tk::OZ_THREADS);
     cfg.dynamicSmemBytes = gsm;
     cfg.stream = stream;
-    static const bool persistent = [] {  // CSM_OZ_GEMM=tile: one CTA per tile
-      const char* e = std::getenv("CSM_OZ_GEMM");
-      return !(e && std::strcmp(e, "tile") == 0);
-    }();
     prof_begin(stream, 2);  // csm_profile_enable(2): the int8 GEMM alone
-    if (persistent) {
+    if (persistent_layout()) {
       const int pair_tiles = (NP / tk::OZ_TN) * (M / (2 * tk::OZ_TM)) * cnt * C.nm;
       int clusters = oz_resident_clusters();
       if (clusters > pair_tiles) clusters = pair_tiles;
