@@ -432,7 +432,7 @@ __device__ __forceinline__ void put(const EpiArgs<TOut>& E, int q, int rg, int c
 
 template <int CL, typename TOut>
 __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const Acc& acc,
-                                         const Acc& acc2, Acc& keep, const Lane<CL>& ln) {
+                                         Acc& acc2, Acc& keep, const Lane<CL>& ln) {
   constexpr int NP = Geo<CL>::NP;
   const double* x = dTables.x8;  // x[0] = x1
   const double* z8 = dTables.z8;
@@ -526,17 +526,29 @@ __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const 
       FOR_PAIRS(put<NP>(E, 0, rg, c, off, E.scale * (keep[P][0] + p0), E.scale * (keep[P][1] + p1));)
       break;
     case E_DEG12B:
+      // y3 is only a term of the next two epilogues, never a product
+      // operand: it stays in this thread's acc2 registers (the non-dual
+      // products in between leave acc2 alone) instead of a shared slot
       FOR_PAIRS({
           const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
+#ifdef CSM_Y3_SMEM
           put<NP>(E, 0, rg, c, off, p0, p1);
+#else
+          acc2[P][0] = p0;
+          acc2[P][1] = p1;
+#endif
           put<NP>(E, 1, rg, c, off, fma(a[3][3], p0, fma(a[3][2], y2.x, fma(a[3][1], y.x, a[3][0] * I0))),
               fma(a[3][3], p1, fma(a[3][2], y2.y, fma(a[3][1], y.y, a[3][0] * I1))));
         })
       break;
     case E_DEG12C:
       FOR_PAIRS({
-          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off),
-                        y3 = ld2(E.in[2], off);
+          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
+#ifdef CSM_Y3_SMEM
+          const double2 y3 = ld2(E.in[2], off);
+#else
+          const double2 y3 = make_double2(acc2[P][0], acc2[P][1]);
+#endif
           const double m0 = fma(a[2][3], y3.x, fma(a[2][2], y2.x, fma(a[2][1], y.x, a[2][0] * I0))) + p0;
           const double m1 = fma(a[2][3], y3.y, fma(a[2][2], y2.y, fma(a[2][1], y.y, a[2][0] * I1))) + p1;
           const double l0 = fma(a[1][3], y3.x, fma(a[1][2], y2.x, fma(a[1][1], y.x, a[1][0] * I0))) + m0;
@@ -548,7 +560,12 @@ __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const 
     case E_DEG12D:
       FOR_PAIRS({
           const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off),
-                        y3 = ld2(E.in[2], off), md = ld2(E.in[3], off);
+                        md = ld2(E.in[3], off);
+#ifdef CSM_Y3_SMEM
+          const double2 y3 = ld2(E.in[2], off);
+#else
+          const double2 y3 = make_double2(acc2[P][0], acc2[P][1]);
+#endif
           const double c0 = fma(a[0][3], y3.x, fma(a[0][2], y2.x, fma(a[0][1], y.x, a[0][0] * I0))) + p0;
           const double c1 = fma(a[0][3], y3.y, fma(a[0][2], y2.y, fma(a[0][1], y.y, a[0][0] * I1))) + p1;
           const double n0 = fma(z[11], c0, fma(z[10], md.x, fma(z[9], y3.x, fma(z[8], y2.x, fma(z[7], y.x, z[6] * I0)))));
