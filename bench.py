@@ -547,11 +547,11 @@ INT8_PEAK_TOPS = 4500.0
 
 def ozaki_applies(n):
     """The Ozaki engine runs a call when NP % 256 == 0 and it is selected
-    (or auto and NP >= 1024)."""
+    (or auto and NP >= 768)."""
     import paper_2010_00465_b200 as csm
     np_ = (n + 63) // 64 * 64
     eng = csm.get_engine()
-    return n > 128 and np_ % 256 == 0 and (eng == "ozaki" or (eng == "auto" and np_ >= 1024))
+    return n > 128 and np_ % 256 == 0 and (eng == "ozaki" or (eng == "auto" and np_ >= 768))
 
 
 def ozaki_roofline(int8_ops_step, gemm_ms, fp64_tflops, dmma_peak):
@@ -591,7 +591,7 @@ def main():
     ap.add_argument("--engine", choices=["auto", "dmma", "ozaki"], default="auto",
                     help="product engine of the tiled chain (n > 128) and the cfg5 slab "
                          "products: FP64 DMMA, Ozaki-II on the int8 tensor cores, or auto "
-                         "(the library default: Ozaki from padded order 1024 up)")
+                         "(the library default: Ozaki from padded order 768 up)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warm-up raised to 3 (timing rule)")

@@ -255,7 +255,7 @@ int csm_graph_safe(int dtype, int64_t batch, int n);
  * tcgen05 int8 GEMM per modulus (16 moduli for float64 results, 9 for
  * float32), Chinese-remainder reconstruction fused with the op's epilogue --
  * whenever the padded order is a multiple of 256 (DMMA otherwise).
- * CSM_ENGINE_AUTO (default): Ozaki for padded orders >= 1024 that are
+ * CSM_ENGINE_AUTO (default): Ozaki for padded orders >= 768 that are
  * multiples of 256, where it is faster; DMMA below.  The chain, (k, s) and
  * the reference interface are unchanged (the products of matcore.py:90-97
  * are computed differently).  csm_workspace_size depends on the engine:

@@ -569,7 +569,7 @@ def set_engine(name: str) -> None:
     block-row chain, process-wide (csm_set_engine): "dmma" (FP64 DMMA),
     "ozaki" (Ozaki-II: exact int8 tensor-core GEMMs per modulus + CRT, for
     padded orders that are multiples of 256) or "auto" (default: Ozaki from
-    padded order 1024 up, DMMA below).  Size workspaces (BatchPlan) after
+    padded order 768 up, DMMA below).  Size workspaces (BatchPlan) after
     changing it."""
     if name not in _ENGINES:
         raise ValueError(f"engine must be one of {sorted(_ENGINES)}")

@@ -845,16 +845,16 @@ size_t tiled_np(int n) { return static_cast<size_t>((n + 63) / 64) * 64; }
 
 // Product engine (process-wide, csm_set_engine): 0 = FP64 DMMA, 1 = Ozaki-II
 // on the int8 tensor cores (ozaki.cuh) for the tiled chain when NP % 256 == 0.
-// 2 = auto (default): Ozaki from NP = 1024 up, where its O(n^2 nm) passes
-// are small enough next to the GEMM (batched n = 1024: 1.23x the DMMA chain,
-// n = 2048: 2.06x, cfg5 8192^2: 3.6x; smaller n is faster on DMMA,
-// DESIGN.md K7).
+// 2 = auto (default): Ozaki from NP = 768 up, where its O(n^2 nm) passes
+// are small enough next to the GEMM (batched n = 768: 1.06x the DMMA chain,
+// n = 1024: 1.3x, n = 2048: 2.1x, cfg5 8192^2: 3.8x; n <= 512 is faster on
+// DMMA, K7).
 static int g_engine = 2;
 void set_engine(int e) { g_engine = e; }
 int engine() { return g_engine; }
 static bool oz_applies(int NP) {
   if (NP % tk::OZ_TN != 0) return false;
-  return g_engine == 1 || (g_engine == 2 && NP >= 1024);
+  return g_engine == 1 || (g_engine == 2 && NP >= 768);
 }
 // moduli: pairwise coprime, <= 256, largest first
 static const int kOzMods[tk::OZ_MAXM] = {256, 255, 253, 251, 247, 241, 239, 233,

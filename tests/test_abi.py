@@ -83,7 +83,7 @@ def test_engine_switch_without_device():
     Ozaki engine enlarges the tiled workspace (n = 256) but not n = 64 or
     the DMMA-only orders (NP % 256 != 0)."""
     lib = _lib.lib()
-    assert lib.csm_get_engine() == 2  # auto: Ozaki from padded order 1024 up
+    assert lib.csm_get_engine() == 2  # auto: Ozaki from padded order 768 up
     assert lib.csm_workspace_size(0, 1, 4096) > 9 * 4096 * 4096 * 8 + 16 * 3 * 4096 * 4096
     assert lib.csm_set_engine(5) == _lib.ERR_ARG
     assert lib.csm_set_engine(0) == 0

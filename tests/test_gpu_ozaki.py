@@ -194,7 +194,7 @@ def test_pade_and_standalone_sines(ozaki):
 
 
 def test_auto_engine_picks_by_size(cuda):
-    """auto (the default): DMMA below padded order 1024 -- bit-identical to
+    """auto (the default): DMMA below padded order 768 -- bit-identical to
     the forced DMMA engine."""
     csm.set_engine("auto")
     assert csm.get_engine() == "auto"
