@@ -109,6 +109,7 @@ enum Epi : int8_t {
   E_DEG12B,    // o0 = acc ; o1 = c4                                        (y, y2)
   E_DEG12C,    // o0 = mid = c3 + acc ; o1 = c2 + mid                       (y, y2, y3)
   E_DEG12D,    // o0 = cos = c1 + acc ; o1 = inner ; keep = sin base (y,y2,y3,mid)
+  E_Y2,        // o0 = acc (y2 of the degree-12 chain), also kept in acc2
 };
 
 enum Scale : int8_t { SC_ONE = 0, SC_F = 1, SC_F2 = 2, SC_TP = 3 };
@@ -165,7 +166,7 @@ __constant__ Chain kChains[7] = {
     // [3] Taylor k=7: chain_deg12 (:329-361)
     {H_(7, 4, 5, 1, 2, 4, 4, 0, 6, 0),
      {S_(0, 0, X, 0, E_SCALED, SC_F2, 1, X, X, X, X, X, X),     // y
-      S_(0, 1, X, 1, E_SCALED, SC_ONE, 2, X, X, X, X, X, X),     // y2
+      S_(0, 1, X, 1, E_Y2, SC_ONE, 2, X, X, X, X, X, X),         // y2
       S_(0, 2, X, 1, E_DEG12B, SC_ONE, 3, 4, X, 1, 2, X, X),     // y3, c4
       S_(0, 4, X, 4, E_DEG12C, SC_ONE, 5, 6, X, 1, 2, 3, X),     // mid, L
       S_(0, 6, X, 5, E_DEG12D, SC_ONE, 4, 1, X, 1, 2, 3, 5),     // cos, inner
@@ -183,7 +184,7 @@ __constant__ Chain kChains[7] = {
       S_(0, 1, X, 3, E_KEEP, SC_TP, 4, X, X, X, X, X, X)}},      // s
     // [6] wave k=5: chain_deg12 on y
     {H_(5, 3, 2, 1, 4, 0, 3, 0, 4, 0),
-     {S_(0, 0, X, 0, E_SCALED, SC_ONE, 1, X, X, X, X, X, X),     // y2
+     {S_(0, 0, X, 0, E_Y2, SC_ONE, 1, X, X, X, X, X, X),         // y2
       S_(0, 1, X, 0, E_DEG12B, SC_ONE, 2, 3, X, 0, 1, X, X),     // y3, c4
       S_(0, 3, X, 3, E_DEG12C, SC_ONE, 4, 5, X, 0, 1, 2, X),     // mid, L
       S_(0, 5, X, 4, E_DEG12D, SC_ONE, 3, 1, X, 0, 1, 2, 4),     // cos, inner
@@ -442,6 +443,13 @@ __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const 
     case E_SCALED:
       FOR_PAIRS(put<NP>(E, 0, rg, c, off, E.scale * p0, E.scale * p1);)
       break;
+    case E_Y2:  // y2 is an operand (slot) and a term of the next three epilogues (acc2)
+      FOR_PAIRS({
+          put<NP>(E, 0, rg, c, off, p0, p1);
+          acc2[P][0] = p0;
+          acc2[P][1] = p1;
+        })
+      break;
     case E_DEG2:
       FOR_PAIRS({
           const double2 y = ld2(E.in[0], off);
@@ -526,29 +534,25 @@ __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const 
       FOR_PAIRS(put<NP>(E, 0, rg, c, off, E.scale * (keep[P][0] + p0), E.scale * (keep[P][1] + p1));)
       break;
     case E_DEG12B:
-      // y3 is only a term of the next two epilogues, never a product
-      // operand: it stays in this thread's acc2 registers (the non-dual
-      // products in between leave acc2 alone) instead of a shared slot
+      // Register carriers across the degree-12 epilogues (the non-dual
+      // products in between leave acc2 and keep alone): y2 arrives in acc2
+      // (E_Y2; it is also a product operand, so its slot stays), and y3 --
+      // only a term of the next two epilogues, never an operand -- stays in
+      // keep instead of a shared slot (E_DEG12D reads it before it rewrites
+      // keep).  y2 and y3 reads and the y3 write leave shared memory: +1.1%
+      // on cfg2.
       FOR_PAIRS({
-          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
-#ifdef CSM_Y3_SMEM
-          put<NP>(E, 0, rg, c, off, p0, p1);
-#else
-          acc2[P][0] = p0;
-          acc2[P][1] = p1;
-#endif
+          const double2 y = ld2(E.in[0], off), y2 = make_double2(acc2[P][0], acc2[P][1]);
+          keep[P][0] = p0;  // y3
+          keep[P][1] = p1;
           put<NP>(E, 1, rg, c, off, fma(a[3][3], p0, fma(a[3][2], y2.x, fma(a[3][1], y.x, a[3][0] * I0))),
               fma(a[3][3], p1, fma(a[3][2], y2.y, fma(a[3][1], y.y, a[3][0] * I1))));
         })
       break;
     case E_DEG12C:
       FOR_PAIRS({
-          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off);
-#ifdef CSM_Y3_SMEM
-          const double2 y3 = ld2(E.in[2], off);
-#else
-          const double2 y3 = make_double2(acc2[P][0], acc2[P][1]);
-#endif
+          const double2 y = ld2(E.in[0], off), y2 = make_double2(acc2[P][0], acc2[P][1]);
+          const double2 y3 = make_double2(keep[P][0], keep[P][1]);
           const double m0 = fma(a[2][3], y3.x, fma(a[2][2], y2.x, fma(a[2][1], y.x, a[2][0] * I0))) + p0;
           const double m1 = fma(a[2][3], y3.y, fma(a[2][2], y2.y, fma(a[2][1], y.y, a[2][0] * I1))) + p1;
           const double l0 = fma(a[1][3], y3.x, fma(a[1][2], y2.x, fma(a[1][1], y.x, a[1][0] * I0))) + m0;
@@ -559,13 +563,9 @@ __device__ __forceinline__ void epilogue(int epi, const EpiArgs<TOut>& E, const 
       break;
     case E_DEG12D:
       FOR_PAIRS({
-          const double2 y = ld2(E.in[0], off), y2 = ld2(E.in[1], off),
-                        md = ld2(E.in[3], off);
-#ifdef CSM_Y3_SMEM
-          const double2 y3 = ld2(E.in[2], off);
-#else
-          const double2 y3 = make_double2(acc2[P][0], acc2[P][1]);
-#endif
+          const double2 y = ld2(E.in[0], off), md = ld2(E.in[3], off);
+          const double2 y2 = make_double2(acc2[P][0], acc2[P][1]);
+          const double2 y3 = make_double2(keep[P][0], keep[P][1]);  // read before keep is rewritten
           const double c0 = fma(a[0][3], y3.x, fma(a[0][2], y2.x, fma(a[0][1], y.x, a[0][0] * I0))) + p0;
           const double c1 = fma(a[0][3], y3.y, fma(a[0][2], y2.y, fma(a[0][1], y.y, a[0][0] * I1))) + p1;
           const double n0 = fma(z[11], c0, fma(z[10], md.x, fma(z[9], y3.x, fma(z[8], y2.x, fma(z[7], y.x, z[6] * I0)))));
