@@ -8,6 +8,7 @@ fused shared-memory kernel.  One step = one pass of the whole pipeline
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config cfg2|cfg1|cfg3|cfg4|cfg5|sweep64..1024]
+                  [--engine auto|dmma|ozaki] [--dist-mode gather|peer]
 
 N > 1 runs under torchrun, one rank per GPU: every rank owns its own
 16384-matrix shard (weak scaling, no collective on the data path); the step
