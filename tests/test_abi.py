@@ -100,3 +100,20 @@ def test_engine_switch_without_device():
         assert lib.csm_slab_engine_bytes(512, 1024) >= 16 * (2 * 512 * 1024 + 1024 * 1024)
     finally:
         assert lib.csm_set_engine(2) == 0
+
+
+def test_slab_op_pair_argument_errors_without_device():
+    """csm_slab_op_pair runs a doubling step: dbl_step < 0 and bad shapes are
+    CSM_ERR_ARG before any device work."""
+    lib = _lib.lib()
+    op = ctypes.create_string_buffer(int(lib.csm_op_bytes()))
+    dummy = ctypes.c_void_p(16)
+    rc = lib.csm_slab_op_pair(op, op, dummy, 64, 128, 0, dummy, dummy, 0, 0.0, -1,
+                              dummy, dummy, 0, dummy, None)
+    assert rc == _lib.ERR_ARG and "doubling" in _lib.last_error()
+    rc = lib.csm_slab_op_pair(op, op, dummy, 60, 128, 0, dummy, dummy, 0, 0.0, 0,
+                              dummy, dummy, 0, dummy, None)
+    assert rc == _lib.ERR_ARG
+    rc = lib.csm_slab_op_pair(None, op, dummy, 64, 128, 0, dummy, dummy, 0, 0.0, 0,
+                              dummy, dummy, 0, dummy, None)
+    assert rc == _lib.ERR_ARG
