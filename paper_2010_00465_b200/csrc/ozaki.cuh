@@ -199,7 +199,8 @@ __device__ __forceinline__ void oz_store_residues(const double (&v)[16], const O
     for (int t = 3 * g; t < 3 * g + 3 && t < NM; ++t) {
       int b[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) b[i] = oz_mod_small(x[i], C, t);
+      for (int i = 0; i < 16; ++i)  // m_0 = 256 divides G_0: its residue is the low byte
+        b[i] = t == 0 ? static_cast<int>(x[i] & 255u) : oz_mod_small(x[i], C, t);
       *reinterpret_cast<uint4*>(out + t * plane) = oz_pack16(b);
     }
   }
