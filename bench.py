@@ -552,7 +552,7 @@ def ozaki_applies(n):
     import paper_2010_00465_b200 as csm
     np_ = (n + 63) // 64 * 64
     eng = csm.get_engine()
-    return n > 128 and np_ % 256 == 0 and (eng == "ozaki" or (eng == "auto" and np_ >= 768))
+    return n > 128 and np_ % 256 == 0 and (eng.startswith("ozaki") or (eng == "auto" and np_ >= 768))
 
 
 def ozaki_roofline(int8_ops_step, gemm_ms, fp64_tflops, dmma_peak):

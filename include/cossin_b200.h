@@ -206,9 +206,11 @@ int csm_theta_table(int family, int precision, double* theta_cos,
  *     input rows (slot 0 alias), s / tp = the matrix's s and t', dbl_step =
  *     -1 for chain ops or the doubling index; outputs that are final are
  *     also written to cos_out / sin_out (the caller's M x NP rows).
- *     scratch: device buffer of csm_slab_scratch_bytes()
+ *     scratch: device buffer of scratch_bytes >= csm_slab_scratch_bytes()
  *     + csm_slab_engine_bytes(M, NP) (the latter is the Ozaki engine's
- *     scratch, 0 under the DMMA engine; csm_slab_op_peer always runs DMMA). */
+ *     scratch for the calling thread's engine, 0 under the DMMA engine;
+ *     csm_slab_op_peer always runs DMMA and needs only the former).  A
+ *     smaller scratch_bytes returns CSM_ERR_WORKSPACE, never overflows. */
 #define CSM_SLAB_SLOTS 9
 size_t csm_op_bytes(void);
 size_t csm_slab_scratch_bytes(void);
@@ -220,14 +222,14 @@ int csm_doubling_program(int c0, int s0, int c1, int s1, void* ops_out);
 int csm_slab_op(const void* op, double* slab, int M, int NP, int row0,
                 const double* rhs_full, const double* in0, int s, double tp,
                 int dbl_step, void* cos_out, void* sin_out, int out_f32,
-                void* scratch, void* stream);
+                void* scratch, size_t scratch_bytes, void* stream);
 /* csm_slab_op_pair: the doubling step's two ops (csm_doubling_program: S C
  * and C C, both with right operand C = rhs_full) in one launch; on the
  * Ozaki engine C is converted once for both (dbl_step >= 0 required). */
 int csm_slab_op_pair(const void* op_a, const void* op_b, double* slab, int M, int NP,
                      int row0, const double* rhs_full, const double* in0, int s,
                      double tp, int dbl_step, void* cos_out, void* sin_out,
-                     int out_f32, void* scratch, void* stream);
+                     int out_f32, void* scratch, size_t scratch_bytes, void* stream);
 /* Fused all-gather + product: like csm_slab_op, but the right operand is
  * NOT gathered -- rhs_slabs (HOST array of nparts pointers) holds each
  * rank's slab base, peer pointers over NVLink (e.g. from torch symmetric
@@ -240,7 +242,7 @@ int csm_slab_op_peer(const void* op, double* slab, int M, int NP, int row0,
                      const double* const* rhs_slabs, int nparts,
                      const double* in0, int s, double tp, int dbl_step,
                      void* cos_out, void* sin_out, int out_f32, void* scratch,
-                     void* stream);
+                     size_t scratch_bytes, void* stream);
 
 /* 1 when csm_cos_sin / csm_wave for (dtype, batch, n) never synchronises
  * the host (K1, or K1c without the side chain), so the call can be
@@ -249,23 +251,35 @@ int csm_slab_op_peer(const void* op, double* slab, int M, int NP, int row0,
 int csm_graph_safe(int dtype, int64_t batch, int n);
 
 /* Product engine of the tiled chain (n > 128; also the Pade and standalone
- * sine calls) and of csm_slab_op, process-wide.  CSM_ENGINE_DMMA: FP64 DMMA
- * (mma.sync m8n8k4).  CSM_ENGINE_OZAKI: each product exactly on integers by
- * the Ozaki-II scheme -- rows / columns scaled to P-bit integers, one
- * tcgen05 int8 GEMM per modulus (16 moduli for float64 results, 9 for
- * float32), Chinese-remainder reconstruction fused with the op's epilogue --
- * whenever the padded order is a multiple of 256 (DMMA otherwise).
+ * sine calls) and of csm_slab_op.  CSM_ENGINE_DMMA: FP64 DMMA (mma.sync
+ * m8n8k4).  CSM_ENGINE_OZAKI: each product exactly on integers by the
+ * Ozaki-II scheme -- rows / columns scaled to P-bit integers, one tcgen05
+ * int8 GEMM per modulus (16 moduli for float64 results, 9 for float32),
+ * Chinese-remainder reconstruction fused with the op's epilogue -- whenever
+ * the padded order is a multiple of 256 (DMMA otherwise).  Every Ozaki
+ * product is checked by an a-priori error bound: when the rounding of the
+ * operands to P bits relative to their row / column maxima could exceed
+ * the fp64 GEMM bound (n u ||C||_1), that product is recomputed on DMMA
+ * (badly scaled operands), so the result is never less accurate than the
+ * bound of the reference's fp64 product (matcore.py:97).
  * CSM_ENGINE_AUTO (default): Ozaki for padded orders >= 768 that are
  * multiples of 256, where it is faster; DMMA below.  The chain, (k, s) and
- * the reference interface are unchanged (the products of matcore.py:90-97
- * are computed differently).  csm_workspace_size depends on the engine:
- * size workspaces after setting it.  Returns CSM_ERR_ARG for an unknown
- * engine. */
+ * the reference interface are unchanged.
+ *   csm_set_engine: the process default (atomic).
+ *   csm_set_thread_engine: an override for the calling thread (-1 clears).
+ * Each call reads the engine once; workspace sizes (csm_workspace_size,
+ * csm_slab_engine_bytes, ...) depend on it, and a call whose workspace is
+ * too small for its engine returns CSM_ERR_WORKSPACE.  Returns CSM_ERR_ARG
+ * for an unknown engine. */
 #define CSM_ENGINE_DMMA 0
 #define CSM_ENGINE_OZAKI 1
 #define CSM_ENGINE_AUTO 2
+/* Experiments and tests only: the Ozaki engine WITHOUT the accuracy guard
+ * (shows what the guard prevents on badly scaled operands). */
+#define CSM_ENGINE_OZAKI_UNGUARDED 3
 int csm_set_engine(int engine);
 int csm_get_engine(void);
+int csm_set_thread_engine(int engine);
 
 /* ---- Measurement helpers (not part of the reference surface) ------------
  * csm_fp64_peak: time a DMMA (mma.sync m8n8k4 f64) throughput loop on the

@@ -11,6 +11,7 @@ from .api import (
     BatchReport,
     cos_sin,
     cos_sin_batched,
+    engine_scope,
     get_engine,
     set_engine,
     identity,
@@ -74,6 +75,7 @@ __all__ = [
     "WaveResult",
     "cos_sin",
     "cos_sin_batched",
+    "engine_scope",
     "get_engine",
     "set_engine",
     "identity",

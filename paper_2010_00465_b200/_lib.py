@@ -62,14 +62,15 @@ SIGNATURES = {
     "csm_chain_program": (_i32, [_i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp, _vp]),
     "csm_doubling_program": (_i32, [_i32, _i32, _i32, _i32, _vp]),
     "csm_slab_op": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _dp, _i32, _vp, _vp,
-                           _i32, _vp, _vp]),
+                           _i32, _vp, _sz, _vp]),
     "csm_slab_op_peer": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _dp, _i32,
-                                _vp, _vp, _i32, _vp, _vp]),
+                                _vp, _vp, _i32, _vp, _sz, _vp]),
     "csm_slab_op_pair": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _dp, _i32,
-                                _vp, _vp, _i32, _vp, _vp]),
+                                _vp, _vp, _i32, _vp, _sz, _vp]),
     "csm_graph_safe": (_i32, [_i32, _i64, _i32]),
     "csm_set_engine": (_i32, [_i32]),
     "csm_get_engine": (_i32, []),
+    "csm_set_thread_engine": (_i32, [_i32]),
     "csm_profile_enable": (_i32, [_i32]),
     "csm_profile_collect": (_i32, [_vp, _vp]),
 }

@@ -18,7 +18,9 @@ result comes from the CUDA library; there is no CPU fallback.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import threading
 from dataclasses import dataclass
 from fractions import Fraction
 from typing import Any, Sequence
@@ -561,7 +563,7 @@ def write_matrix(path: str, a) -> None:
             fh.write(" ".join(repr(float(v)) for v in row) + "\n")
 
 
-_ENGINES = {"dmma": 0, "ozaki": 1, "auto": 2}
+_ENGINES = {"dmma": 0, "ozaki": 1, "auto": 2, "ozaki-unguarded": 3}
 
 
 def set_engine(name: str) -> None:
@@ -577,12 +579,39 @@ def set_engine(name: str) -> None:
 
 
 def get_engine() -> str:
+    """The engine calls on this thread run with (a thread override from
+    engine_scope, else the process default)."""
     code = int(_lib.lib().csm_get_engine())
     return {v: k for k, v in _ENGINES.items()}[code]
 
 
+_TLS = threading.local()
+
+
+@contextlib.contextmanager
+def engine_scope(name: str):
+    """Run the calls of this thread inside the block on `name`
+    (csm_set_thread_engine), leaving the process default and other threads
+    untouched; scopes nest.  Workspaces sized inside the block match the
+    calls made in it."""
+    if name not in _ENGINES:
+        raise ValueError(f"engine must be one of {sorted(_ENGINES)}")
+    L = _lib.lib()
+    stack = getattr(_TLS, "engines", None)
+    if stack is None:
+        stack = _TLS.engines = []
+    stack.append(_ENGINES[name])
+    _lib.check(L.csm_set_thread_engine(_ENGINES[name]), "csm_set_thread_engine")
+    try:
+        yield
+    finally:
+        stack.pop()
+        _lib.check(L.csm_set_thread_engine(stack[-1] if stack else -1),
+                   "csm_set_thread_engine")
+
+
 __all__ = [
-    "BatchReport", "cos_sin", "get_engine", "set_engine", "cos_sin_batched", "identity",
+    "BatchReport", "cos_sin", "engine_scope", "get_engine", "set_engine", "cos_sin_batched", "identity",
     "pade_cos_sin", "pade_cos_sin_batched",
     "matrix_from_rows", "norm1", "read_matrix", "select_batch",
     "select_scheme", "taylor_cos_sin", "taylor_sin9", "wave_cos_sin",

@@ -36,8 +36,9 @@ size_t schedule_ws_bytes();
 cudaError_t launch_schedule(const int32_t* K, const int32_t* S, const int32_t* status,
                             int64_t batch, int* bins, int32_t* order, cudaStream_t stream,
                             int64_t* launches);
-size_t tiled_workspace_bytes(int64_t batch, int n);
+size_t tiled_workspace_bytes(int64_t batch, int n, int eng);
 void set_engine(int e);
+void set_thread_engine(int e);
 int engine();
 int k1c_resident_sms();
 size_t op_bytes();
@@ -45,15 +46,15 @@ int chain_program(bool wave, int k, bool fold, void* ops_out, int max_ops, int32
                   int max_steps, int32_t* cos_slot, int32_t* sin_slot);
 void doubling_program(int c0, int s0, int c1, int s1, void* ops_out);
 size_t slab_scratch_bytes();
-size_t slab_engine_bytes(int M, int NP);
+size_t slab_engine_bytes(int M, int NP, int eng);
 cudaError_t slab_op(const void* const* op_host, int nops, double* slab, int M, int NP, int row0,
                     const double* rhs_full, const double* in0, int s, double tp, int dbl_step,
                     void* cout, void* sout, int out_f32, void* scratch, cudaStream_t stream,
-                    int64_t* launches, const double* const* parts_host, int nparts);
+                    int64_t* launches, const double* const* parts_host, int nparts, int eng);
 cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void* c_out,
                       void* s_out, int64_t batch, int n, const int32_t* dK, const int32_t* dS,
                       const int32_t* dStatus, void* ws, cudaStream_t stream, int64_t* launches,
-                      int special);
+                      int special, int eng);
 size_t ddref_workspace_doubles(int64_t batch, int n);
 void ddref_series_consts(double* out28);
 cudaError_t dd_matmul(const double* xh, const double* xl, const double* yh, const double* yl,
@@ -155,13 +156,20 @@ int check_device() {
   return CSM_SUCCESS;
 }
 
-int check_common(int dtype, int64_t batch, int n, size_t ws_bytes) {
+size_t workspace_size(int64_t batch, int n, int eng) {
+  if (batch < 0 || n < 0) return 0;
+  size_t bytes = common_bytes(batch);
+  if (n > 64) bytes += csm::tiled_workspace_bytes(batch, n, eng) + 256;
+  return bytes;
+}
+
+int check_common(int dtype, int64_t batch, int n, size_t ws_bytes, int eng) {
   if (dtype != CSM_F64 && dtype != CSM_F32 && dtype != CSM_F32_IN_F64_OUT)
     return fail(CSM_ERR_ARG, "dtype must be CSM_F64, CSM_F32 or CSM_F32_IN_F64_OUT");
   if (batch < 0 || n < 0) return fail(CSM_ERR_ARG, "batch and n must be nonnegative");
   if (batch > (int64_t(1) << 31) - 1) return fail(CSM_ERR_ARG, "batch too large");
-  if (ws_bytes < csm_workspace_size(dtype, batch, n))
-    return fail(CSM_ERR_WORKSPACE, "workspace smaller than csm_workspace_size()");
+  if (ws_bytes < workspace_size(batch, n, eng))
+    return fail(CSM_ERR_WORKSPACE, "workspace smaller than csm_workspace_size() for this call's engine");
   return CSM_SUCCESS;
 }
 
@@ -205,7 +213,7 @@ cudaStream_t side_stream() {
 // After K/S/status are on the device: run K1/K1c or the tiled chain.
 int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, void* s,
                 int64_t batch, int n, const int32_t* K, const int32_t* S, const int32_t* st,
-                const CommonWs& w, cudaStream_t stream) {
+                const CommonWs& w, cudaStream_t stream, int eng) {
   if (n == 0 || batch == 0) return CSM_SUCCESS;
   cudaError_t e;
   if (n <= fused_max()) {
@@ -241,7 +249,7 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
       e = csm::run_tiled(dtype, wave, static_cast<const char*>(a) + bf * nn * in_elt,
                          t ? t + bf : nullptr, static_cast<char*>(c) + bf * nn * out_elt,
                          static_cast<char*>(s) + bf * nn * out_elt, batch - bf, n, K + bf, S + bf,
-                         st + bf, w.tiled, side, &g_launches, 0);
+                         st + bf, w.tiled, side, &g_launches, 0, eng);
       g_prof_hold = false;
       if (e != cudaSuccess) return cuda_fail(e, "side tiled chain");
       cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
@@ -251,7 +259,7 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
     csm::prof_end(stream);
   } else {
     e = csm::run_tiled(dtype, wave, a, t, c, s, batch, n, K, S, st, w.tiled, stream, &g_launches,
-                       0);
+                       0, eng);
     if (e != cudaSuccess) return cuda_fail(e, "tiled chain");
   }
   return CSM_SUCCESS;
@@ -261,7 +269,8 @@ int pipeline(int dtype, int precision, bool wave, const void* a, const double* t
              void* s, int64_t batch, int n, int32_t* k, int32_t* sx, int32_t* status, void* ws,
              size_t ws_bytes, void* stream_v) {
   g_launches = 0;
-  int rc = check_common(dtype, batch, n, ws_bytes);
+  const int eng = csm::engine();  // one engine for the whole call
+  int rc = check_common(dtype, batch, n, ws_bytes, eng);
   if (rc) return rc;
   if (precision != CSM_PREC_DOUBLE && precision != CSM_PREC_SINGLE)
     return fail(CSM_ERR_ARG, "precision must be CSM_PREC_DOUBLE or CSM_PREC_SINGLE");
@@ -283,13 +292,14 @@ int pipeline(int dtype, int precision, bool wave, const void* a, const double* t
                          stream);
   if (e != cudaSuccess) return cuda_fail(e, "select kernel");
   ++g_launches;
-  return run_compute(dtype, wave, a, t, c, s, batch, n, k, sx, status, w, stream);
+  return run_compute(dtype, wave, a, t, c, s, batch, n, k, sx, status, w, stream, eng);
 }
 
 int core(int dtype, bool wave, int kval, const void* a, const double* t, void* c, void* s,
          int64_t batch, int n, int32_t* status, void* ws, size_t ws_bytes, void* stream_v) {
   g_launches = 0;
-  int rc = check_common(dtype, batch, n, ws_bytes);
+  const int eng = csm::engine();
+  int rc = check_common(dtype, batch, n, ws_bytes, eng);
   if (rc) return rc;
   const bool ok = wave ? (kval == 3 || kval == 4 || kval == 5)
                        : (kval == 3 || kval == 4 || kval == 6 || kval == 7);
@@ -303,7 +313,7 @@ int core(int dtype, bool wave, int kval, const void* a, const double* t, void* c
   cudaError_t e = csm::launch_fill_ks(w.kbuf, w.sbuf, status, batch, kval, stream);
   if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
   ++g_launches;
-  return run_compute(dtype, wave, a, t, c, s, batch, n, w.kbuf, w.sbuf, status, w, stream);
+  return run_compute(dtype, wave, a, t, c, s, batch, n, w.kbuf, w.sbuf, status, w, stream, eng);
 }
 
 // ---- FP64 DMMA peak probe --------------------------------------------------
@@ -334,10 +344,7 @@ int64_t csm_last_launch_count(void) { return g_launches; }
 
 size_t csm_workspace_size(int dtype, int64_t batch, int n) {
   (void)dtype;
-  if (batch < 0 || n < 0) return 0;
-  size_t bytes = common_bytes(batch);
-  if (n > 64) bytes += csm::tiled_workspace_bytes(batch, n) + 256;
-  return bytes;
+  return workspace_size(batch, n, csm::engine());
 }
 
 int csm_norm1(int dtype, const void* a, int64_t batch, int n, double* norms, int32_t* status,
@@ -536,41 +543,55 @@ int csm_doubling_program(int c0, int s0, int c1, int s1, void* ops_out) {
 
 size_t csm_slab_engine_bytes(int M, int NP) {
   if (M <= 0 || NP <= 0) return 0;
-  return csm::slab_engine_bytes(M, NP);
+  return csm::slab_engine_bytes(M, NP, csm::engine());
+}
+
+// Shared checks of the slab entry points; on success *eng is the call's
+// engine snapshot (peer products always run DMMA and need no engine bytes).
+static int slab_checks(const double* slab, int M, int NP, int row0, const void* scratch,
+                       size_t scratch_bytes, bool peer, int* eng) {
+  if (!slab || !scratch) return fail(CSM_ERR_ARG, "null pointer argument");
+  if (M <= 0 || NP <= 0 || M % 64 || NP % 64 || row0 < 0 || row0 + M > NP)
+    return fail(CSM_ERR_ARG, "slab shape must be M x NP with M, NP multiples of 64");
+  *eng = csm::engine();
+  const size_t need = csm::slab_scratch_bytes() + (peer ? 0 : csm::slab_engine_bytes(M, NP, *eng));
+  if (scratch_bytes < need)
+    return fail(CSM_ERR_WORKSPACE,
+                "scratch smaller than csm_slab_scratch_bytes() + csm_slab_engine_bytes(M, NP) "
+                "for this call's engine");
+  return check_device();
 }
 
 int csm_slab_op(const void* op, double* slab, int M, int NP, int row0, const double* rhs_full,
                 const double* in0, int s, double tp, int dbl_step, void* cos_out, void* sin_out,
-                int out_f32, void* scratch, void* stream) {
+                int out_f32, void* scratch, size_t scratch_bytes, void* stream) {
   g_launches = 0;
-  if (!op || !slab || !rhs_full || !scratch) return fail(CSM_ERR_ARG, "null pointer argument");
-  if (M <= 0 || NP <= 0 || M % 64 || NP % 64 || row0 < 0 || row0 + M > NP)
-    return fail(CSM_ERR_ARG, "slab shape must be M x NP with M, NP multiples of 64");
-  int rc = check_device();
+  if (!op || !rhs_full) return fail(CSM_ERR_ARG, "null pointer argument");
+  int eng = 0;
+  int rc = slab_checks(slab, M, NP, row0, scratch, scratch_bytes, false, &eng);
   if (rc) return rc;
   const void* ops[1] = {op};
   cudaError_t e = csm::slab_op(ops, 1, slab, M, NP, row0, rhs_full, in0, s, tp, dbl_step,
                                cos_out, sin_out, out_f32, scratch,
-                               static_cast<cudaStream_t>(stream), &g_launches, nullptr, 0);
+                               static_cast<cudaStream_t>(stream), &g_launches, nullptr, 0, eng);
   if (e != cudaSuccess) return cuda_fail(e, "slab op");
   return CSM_SUCCESS;
 }
 
 int csm_slab_op_pair(const void* op_a, const void* op_b, double* slab, int M, int NP, int row0,
                      const double* rhs_full, const double* in0, int s, double tp, int dbl_step,
-                     void* cos_out, void* sin_out, int out_f32, void* scratch, void* stream) {
+                     void* cos_out, void* sin_out, int out_f32, void* scratch,
+                     size_t scratch_bytes, void* stream) {
   g_launches = 0;
-  if (!op_a || !op_b || !slab || !rhs_full || !scratch)
-    return fail(CSM_ERR_ARG, "null pointer argument");
-  if (M <= 0 || NP <= 0 || M % 64 || NP % 64 || row0 < 0 || row0 + M > NP)
-    return fail(CSM_ERR_ARG, "slab shape must be M x NP with M, NP multiples of 64");
+  if (!op_a || !op_b || !rhs_full) return fail(CSM_ERR_ARG, "null pointer argument");
   if (dbl_step < 0) return fail(CSM_ERR_ARG, "csm_slab_op_pair runs a doubling step (dbl_step >= 0)");
-  int rc = check_device();
+  int eng = 0;
+  int rc = slab_checks(slab, M, NP, row0, scratch, scratch_bytes, false, &eng);
   if (rc) return rc;
   const void* ops[2] = {op_a, op_b};
   cudaError_t e = csm::slab_op(ops, 2, slab, M, NP, row0, rhs_full, in0, s, tp, dbl_step,
                                cos_out, sin_out, out_f32, scratch,
-                               static_cast<cudaStream_t>(stream), &g_launches, nullptr, 0);
+                               static_cast<cudaStream_t>(stream), &g_launches, nullptr, 0, eng);
   if (e != cudaSuccess) return cuda_fail(e, "slab op pair");
   return CSM_SUCCESS;
 }
@@ -578,19 +599,20 @@ int csm_slab_op_pair(const void* op_a, const void* op_b, double* slab, int M, in
 int csm_slab_op_peer(const void* op, double* slab, int M, int NP, int row0,
                      const double* const* rhs_slabs, int nparts, const double* in0, int s,
                      double tp, int dbl_step, void* cos_out, void* sin_out, int out_f32,
-                     void* scratch, void* stream) {
+                     void* scratch, size_t scratch_bytes, void* stream) {
   g_launches = 0;
-  if (!op || !slab || !rhs_slabs || !scratch) return fail(CSM_ERR_ARG, "null pointer argument");
-  if (M <= 0 || NP <= 0 || M % 64 || NP % 64 || nparts <= 0 || nparts > 64 || nparts * M != NP)
+  if (!op || !rhs_slabs) return fail(CSM_ERR_ARG, "null pointer argument");
+  if (nparts <= 0 || nparts > 64 || nparts * M != NP)
     return fail(CSM_ERR_ARG, "need M, NP multiples of 64 and nparts * M == NP (<= 64 parts)");
   for (int i = 0; i < nparts; ++i)
     if (!rhs_slabs[i]) return fail(CSM_ERR_ARG, "null peer slab");
-  int rc = check_device();
+  int eng = 0;
+  int rc = slab_checks(slab, M, NP, row0, scratch, scratch_bytes, true, &eng);
   if (rc) return rc;
   const void* ops[1] = {op};
   cudaError_t e = csm::slab_op(ops, 1, slab, M, NP, row0, nullptr, in0, s, tp, dbl_step, cos_out,
                                sin_out, out_f32, scratch, static_cast<cudaStream_t>(stream),
-                               &g_launches, rhs_slabs, nparts);
+                               &g_launches, rhs_slabs, nparts, CSM_ENGINE_DMMA);
   if (e != cudaSuccess) return cuda_fail(e, "peer slab op");
   return CSM_SUCCESS;
 }
@@ -598,7 +620,7 @@ int csm_slab_op_peer(const void* op, double* slab, int M, int NP, int row0,
 size_t csm_sine_workspace_size(int dtype, int64_t batch, int n) {
   (void)dtype;
   if (batch < 0 || n < 0) return 0;
-  return common_bytes(batch) + csm::tiled_workspace_bytes(batch, n) + 256;
+  return common_bytes(batch) + csm::tiled_workspace_bytes(batch, n, csm::engine()) + 256;
 }
 
 static int standalone_sine(int dtype, bool wave, const void* a, const double* t, void* s_out,
@@ -608,7 +630,8 @@ static int standalone_sine(int dtype, bool wave, const void* a, const double* t,
   if (dtype != CSM_F64 && dtype != CSM_F32 && dtype != CSM_F32_IN_F64_OUT)
     return fail(CSM_ERR_ARG, "bad dtype");
   if (batch < 0 || n < 0) return fail(CSM_ERR_ARG, "batch and n must be nonnegative");
-  if (ws_bytes < csm_sine_workspace_size(dtype, batch, n))
+  const int eng = csm::engine();
+  if (ws_bytes < common_bytes(batch) + csm::tiled_workspace_bytes(batch, n, eng) + 256)
     return fail(CSM_ERR_WORKSPACE, "workspace smaller than csm_sine_workspace_size()");
   if (batch == 0 || n == 0) return CSM_SUCCESS;
   if (!a || !s_out || !status || !ws || (wave && !t)) return fail(CSM_ERR_ARG, "null pointer argument");
@@ -620,7 +643,7 @@ static int standalone_sine(int dtype, bool wave, const void* a, const double* t,
   if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
   ++g_launches;
   e = csm::run_tiled(dtype, wave, a, t, nullptr, s_out, batch, n, w.kbuf, w.sbuf, status, w.tiled,
-                     stream, &g_launches, wave ? 2 : 1);
+                     stream, &g_launches, wave ? 2 : 1, eng);
   if (e != cudaSuccess) return cuda_fail(e, "standalone sine");
   return CSM_SUCCESS;
 }
@@ -733,7 +756,7 @@ int csm_ddref_cos_sin(const double* a, double* cos_out, double* sin_out, int64_t
 size_t csm_pade_workspace_size(int dtype, int64_t batch, int n) {
   (void)dtype;
   if (batch < 0 || n < 0) return 0;
-  return common_bytes(batch) + csm::tiled_workspace_bytes(batch, n) + 256;
+  return common_bytes(batch) + csm::tiled_workspace_bytes(batch, n, csm::engine()) + 256;
 }
 
 int csm_pade_cos_sin(int dtype, int precision, const void* a, void* cos_out, void* sin_out,
@@ -745,7 +768,8 @@ int csm_pade_cos_sin(int dtype, int precision, const void* a, void* cos_out, voi
   if (precision != CSM_PREC_DOUBLE && precision != CSM_PREC_SINGLE)
     return fail(CSM_ERR_ARG, "bad precision");
   if (batch < 0 || n < 0) return fail(CSM_ERR_ARG, "batch and n must be nonnegative");
-  if (ws_bytes < csm_pade_workspace_size(dtype, batch, n))
+  const int eng = csm::engine();
+  if (ws_bytes < common_bytes(batch) + csm::tiled_workspace_bytes(batch, n, eng) + 256)
     return fail(CSM_ERR_WORKSPACE, "workspace smaller than csm_pade_workspace_size()");
   if (batch == 0) return CSM_SUCCESS;
   if (!k || !sx || !status || !ws || (n > 0 && (!a || !cos_out || !sin_out)))
@@ -768,7 +792,7 @@ int csm_pade_cos_sin(int dtype, int precision, const void* a, void* cos_out, voi
   ++g_launches;
   if (n == 0) return CSM_SUCCESS;
   e = csm::run_tiled(dtype, false, a, nullptr, cos_out, sin_out, batch, n, k, sx, status, w.tiled,
-                     stream, &g_launches, 3);
+                     stream, &g_launches, 3, eng);
   if (e != cudaSuccess) return cuda_fail(e, "pade chain");
   return CSM_SUCCESS;
 }
@@ -804,13 +828,22 @@ int csm_profile_collect(double* total_ms, int64_t* intervals) {
 }
 
 int csm_set_engine(int engine) {
-  if (engine != CSM_ENGINE_DMMA && engine != CSM_ENGINE_OZAKI && engine != CSM_ENGINE_AUTO)
+  if (engine != CSM_ENGINE_DMMA && engine != CSM_ENGINE_OZAKI && engine != CSM_ENGINE_AUTO &&
+      engine != CSM_ENGINE_OZAKI_UNGUARDED)
     return fail(CSM_ERR_ARG, "engine must be CSM_ENGINE_DMMA, CSM_ENGINE_OZAKI or CSM_ENGINE_AUTO");
   csm::set_engine(engine);
   return CSM_SUCCESS;
 }
 
 int csm_get_engine(void) { return csm::engine(); }
+
+int csm_set_thread_engine(int engine) {
+  if (engine != -1 && engine != CSM_ENGINE_DMMA && engine != CSM_ENGINE_OZAKI &&
+      engine != CSM_ENGINE_AUTO && engine != CSM_ENGINE_OZAKI_UNGUARDED)
+    return fail(CSM_ERR_ARG, "thread engine must be -1 (none) or a CSM_ENGINE_* value");
+  csm::set_thread_engine(engine);
+  return CSM_SUCCESS;
+}
 
 int csm_fp64_peak(int iters, double* tflops, void* stream_v) {
   if (!tflops || iters <= 0) return fail(CSM_ERR_ARG, "bad arguments");

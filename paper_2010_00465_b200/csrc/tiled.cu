@@ -25,6 +25,7 @@
 // (trig / wave use), driver.py:91-98 (doubling), driver.py:115/:139
 // (scaling), matcore.py:107-121 (linear combinations, fused here).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -110,6 +111,10 @@ struct LaunchArgs {
   // NVLink); the product streams its rows straight from the owner, tile by
   // tile, instead of reading an all-gathered copy.  Null otherwise.
   const double* const* rhs_parts;
+  // Ozaki accuracy fallback: when set, only items whose flag is nonzero run
+  // (flag index = item - only_base); the others leave at once.
+  const unsigned* only;
+  int only_base;
 };
 
 // Slot sl of matrix b (slot 0 may alias the caller's input).
@@ -249,6 +254,7 @@ __global__ void __launch_bounds__(THREADS, CSM_TILED_MINB) gemm_epi_kernel(const
   double* Bs = sm + STAGES * A_STAGE;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int item = static_cast<int>(blockIdx.y) + args.item_base;
+  if (args.only && args.only[item - args.only_base] == 0u) return;  // not a fallback item
   Seg sg = args.seg[0];
 #pragma unroll
   for (int i = 1; i < MAXSEG; ++i)
@@ -843,22 +849,30 @@ void free_pair(int c0, int s0, int* c1, int* s1) {
 
 size_t tiled_np(int n) { return static_cast<size_t>((n + 63) / 64) * 64; }
 
-// Product engine (process-wide, csm_set_engine): 0 = FP64 DMMA, 1 = Ozaki-II
-// on the int8 tensor cores (ozaki.cuh) for the tiled chain when NP % 256 == 0.
-// 2 = auto (default): Ozaki from NP = 768 up, where its O(n^2 nm) passes
-// are small enough next to the GEMM (batched n = 768: 1.06x the DMMA chain,
-// n = 1024: 1.3x, n = 2048: 2.1x, cfg5 8192^2: 3.8x; n <= 512 is faster on
-// DMMA, K7).
-static int g_engine = 2;
-void set_engine(int e) { g_engine = e; }
-int engine() { return g_engine; }
-static bool oz_applies(int NP) {
+// Product engine: 0 = FP64 DMMA, 1 = Ozaki-II on the int8 tensor cores
+// (ozaki.cuh) for the tiled chain when NP % 256 == 0, 2 = auto (default):
+// Ozaki from NP = 768 up, where its O(n^2 nm) passes are small enough next
+// to the GEMM (batched n = 768: 1.06x the DMMA chain, n = 1024: 1.3x,
+// n = 2048: 2.1x, cfg5 8192^2: 3.8x; n <= 512 is faster on DMMA, DESIGN.md
+// K7).  The process default (csm_set_engine) is atomic; a thread may
+// override it (csm_set_thread_engine).  Every entry point reads the engine
+// ONCE (engine()) and passes that snapshot down, so a call never mixes
+// engines and its workspace check matches what it runs.
+static std::atomic<int> g_engine{2};
+static thread_local int t_engine = -1;
+void set_engine(int e) { g_engine.store(e, std::memory_order_relaxed); }
+void set_thread_engine(int e) { t_engine = e; }
+int engine() { return t_engine >= 0 ? t_engine : g_engine.load(std::memory_order_relaxed); }
+static bool oz_applies(int NP, int eng) {
   if (NP % tk::OZ_TN != 0) return false;
-  return g_engine == 1 || (g_engine == 2 && NP >= 768);
+  return eng == 1 || eng == 3 || (eng == 2 && NP >= 768);
 }
 // moduli: pairwise coprime, <= 256, largest first
-static const int kOzMods[tk::OZ_MAXM] = {256, 255, 253, 251, 247, 241, 239, 233,
-                                        229, 227, 223, 217, 211, 199, 197, 193};
+static constexpr int kOzMods[tk::OZ_MAXM] = {256, 255, 253, 251, 247, 241, 239, 233,
+                                            229, 227, 223, 217, 211, 199, 197, 193};
+// oz_store_residues takes modulus 0's residue as the low byte of its group's
+// residue: valid only while m_0 = 256 and m_0 opens group 0
+static_assert(kOzMods[0] == 256, "the mod-256 shortcut of oz_store_residues needs m_0 = 256");
 int oz_moduli(int out_f32) { return out_f32 ? 9 : 16; }
 
 // CRT constants for the first nm moduli and contraction depth K.
@@ -906,11 +920,36 @@ tk::OzConst oz_const(int nm, int K) {
   return C;
 }
 
-// Ozaki scratch per product item (M = NP rows): row / column maxima, the
-// residue planes of both operands and of the product.
-static size_t oz_item_bytes(size_t NP) {
-  return 2 * NP * sizeof(unsigned long long) + 3 * tk::OZ_MAXM * NP * NP + 256 + 8;
+// Ozaki scratch, carved from `base` (nullptr: only measure).  nL items own
+// an M-row left operand and product, nR items a right operand's maxima and
+// column sums, nRp items the right operand's residue planes (a doubling
+// pair shares one).  Returns the bytes used; the one function sizes and
+// carves, so the two cannot disagree.
+static size_t oz_carve(char* base, int64_t nL, int64_t nR, int64_t nRp, size_t M, size_t NP,
+                       tk::OzArgs* out) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    off = (off + 255) & ~size_t(255);
+    char* p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  };
+  const size_t l = static_cast<size_t>(nL), r = static_cast<size_t>(nR);
+  tk::OzArgs O{};
+  O.mxL = reinterpret_cast<unsigned long long*>(take(l * M * 8));
+  O.rsumL = reinterpret_cast<double*>(take(l * M * 8));
+  O.mxR = reinterpret_cast<unsigned long long*>(take(r * NP * 8));
+  O.csumR = reinterpret_cast<double*>(take(r * (NP / 64) * NP * 8));
+  O.csumC = reinterpret_cast<double*>(take(l * (M / 64) * NP * 8));
+  O.bad = reinterpret_cast<unsigned*>(take(std::max(l, r) * 4));
+  O.flag = reinterpret_cast<unsigned*>(take(l * 4));
+  O.pL = reinterpret_cast<int8_t*>(take(l * tk::OZ_MAXM * M * NP));
+  O.pR = reinterpret_cast<int8_t*>(take(static_cast<size_t>(nRp) * tk::OZ_MAXM * NP * NP));
+  O.res = reinterpret_cast<int8_t*>(take(l * tk::OZ_MAXM * M * NP));
+  if (out) *out = O;
+  return off + 256;
 }
+static size_t oz_item_bytes(size_t NP) { return oz_carve(nullptr, 1, 1, 1, NP, NP, nullptr); }
 static int64_t oz_cap_items(int64_t batch, size_t NP) {
   const size_t budget = static_cast<size_t>(4) << 30;
   int64_t cap = static_cast<int64_t>(budget / oz_item_bytes(NP));
@@ -918,15 +957,17 @@ static int64_t oz_cap_items(int64_t batch, size_t NP) {
   return std::min<int64_t>(cap, 65535 / tk::OZ_MAXM);
 }
 
-size_t tiled_workspace_bytes(int64_t batch, int n) {
+size_t tiled_workspace_bytes(int64_t batch, int n, int eng) {
   const size_t NP = tiled_np(n);
   size_t bytes = 0;
   bytes += static_cast<size_t>(batch) * tk::NSLOT * NP * NP * sizeof(double);  // slots
   bytes += static_cast<size_t>(batch) * sizeof(double);                        // tsc
   bytes += static_cast<size_t>(batch) * 2 * sizeof(int32_t) + 256;             // idx
   bytes += 128 * sizeof(Op) + 256;                                             // op table
-  if (oz_applies(static_cast<int>(NP)))
-    bytes += static_cast<size_t>(oz_cap_items(batch, NP)) * oz_item_bytes(NP) + 1024;
+  if (oz_applies(static_cast<int>(NP), eng)) {
+    const int64_t cap = oz_cap_items(batch, NP);
+    bytes += oz_carve(nullptr, cap, cap, cap, NP, NP, nullptr) + 256;
+  }
   return bytes;
 }
 
@@ -935,11 +976,11 @@ struct TiledWs {
   double* tsc;
   int32_t* idx;
   Op* ops;
-  tk::OzArgs oz;  // Ozaki scratch (engine 1 only)
+  tk::OzArgs oz;  // Ozaki scratch (when the engine runs it)
   int64_t oz_cap;
 };
 
-static TiledWs carve(void* ws, int64_t batch, int n) {
+static TiledWs carve(void* ws, int64_t batch, int n, int eng) {
   const size_t NP = tiled_np(n);
   char* p = static_cast<char*>(ws);
   TiledWs w{};
@@ -953,22 +994,11 @@ static TiledWs carve(void* ws, int64_t batch, int n) {
   p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
   w.ops = reinterpret_cast<Op*>(p);
   p += 128 * sizeof(Op) + 256;
-  if (oz_applies(static_cast<int>(NP))) {
+  if (oz_applies(static_cast<int>(NP), eng)) {
     const int64_t cap = oz_cap_items(batch, NP);
     p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
     w.oz_cap = cap;
-    w.oz.mxL = reinterpret_cast<unsigned long long*>(p);
-    p += static_cast<size_t>(cap) * NP * 8;
-    w.oz.mxR = reinterpret_cast<unsigned long long*>(p);
-    p += static_cast<size_t>(cap) * NP * 8;
-    w.oz.bad = reinterpret_cast<unsigned*>(p);
-    p += static_cast<size_t>(cap) * 8;
-    p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
-    w.oz.pL = reinterpret_cast<int8_t*>(p);
-    p += static_cast<size_t>(cap) * tk::OZ_MAXM * NP * NP;
-    w.oz.pR = reinterpret_cast<int8_t*>(p);
-    p += static_cast<size_t>(cap) * tk::OZ_MAXM * NP * NP;
-    w.oz.res = reinterpret_cast<int8_t*>(p);
+    oz_carve(p, cap, cap, cap, NP, NP, &w.oz);
   }
   return w;
 }
@@ -1012,9 +1042,14 @@ static int oz_resident_clusters() {
 
 // One tiled launch (all items of plan A) through the Ozaki engine, in
 // chunks of at most cap items: maxima, residues, nm int8 GEMMs, CRT +
-// epilogue.  Seven launches per chunk.
+// epilogue, then the accuracy guard (oz_guard) and the DMMA rerun of the
+// items it flags (the CTAs of unflagged items leave at once).  An op's
+// outputs never alias its operands or epilogue sources (build_program; the
+// tile-parallel kernels rely on that too), so the rerun rewrites exactly
+// what the CRT epilogue wrote.  Eight launches per chunk.
 static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scratch, int64_t cap,
-                                 const tk::OzConst& C, cudaStream_t stream, int64_t* launches) {
+                                 const tk::OzConst& C, cudaStream_t stream, int64_t* launches,
+                                 bool guard) {
   const int NP = A.NP, M = A.M;
   const unsigned tiles = static_cast<unsigned>((M / tk::BM) * (NP / tk::BN));
   for (int done = 0; done < A.total; done += static_cast<int>(cap)) {
@@ -1075,6 +1110,16 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
       tk::oz_crt_epi<16><<<gcrt, tk::THREADS, tk::OZ_CRT_SMEM, stream>>>(A, O, C);
     else
       tk::oz_crt_epi<9><<<gcrt, tk::THREADS, tk::OZ_CRT_SMEM, stream>>>(A, O, C);
+    if (guard) {
+      tk::oz_guard<<<cnt, 256, 0, stream>>>(A, O, C);
+      tk::LaunchArgs R = A;  // DMMA rerun of the flagged items only
+      R.item_base = done;
+      R.only = O.flag;
+      R.only_base = done;
+      tk::gemm_epi_kernel<<<dim3(tiles, static_cast<unsigned>(cnt), 1), tk::THREADS, tk::SMEM,
+                            stream>>>(R);
+      *launches += 2;
+    }
     *launches += 6;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
@@ -1086,11 +1131,11 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
 cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void* c_out,
                       void* s_out, int64_t batch, int n, const int32_t* dK,
                       const int32_t* dS, const int32_t* dStatus, void* ws,
-                      cudaStream_t stream, int64_t* launches, int special) {
+                      cudaStream_t stream, int64_t* launches, int special, int eng) {
   cudaError_t e;
   const int NP = static_cast<int>(tiled_np(n));
   const size_t mat_stride = static_cast<size_t>(tk::NSLOT) * NP * NP;
-  TiledWs w = carve(ws, batch, n);
+  TiledWs w = carve(ws, batch, n, eng);
   std::vector<int32_t> hk(batch), hs(batch), hst(batch);
   e = cudaMemcpyAsync(hk.data(), dK, batch * 4, cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(hs.data(), dS, batch * 4, cudaMemcpyDeviceToHost, stream);
@@ -1243,7 +1288,7 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     A.row0 = 0;
     A.rhs_full = nullptr;
     A.rhs_parts = nullptr;
-    const bool use_oz = oz_applies(NP);
+    const bool use_oz = oz_applies(NP, eng);
     const tk::OzConst ozc = use_oz ? oz_const(oz_moduli(out_f32), NP) : tk::OzConst{};
     size_t lu_smem = 0;
     if (pade && NP == 64) {  // den + both right-hand sides staged in shared memory
@@ -1270,7 +1315,8 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
       for (size_t i = 0; i < L.seg.size(); ++i) A.seg[i] = L.seg[i];
       A.total = L.total;
       if (use_oz) {
-        if ((e = run_oz_launch(A, w.oz, w.oz_cap, ozc, stream, launches)) != cudaSuccess) return e;
+        if ((e = run_oz_launch(A, w.oz, w.oz_cap, ozc, stream, launches, eng != 3)) != cudaSuccess)
+          return e;
         continue;
       }
       for (int done = 0; done < L.total; done += 65535) {
@@ -1347,13 +1393,14 @@ size_t slab_scratch_bytes() { return 2 * sizeof(Op) + 64 + kMaxParts * sizeof(do
 
 // Extra slab scratch the Ozaki engine needs for an M x NP slab (0 when the
 // DMMA engine runs it).
-static bool oz_slab_applies(int M, int NP) { return oz_applies(NP) && M % (2 * tk::OZ_TM) == 0; }
+static bool oz_slab_applies(int M, int NP, int eng) {
+  return oz_applies(NP, eng) && M % (2 * tk::OZ_TM) == 0;
+}
 // Sized for csm_slab_op_pair: two left operands and products, one right
-// operand (the pair shares it).
-size_t slab_engine_bytes(int M, int NP) {
-  if (!oz_slab_applies(M, NP)) return 0;
-  const size_t m = static_cast<size_t>(M), np = static_cast<size_t>(NP);
-  return 2 * (m + np) * 8 + 16 + tk::OZ_MAXM * (4 * m * np + np * np) + 6 * 256;
+// operand's residue planes (the pair shares it).
+size_t slab_engine_bytes(int M, int NP, int eng) {
+  if (!oz_slab_applies(M, NP, eng)) return 0;
+  return oz_carve(nullptr, 2, 2, 1, static_cast<size_t>(M), static_cast<size_t>(NP), nullptr) + 256;
 }
 
 // Run one Op on a block-row slab: out rows = L_rows * rhs_full (+ epilogue).
@@ -1364,7 +1411,7 @@ size_t slab_engine_bytes(int M, int NP) {
 cudaError_t slab_op(const void* const* op_host, int nops, double* slab, int M, int NP, int row0,
                     const double* rhs_full, const double* in0, int s, double tp, int dbl_step,
                     void* cout, void* sout, int out_f32, void* scratch, cudaStream_t stream,
-                    int64_t* launches, const double* const* parts_host, int nparts) {
+                    int64_t* launches, const double* const* parts_host, int nparts, int eng) {
   if (M % tk::BM != 0 || NP % tk::BN != 0) return cudaErrorInvalidValue;
   if (nparts < 0 || nparts > kMaxParts || (nparts > 0 && nparts * M != NP))
     return cudaErrorInvalidValue;
@@ -1411,25 +1458,12 @@ cudaError_t slab_op(const void* const* op_host, int nops, double* slab, int M, i
   A.rhs_parts = nparts > 0 ? d->parts : nullptr;
   A.M = M;
   A.row0 = row0;
-  if (nparts == 0 && oz_slab_applies(M, NP)) {  // Ozaki engine (gathered right operand)
-    auto align = [](char* p) {
-      return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
-    };
-    char* p = align(static_cast<char*>(scratch) + slab_scratch_bytes());
-    const size_t m = static_cast<size_t>(M), np = static_cast<size_t>(NP);
+  if (nparts == 0 && oz_slab_applies(M, NP, eng)) {  // Ozaki engine (gathered right operand)
+    char* p = reinterpret_cast<char*>(
+        (reinterpret_cast<uintptr_t>(scratch) + slab_scratch_bytes() + 255) & ~uintptr_t(255));
     tk::OzArgs O{};  // two items' L-side scratch; the pair's right operand once
-    O.mxL = reinterpret_cast<unsigned long long*>(p);
-    p = align(p + 2 * m * 8);
-    O.mxR = reinterpret_cast<unsigned long long*>(p);
-    p = align(p + 2 * np * 8);
-    O.bad = reinterpret_cast<unsigned*>(p);
-    p = align(p + 16);
-    O.pL = reinterpret_cast<int8_t*>(p);
-    p = align(p + 2 * tk::OZ_MAXM * m * np);
-    O.pR = reinterpret_cast<int8_t*>(p);
-    p = align(p + tk::OZ_MAXM * np * np);
-    O.res = reinterpret_cast<int8_t*>(p);
-    return run_oz_launch(A, O, nops, oz_const(oz_moduli(out_f32), NP), stream, launches);
+    oz_carve(p, 2, 2, 1, static_cast<size_t>(M), static_cast<size_t>(NP), &O);
+    return run_oz_launch(A, O, nops, oz_const(oz_moduli(out_f32), NP), stream, launches, eng != 3);
   }
   dim3 grid(static_cast<unsigned>((M / tk::BM) * (NP / tk::BN)), static_cast<unsigned>(nops), 1);
   tk::gemm_epi_kernel<<<grid, tk::THREADS, tk::SMEM, stream>>>(A);

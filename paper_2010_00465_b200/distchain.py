@@ -105,7 +105,7 @@ def _device_slab_op(op: OpView, slab, M, n, row0, rhs_full, in0, s, dbl_step,
     _lib.check(_lib.lib().csm_slab_op(
         raw, vp(slab.data_ptr()), M, n, row0, vp(rhs_full.data_ptr()),
         vp(in0.data_ptr()), s, 0.0, dbl_step, vp(cos_rows.data_ptr()),
-        vp(sin_rows.data_ptr()), 0, vp(scratch.data_ptr()),
+        vp(sin_rows.data_ptr()), 0, vp(scratch.data_ptr()), scratch.numel(),
         vp(int((stream or torch.cuda.current_stream()).cuda_stream))), "csm_slab_op")
     return int(_lib.lib().csm_last_launch_count())
 
@@ -120,7 +120,7 @@ def _device_slab_op_pair(ops, slab, M, n, row0, rhs_full, in0, s, dbl_step, cos_
     _lib.check(_lib.lib().csm_slab_op_pair(
         raw[0], raw[1], vp(slab.data_ptr()), M, n, row0, vp(rhs_full.data_ptr()),
         vp(in0.data_ptr()), s, 0.0, dbl_step, vp(cos_rows.data_ptr()),
-        vp(sin_rows.data_ptr()), 0, vp(scratch.data_ptr()),
+        vp(sin_rows.data_ptr()), 0, vp(scratch.data_ptr()), scratch.numel(),
         vp(int((stream or torch.cuda.current_stream()).cuda_stream))), "csm_slab_op_pair")
     return int(_lib.lib().csm_last_launch_count())
 
@@ -143,9 +143,26 @@ def _device_slab_op_peer(op: OpView, slab, M, n, row0, rhs_slabs, in0, s, dbl_st
     _lib.check(_lib.lib().csm_slab_op_peer(
         raw, vp(slab.data_ptr()), M, n, row0, parts, len(rhs_slabs), vp(in0.data_ptr()), s,
         0.0, dbl_step, vp(cos_rows.data_ptr()), vp(sin_rows.data_ptr()), 0,
-        vp(scratch.data_ptr()),
+        vp(scratch.data_ptr()), scratch.numel(),
         vp(int((stream or torch.cuda.current_stream()).cuda_stream))), "csm_slab_op_peer")
     return int(_lib.lib().csm_last_launch_count())
+
+
+def _slab_scratch_size(M: int, n: int) -> int:
+    """Scratch bytes of the slab calls under the calling thread's engine
+    (the library checks the size it is given and fails rather than
+    overflowing)."""
+    L = _lib.lib()
+    return int(L.csm_slab_scratch_bytes()) + int(L.csm_slab_engine_bytes(M, n))
+
+
+def _peer_engine():
+    """Peer mode runs every product on the DMMA engine: csm_slab_op_peer is
+    DMMA-only, and the products whose right operand is the replicated A (run
+    through csm_slab_op) take the same engine, so one chain never mixes
+    engines."""
+    from .api import engine_scope
+    return engine_scope("dmma")
 
 
 slab_op = _device_slab_op
@@ -188,8 +205,7 @@ def cos_sin_distributed(a, precision: Precision = Precision.DOUBLE, *,
     scratch = None
     if dev.type == "cuda":  # + the Ozaki engine's scratch when it runs the products
         L = _lib.lib()
-        scratch = torch.empty(int(L.csm_slab_scratch_bytes()) + int(L.csm_slab_engine_bytes(M, n)),
-                              dtype=torch.uint8, device=dev)
+        scratch = torch.empty(_slab_scratch_size(M, n), dtype=torch.uint8, device=dev)
     in0 = a[row0:row0 + M]
     cache: dict[int, object] = {}
     stats = DistStats(k, s, 0, 0)
@@ -306,21 +322,22 @@ def cos_sin_virtual_ranks(a, world: int, precision: Precision = Precision.DOUBLE
     slabs = [torch.empty((NSLOT, M, n), dtype=torch.float64, device=dev) for _ in range(world)]
     cos = torch.empty((n, n), dtype=torch.float64, device=dev)
     sin = torch.empty_like(cos)
-    scratch = None
-    if dev.type == "cuda":
-        scratch = torch.empty(int(_lib.lib().csm_slab_scratch_bytes()), dtype=torch.uint8,
-                              device=dev)
     stats = DistStats(k, s, 0, 0)
-    gens = [_peer_rank_program(a, precision, r, world, slabs[r], slabs,
-                               cos[r * M:(r + 1) * M], sin[r * M:(r + 1) * M], scratch, stats)
-            for r in range(world)]
-    done = False
-    while not done:
-        for g in gens:  # one step of every rank, then the (implicit) barrier
-            try:
-                next(g)
-            except StopIteration:
-                done = True
+    with _peer_engine():
+        scratch = None
+        if dev.type == "cuda":
+            scratch = torch.empty(_slab_scratch_size(M, n), dtype=torch.uint8, device=dev)
+        gens = [_peer_rank_program(a, precision, r, world, slabs[r], slabs,
+                                   cos[r * M:(r + 1) * M], sin[r * M:(r + 1) * M], scratch,
+                                   stats)
+                for r in range(world)]
+        done = False
+        while not done:
+            for g in gens:  # one step of every rank, then the (implicit) barrier
+                try:
+                    next(g)
+                except StopIteration:
+                    done = True
     return cos, sin, stats
 
 
@@ -354,9 +371,9 @@ def cos_sin_distributed_peer(a, precision: Precision = Precision.DOUBLE, *, grou
     if ctx is None:  # symmetric slabs are allocated and mapped once per shape
         slab = symm_mem.empty((NSLOT, M, n), dtype=torch.float64, device=dev)
         hdl = symm_mem.rendezvous(slab, grp.group_name)
-        ctx = (slab, hdl, [int(p) for p in hdl.buffer_ptrs],
-               torch.empty(int(_lib.lib().csm_slab_scratch_bytes()), dtype=torch.uint8,
-                           device=dev))
+        with _peer_engine():
+            scratch = torch.empty(_slab_scratch_size(M, n), dtype=torch.uint8, device=dev)
+        ctx = (slab, hdl, [int(p) for p in hdl.buffer_ptrs], scratch)
         _PEER_CTX[key] = ctx
         hdl.barrier(channel=0)  # every peer mapping is live
     slab, hdl, ptrs, scratch = ctx
@@ -364,9 +381,10 @@ def cos_sin_distributed_peer(a, precision: Precision = Precision.DOUBLE, *, grou
     sin_rows = torch.empty_like(cos_rows)
     stats = DistStats(k, s, 0, 0)
     hdl.barrier(channel=0)  # no rank still reads the previous call's slabs
-    for _ in _peer_rank_program(a, precision, rank, world, slab, ptrs, cos_rows, sin_rows,
-                                scratch, stats):
-        hdl.barrier(channel=0)  # this step's rows are written on every rank
+    with _peer_engine():
+        for _ in _peer_rank_program(a, precision, rank, world, slab, ptrs, cos_rows, sin_rows,
+                                    scratch, stats):
+            hdl.barrier(channel=0)  # this step's rows are written on every rank
     if not gather_outputs or world == 1:
         return cos_rows, sin_rows, stats
     cfull = torch.empty((n, n), dtype=torch.float64, device=dev)

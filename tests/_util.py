@@ -62,3 +62,62 @@ def laplacian_wave(rng, count, n):
     a = lap[None, :, :] + v[:, :, None] * np.eye(n)[None, :, :]
     t = 10.0 ** rng.uniform(-4.0, -1.0, count)
     return a, t
+
+
+# ---------------------------------------------------------------------------
+# Badly scaled test matrices for the Ozaki engine's accuracy guard.  The four
+# structured families restate the reference gallery's definitions
+# (/root/reference/pkg/src/cossinm/gallery.py: _frank :68-74, _lehmer
+# :110-112, _grcar :127-131, _pascal_lower :143-149), rescaled to a target
+# 1-norm the way generate_corpus does (_rescaled, gallery.py:182-183).
+
+def gallery_pascal_lower(n):
+    m = np.zeros((n, n))
+    m[:, 0] = 1.0
+    for i in range(1, n):
+        m[i, 1:i + 1] = m[i - 1, 0:i] + m[i - 1, 1:i + 1]
+    return m
+
+
+def gallery_frank(n):
+    i, j = np.indices((n, n))
+    return np.where(j >= i - 1, n - np.maximum(i, j), 0).astype(np.float64)
+
+
+def gallery_lehmer(n):
+    i, j = np.indices((n, n)) + 1
+    return np.minimum(i, j) / np.maximum(i, j)
+
+
+def gallery_grcar(n):
+    m = -np.eye(n, k=-1)
+    for k in range(4):
+        m += np.eye(n, k=k)
+    return m
+
+
+def graded(rng, n, spread):
+    """D B D^-1 with D = diag(logspace(0, log10 spread)) and B ~ N(0,1):
+    rows and columns graded over `spread` (entries span spread^2)."""
+    d = np.logspace(0.0, np.log10(spread), n)
+    return (d[:, None] * rng.standard_normal((n, n))) / d[None, :]
+
+
+def rescaled(m, target):
+    """gallery._rescaled: m * (target / norm1(m))."""
+    return m * (target / np.abs(m).sum(axis=0).max())
+
+
+def permuted_noise(fn, a, rng):
+    """The reference's own noise floor for input `a`: run the
+    oracle `fn` (returning (cos, sin, ...)) on P a P^T and undo P -- the
+    same matrix function with every GEMM summed in a different order.
+    Returns (outputs of fn(a), max relative 1-norm distance of the pair)."""
+    out = fn(a)
+    perm = rng.permutation(a.shape[-1])
+    inv = np.argsort(perm)
+    outp = fn(a[np.ix_(perm, perm)])
+    noise = 0.0
+    for x, xp in zip(out[:2], outp[:2]):
+        noise = max(noise, rel1(xp[np.ix_(inv, inv)], x))
+    return out, noise

@@ -6,6 +6,7 @@ import re
 
 import pytest
 
+import paper_2010_00465_b200 as csm
 from paper_2010_00465_b200 import _lib
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -109,11 +110,52 @@ def test_slab_op_pair_argument_errors_without_device():
     op = ctypes.create_string_buffer(int(lib.csm_op_bytes()))
     dummy = ctypes.c_void_p(16)
     rc = lib.csm_slab_op_pair(op, op, dummy, 64, 128, 0, dummy, dummy, 0, 0.0, -1,
-                              dummy, dummy, 0, dummy, None)
+                              dummy, dummy, 0, dummy, 1 << 40, None)
     assert rc == _lib.ERR_ARG and "doubling" in _lib.last_error()
     rc = lib.csm_slab_op_pair(op, op, dummy, 60, 128, 0, dummy, dummy, 0, 0.0, 0,
-                              dummy, dummy, 0, dummy, None)
+                              dummy, dummy, 0, dummy, 1 << 40, None)
     assert rc == _lib.ERR_ARG
     rc = lib.csm_slab_op_pair(None, op, dummy, 64, 128, 0, dummy, dummy, 0, 0.0, 0,
-                              dummy, dummy, 0, dummy, None)
+                              dummy, dummy, 0, dummy, 1 << 40, None)
     assert rc == _lib.ERR_ARG
+
+
+def test_slab_scratch_size_is_checked_without_device():
+    """The slab calls take the scratch size and refuse a buffer smaller than
+    csm_slab_scratch_bytes() + csm_slab_engine_bytes(M, NP) of the call's
+    engine (CSM_ERR_WORKSPACE) before touching the device."""
+    lib = _lib.lib()
+    op = ctypes.create_string_buffer(int(lib.csm_op_bytes()))
+    dummy = ctypes.c_void_p(16)
+    base = int(lib.csm_slab_scratch_bytes())
+    assert lib.csm_set_thread_engine(1) == 0  # Ozaki: engine bytes at 512 x 1024
+    try:
+        need = base + int(lib.csm_slab_engine_bytes(512, 1024))
+        assert need > base
+        rc = lib.csm_slab_op(op, dummy, 512, 1024, 0, dummy, dummy, 0, 0.0, -1,
+                             dummy, dummy, 0, dummy, need - 1, None)
+        assert rc == _lib.ERR_WORKSPACE and "scratch" in _lib.last_error()
+        rc = lib.csm_slab_op_pair(op, op, dummy, 512, 1024, 0, dummy, dummy, 0, 0.0, 0,
+                                  dummy, dummy, 0, dummy, base, None)
+        assert rc == _lib.ERR_WORKSPACE
+    finally:
+        assert lib.csm_set_thread_engine(-1) == 0
+
+
+def test_thread_engine_override_is_per_thread():
+    """csm_set_thread_engine overrides the process default for the calling
+    thread only; engine_scope nests and restores."""
+    import threading
+    lib = _lib.lib()
+    assert lib.csm_set_thread_engine(7) == _lib.ERR_ARG
+    seen = {}
+    with csm.engine_scope("dmma"):
+        assert csm.get_engine() == "dmma"
+        with csm.engine_scope("ozaki"):
+            assert csm.get_engine() == "ozaki"
+            th = threading.Thread(target=lambda: seen.setdefault("other", csm.get_engine()))
+            th.start()
+            th.join()
+        assert csm.get_engine() == "dmma"
+    assert csm.get_engine() == "auto"
+    assert seen["other"] == "auto"  # another thread sees the process default
