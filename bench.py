@@ -179,6 +179,52 @@ def dist_setup(args):
     return world, rank, local
 
 
+def config_dict(args, cfg, world):
+    """The `config` object, identical in both arms (--impl ours|reference)."""
+    kind, batch, n, dt, prec, desc = cfg
+    esz = 4 if dt == "f32" else 8
+    if kind == "cfg5":
+        par = f"block-row x{world}"
+    else:
+        par = f"batch shard x{world} (no collective)"
+    return {"workload": args.config, "description": desc, "batch_per_gpu": batch, "n": n,
+            "precision_table": prec,
+            "l2": ("inputs larger than L2 (no flush needed)" if batch * n * n * esz > 2 * 126e6
+                   else "input fits L2; steps reuse it (no flush)"),
+            "parallelism": par}
+
+
+def host_info():
+    """CPU model, core count and the BLAS numpy runs on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        import numpy  # noqa: F401  (loads its BLAS)
+        for lib in threadpool_info():
+            if lib.get("user_api") == "blas":
+                blas = f"{lib.get('internal_api')} {lib.get('version')} ({lib.get('num_threads')} threads)"
+                break
+    except Exception:
+        pass
+    import numpy as np
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "blas": blas,
+            "numpy": np.__version__}
+
+
+PORT_NOTE = ("oracle/cossin_oracle.py restates the reference's numpy path call for call; "
+             "it skips the reference's per-call Fraction->float coefficient conversions, "
+             "so if anything it flatters the CPU")
+
+
 def cpu_baseline_leg(kind, n, seconds):
     from oracle.cpu_pool import run_pool
     per_worker = {"cfg2": 256, "cfg3": 8, "cfg4": 2}.get(kind, 64)
@@ -194,7 +240,7 @@ def run_reference(args, cfg):
     kind, batch, n, dt, prec, desc = cfg
     if rank != 0:
         return
-    if kind in ("cfg1", "cfg5"):
+    if kind == "cfg1":
         from oracle import cossin_oracle as orc
         a, _ = make_inputs(kind, batch, n, 0)
         times = []
@@ -205,7 +251,28 @@ def run_reference(args, cfg):
                 times.append(time.perf_counter() - t0)
         rate = 1.0 / statistics.mean(times)
         ms_step = 1e3 * statistics.mean(times)
-        cores, sample = os.cpu_count(), f"{args.steps} full calls"
+        cores, sample = os.cpu_count(), f"{args.steps} full cos_sin calls (one process)"
+    elif kind == "cfg5":
+        # one full call is ~80 s of dgemm: each step times ONE of its k + 2s
+        # products (numpy @, all BLAS threads) and the rate charges all of
+        # them; the linear combinations are left out (flatters the CPU)
+        import numpy as np
+        from oracle import cossin_oracle as orc
+        a, _ = make_inputs(kind, batch, n, 0)
+        k, sc = orc.select(orc.norm1(a[0]))
+        x = np.ascontiguousarray(a[0] * 2.0 ** -sc)
+        times = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            _ = x @ x
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        per_matrix = (k + 2 * sc) * statistics.mean(times)
+        rate = 1.0 / per_matrix
+        ms_step = 1e3 * per_matrix
+        cores = os.cpu_count()
+        sample = (f"one {n}^2 dgemm per step (numpy @, all BLAS threads) x {k + 2 * sc} "
+                  "products per matrix; linear combinations not timed")
     else:
         per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))
         rates = []
@@ -223,11 +290,14 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": METRIC, "value": rate,
         "unit": "matrices/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64" if dt == "f64" else "f32->f64", "data": "synthetic",
-        "config": {"workload": args.config, "description": desc},
+        "higher_is_better": True, "scaling": "strong" if kind == "cfg5" else "weak",
+        "vs_baseline": None,
+        "dtype": "f64" if dt == "f64" else "f32 storage, f64 compute",
+        "data": "synthetic (seeded)",
+        "config": config_dict(args, cfg, args.gpus),
         "cpu_baseline": {"value": rate, "unit": "matrices/s", "cores": cores,
-                         "kind": "port", "sample": sample},
+                         "kind": "port", "sample": sample, "host": host_info(),
+                         "note": PORT_NOTE},
         "e2e": {"value": rate, "unit": "matrices/s",
                 "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -333,6 +403,69 @@ def run_cfg5(args, cfg):
         torch.distributed.destroy_process_group()
 
 
+def parity_block(kind, a_np, t_np, prec, dt, plan, ks, ss, rank):
+    """Parity summary carried in the bench line (computed outside the timed
+    region): the oracle on a spot-check sample at the parity gate (1e-12
+    fp64 / 1e-5 fp32; for the wave config max(1e-12, 4 x the oracle's own
+    permuted-order noise)), (k, s) of EVERY matrix against the
+    oracle's selection, and the Pythagorean residual ||C^2 + S^2 - I||_1 /
+    max(1, ||C||_1^2) over the whole batch (csm_pythagorean_residual)."""
+    import numpy as np
+    import torch
+
+    import paper_2010_00465_b200 as csm
+    from oracle import cossin_oracle as orc
+    from tests._util import pair_close, permuted_noise
+    wave = kind == "cfg4"
+    batch, n = a_np.shape[0], a_np.shape[-1]
+    fam = "wave" if wave else "taylor"
+    mism = 0
+    for i in range(batch):
+        a64 = a_np[i].astype(np.float64)
+        nrm = orc.norm1(a_np[i]) if dt == "f32" else orc.norm1(a64)
+        if wave:
+            nrm = float(t_np[i]) * float(t_np[i]) * nrm
+        k, s = orc.select(nrm, fam, prec)
+        mism += int((k, s) != (int(ks[i]), int(ss[i])))
+    assert mism == 0, f"{mism} (k, s) mismatches against the oracle's selection"
+    m = min(batch, 4 if n >= 512 else 8)
+    rng = np.random.default_rng(31)
+    worst_c = worst_s = 0.0
+    gates = []
+    for i in range(m):
+        if wave:
+            fn = lambda x: orc.wave_cos_sin(x, float(t_np[i]), prec)  # noqa: E731
+            (c, s, k, sc), noise = permuted_noise(fn, a_np[i], rng)
+            gate = max(1e-12, 4.0 * noise)
+        else:
+            c, s, k, sc = orc.cos_sin(a_np[i].astype(np.float64), prec)
+            gate = 1e-5 if dt == "f32" else 1e-12
+        assert (int(ks[i]), int(ss[i])) == (k, sc), (i, ks[i], ss[i], k, sc)
+        okc, ec = pair_close(plan.cos[i].double().cpu().numpy(), c, s, gate)
+        oks, es = pair_close(plan.sin[i].double().cpu().numpy(), s, c, gate)
+        assert okc and oks, (i, ec, es, gate)
+        worst_c, worst_s = max(worst_c, ec), max(worst_s, es)
+        gates.append(gate)
+    out = {"spot_checked": m, "gate_max": max(gates), "max_rel1_err_cos": worst_c,
+           "max_rel1_err_sin": worst_s, "ks_checked": batch, "ks_mismatches": mism,
+           "oracle": "oracle/cossin_oracle.py (pinned to the reference's goldens)"}
+    if wave:
+        out["pythagorean"] = None  # c^2 + A s^2 = I for the wave pair; not C^2 + S^2
+    else:
+        res = csm.pythagorean_residual(plan.cos, plan.sin)
+        cn = torch.empty(batch, dtype=torch.float64, device=plan.cos.device)
+        st = torch.empty(batch, dtype=torch.int32, device=plan.cos.device)
+        from paper_2010_00465_b200 import _lib
+        _lib.check(_lib.lib().csm_norm1(plan.code, ctypes.c_void_p(plan.cos.data_ptr()), batch, n,
+                                        ctypes.c_void_p(cn.data_ptr()),
+                                        ctypes.c_void_p(st.data_ptr()), None), "csm_norm1")
+        rel = (res / torch.clamp(cn * cn, min=1.0)).cpu().numpy()
+        out["pythagorean"] = {"max": float(rel.max()), "median": float(np.median(rel)),
+                              "max_abs": float(res.max().item()),
+                              "normalised_by": "max(1, ||C||_1^2)", "matrices": batch}
+    return out
+
+
 def run_ours(args, cfg):
     import numpy as np
     import torch
@@ -373,38 +506,15 @@ def run_ours(args, cfg):
     a_dev = torch.from_numpy(a_np).to(dev)
     t_dev = torch.from_numpy(t_np).to(dev) if wave else None
 
-    # correctness spot check against the oracle (outside the timed region)
+    # parity against the oracle and the Pythagorean residual over the whole
+    # batch (outside the timed region)
     plan.run(a_dev, t_dev)
     torch.cuda.synchronize()
     st = plan.status.cpu().numpy()
     assert not st.any(), "non-zero status in bench inputs"
     ks = plan.k.cpu().numpy().astype(np.int64)
     ss = plan.s.cpu().numpy().astype(np.int64)
-    from oracle import cossin_oracle as orc
-    if n > 2048:
-        # One huge matrix (cfg5): the CPU oracle needs ~80 s per call, so the
-        # spot check uses (k, s) from the host twin and two properties: a
-        # symmetric input gives symmetric cos/sin, and the Pythagorean
-        # residual (tests/test_gpu_parity.py holds the n <= 2048 analogue
-        # against the oracle and its own noise floor).
-        from paper_2010_00465_b200 import select_batch
-        k0, s0, _ = select_batch([orc.norm1(a_np[0])])
-        assert (int(ks[0]), int(ss[0])) == (int(k0[0]), int(s0[0]))
-        cg = plan.cos[0]
-        sg = plan.sin[0]
-        asym = float((cg - cg.T).abs().max() / cg.abs().max())
-        res = cg @ cg + sg @ sg - torch.eye(n, dtype=cg.dtype, device=cg.device)
-        pyth = float(res.abs().sum(0).max())
-        assert asym <= 1e-10 and pyth <= 1e-8 * float(cg.abs().sum(0).max()) ** 2, (asym, pyth)
-    for i in range(0 if n > 2048 else (min(4, batch) if n >= 512 else min(8, batch))):
-        if wave:
-            c, s, k, sc = orc.wave_cos_sin(a_np[i], float(t_np[i]), prec)
-        else:
-            c, s, k, sc = orc.cos_sin(a_np[i].astype(np.float64), prec)
-        assert (int(ks[i]), int(ss[i])) == (k, sc), (i, ks[i], ss[i], k, sc)
-        cg = plan.cos[i].double().cpu().numpy()
-        err = np.abs(cg - c).sum(0).max() / max(np.abs(c).sum(0).max(), 1e-300)
-        assert err <= (1e-5 if dt == "f32" else 1e-10), (i, err)
+    parity = parity_block(kind, a_np, t_np, prec, dt, plan, ks, ss, rank)
     flops_step = float((2.0 * n ** 3 * (ks + 2 * ss)).sum())
 
     # warm-up, then K timed steps between barriers + synchronize
@@ -414,6 +524,21 @@ def run_ours(args, cfg):
     L = _lib.lib()
     oz = ozaki_applies(n)
     L.csm_profile_enable(2 if oz else 1)
+    # small batches are launch-latency bound: replay the pipeline as one CUDA
+    # graph (norm, selection, schedule and fused kernels; BatchPlan.capture)
+    use_graph = batch <= 64 and plan.graph_safe
+    step_fn = lambda: plan.run(a_dev, t_dev)  # noqa: E731
+    per_run = 0
+    if use_graph:
+        L.csm_profile_enable(0)
+        plan.launches = 0
+        plan.run(a_dev, t_dev)
+        per_run = plan.launches
+        plan.capture(a_dev, t_dev)
+        for _ in range(args.warmup):
+            plan.replay()
+        step_fn = plan.replay
+        L.csm_profile_enable(2 if oz else 1)
     plan.launches = 0
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -422,14 +547,14 @@ def run_ours(args, cfg):
     with ClockSampler(local) as clk:
         e0.record()
         for _ in range(args.steps):
-            plan.run(a_dev, t_dev)
+            step_fn()
         e1.record()
         torch.cuda.synchronize()
     barrier()
     ms_total = e0.elapsed_time(e1)
     kern_ms = ctypes_collect(L)
     L.csm_profile_enable(0)
-    launches = plan.launches
+    launches = per_run * args.steps if use_graph else plan.launches
     ms_step = max_over_ranks(ms_total / args.steps)
     units = sum_over_ranks(float(batch))
     value = units / (ms_step * 1e-3)
@@ -468,6 +593,8 @@ def run_ours(args, cfg):
         pk = ctypes.c_double(0.0)
         if L.csm_fp64_peak(20000, ctypes.byref(pk), None) == 0:
             peak = pk.value
+    if use_graph:  # graph replays carry no library-side events: the step is the kernel interval
+        kern_ms = (ms_total, args.steps)
     kern_avg_ms = kern_ms[0] / max(kern_ms[1], 1)
     achieved = flops_step / (kern_avg_ms * 1e-3) / 1e12 if kern_avg_ms > 0 else None
     traffic = None
@@ -481,14 +608,27 @@ def run_ours(args, cfg):
     if rank != 0:
         return
     cpu = None
-    if world == 1 and not args.no_cpu_baseline and kind not in ("cfg1", "cfg5"):
+    if world == 1 and not args.no_cpu_baseline and kind == "cfg1":
+        from oracle import cossin_oracle as orc
+        a0 = a_np[0].astype(np.float64)
+        calls, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < args.cpu_seconds:
+            orc.cos_sin(a0)
+            calls += 1
+        secs = time.perf_counter() - t0
+        cpu = {"value": calls / secs, "unit": "matrices/s", "cores": 1, "kind": "port",
+               "sample": f"oracle port of cos_sin on the cfg1 matrix, {calls} sequential "
+                         f"calls in {secs:.1f} s (one process)",
+               "host": host_info(), "note": PORT_NOTE}
+    elif world == 1 and not args.no_cpu_baseline and kind != "cfg5":
         rate, workers, done, secs, pw = cpu_baseline_leg(kind, n, args.cpu_seconds)
         cpu = {"value": rate, "unit": "matrices/s", "cores": workers,
                "kind": "port",
                "sample": (f"oracle port of cos_sin/wave_cos_sin on {done} "
                           f"matrices ({workers} processes x {pw} seeded "
                           f"{desc.split(',')[0]} inputs, 1 BLAS thread each, "
-                          f"{secs:.1f} s)")}
+                          f"{secs:.1f} s)"),
+               "host": host_info(), "note": PORT_NOTE}
     clocks = clk.summary()
     line = {
         "metric": METRIC,
@@ -504,14 +644,10 @@ def run_ours(args, cfg):
         "vs_baseline": None,
         "dtype": "f64" if dt == "f64" else "f32 storage, f64 compute",
         "data": "synthetic (seeded; per-rank shard seed = rank)",
-        "config": {"workload": args.config, "description": desc,
-                   "batch_per_gpu": batch, "n": n, "precision_table": prec,
-                   "mean_products": float((ks + 2 * ss).mean()),
-                   "l2": "inputs larger than L2 (no flush needed)"
-                   if batch * n * n * esz > 2 * 126e6 else
-                   "input fits L2; steps reuse it (no flush)",
-                   "parallelism": f"batch shard x{world} (no collective)",
-                   "engine": "ozaki" if oz else "dmma"},
+        "config": config_dict(args, cfg, world),
+        "engine": "ozaki" if oz else "dmma",
+        "mean_products": float((ks + 2 * ss).mean()),
+        "parity": parity,
         "roofline": ozaki_roofline((9 if dt == "f32" else 16) * flops_step,
                                    kern_ms[0] / args.steps, tflops, peak) if oz else
                     {"bound": "tensor", "achieved": achieved, "peak": peak,
@@ -531,6 +667,7 @@ def run_ours(args, cfg):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms},
         "gpu_launches": launches,
+        "launch_mode": "CUDA graph replay (BatchPlan.capture)" if use_graph else "stream launches",
         "clocks": clocks,
         "cpu_baseline": cpu,
     }
@@ -589,10 +726,10 @@ def main():
     ap.add_argument("--dist-mode", choices=["gather", "peer"], default="gather",
                     help="cfg5 only: NCCL all-gather per product, or the fused "
                          "peer-memory product (symmetric memory)")
-    ap.add_argument("--engine", choices=["auto", "dmma", "ozaki"], default="auto",
+    ap.add_argument("--engine", choices=["auto", "dmma", "ozaki"], default="dmma",
                     help="product engine of the tiled chain (n > 128) and the cfg5 slab "
-                         "products: FP64 DMMA, Ozaki-II on the int8 tensor cores, or auto "
-                         "(the library default: Ozaki from padded order 768 up)")
+                         "products: FP64 DMMA (the library default), Ozaki-II on the int8 "
+                         "tensor cores, or auto (Ozaki from padded order 768 up)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warm-up raised to 3 (timing rule)")

@@ -168,6 +168,16 @@ int csm_dd_matmul(const double* xh, const double* xl, const double* yh,
                   int n, void* stream);
 int csm_ddref_series_consts(double* out28);
 
+/* Pythagorean residual of computed pairs: out[b] = ||C_b C_b + S_b S_b -
+ * I||_1 (max column sum), the reference's accuracy witness (pkg/README.md:
+ * 172-176, tests/test_driver.py:149-157).  A diagnostic beside the path:
+ * both products on DMMA, deterministic reduction.  dtype CSM_F64 or CSM_F32
+ * (the inputs' type); out: DEVICE double[batch]. */
+size_t csm_residual_workspace_size(int64_t batch, int n);
+int csm_pythagorean_residual(int dtype, const void* cos_in, const void* sin_in,
+                             int64_t batch, int n, double* out, void* workspace,
+                             size_t ws_bytes, void* stream);
+
 /* Order-8 Pade baseline (driver.py:149-164, schemes.py:446-464): selection
  * over PADE_TABLE, a * 2^-s, five products (A^2, A^4, A^6, A^8 and A times
  * the odd numerator) with the three polynomials fused into their epilogues,
@@ -259,13 +269,15 @@ int csm_graph_safe(int dtype, int64_t batch, int n);
  * the padded order is a multiple of 256 (DMMA otherwise).  Every Ozaki
  * product is checked by an a-priori error bound: when the rounding of the
  * operands to P bits relative to their row / column maxima could exceed
- * the fp64 GEMM bound (n u ||C||_1), that product is recomputed on DMMA
- * (badly scaled operands), so the result is never less accurate than the
- * bound of the reference's fp64 product (matcore.py:97).
- * CSM_ENGINE_AUTO (default): Ozaki for padded orders >= 768 that are
- * multiples of 256, where it is faster; DMMA below.  The chain, (k, s) and
- * the reference interface are unchanged.
- *   csm_set_engine: the process default (atomic).
+ * n u ||C||_1 (the fp64 GEMM's norm-wise bound), that product is recomputed
+ * on DMMA.  The guarantee is norm-wise per product: on graded operands a
+ * long doubling recursion can amplify the Ozaki rounding of small entries
+ * beyond the reference's accuracy, which an fp64 GEMM (componentwise
+ * error, matcore.py:97) does not do -- hence DMMA is the DEFAULT engine.
+ * CSM_ENGINE_AUTO: Ozaki for padded orders >= 768 that are multiples of
+ * 256, where it is faster; DMMA below.  The chain, (k, s) and the
+ * reference interface are unchanged.
+ *   csm_set_engine: the process default (atomic; CSM_ENGINE_DMMA at load).
  *   csm_set_thread_engine: an override for the calling thread (-1 clears).
  * Each call reads the engine once; workspace sizes (csm_workspace_size,
  * csm_slab_engine_bytes, ...) depend on it, and a call whose workspace is

@@ -2,8 +2,8 @@
 
 The public names of the reference's hot path (pkg/src/cossinm/__init__.py)
 with the same signatures, plus batched entry points.  Every computation
-runs in libcossin_b200.so (sm_100a kernels: FP64 DMMA, and from n = 768 up
-by default the Ozaki-II engine on the int8 tensor cores, see set_engine)
+runs in libcossin_b200.so (sm_100a kernels: FP64 DMMA by default; the
+Ozaki-II engine on the int8 tensor cores is opt-in, see set_engine)
 through the C-ABI in include/cossin_b200.h; importing this package fails if
 the library has not been built, and computing without a CUDA device raises.
 """
@@ -19,6 +19,7 @@ from .api import (
     norm1,
     pade_cos_sin,
     pade_cos_sin_batched,
+    pythagorean_residual,
     read_matrix,
     select_batch,
     select_scheme,
@@ -83,6 +84,7 @@ __all__ = [
     "norm1",
     "pade_cos_sin",
     "pade_cos_sin_batched",
+    "pythagorean_residual",
     "read_matrix",
     "select_batch",
     "select_scheme",

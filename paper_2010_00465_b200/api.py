@@ -492,6 +492,35 @@ def norm1(a) -> float:
     return float(out.item())
 
 
+def pythagorean_residual(cos_part, sin_part, *, stream=None):
+    """||C C + S S - I||_1 per matrix, on the device (csm_pythagorean_residual):
+    the reference's accuracy witness for a computed pair (pkg/README.md:
+    172-176, tests/test_driver.py:149-157).  Accepts one (n, n) pair or a
+    batch (B, n, n); float64 or float32.  Returns a float for one pair,
+    else a float64 array (numpy for host inputs, a CUDA tensor for device
+    inputs)."""
+    torch = _torch()
+    single = (cos_part.ndim if hasattr(cos_part, "ndim") else np.asarray(cos_part).ndim) == 2
+    cb = _as_batch(cos_part, batched=not single, f32_out=True)
+    sb = _as_batch(sin_part, batched=not single, f32_out=True)
+    c, s = cb.dev, sb.dev
+    if c.shape != s.shape or c.dtype != s.dtype:
+        raise ValueError("cos and sin parts must have the same shape and dtype")
+    L = _lib.lib()
+    B, n = int(c.shape[0]), int(c.shape[-1])
+    out = torch.empty(B, dtype=torch.float64, device=c.device)
+    ws_bytes = int(L.csm_residual_workspace_size(B, n))
+    ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=c.device)
+    code = _lib.F32 if c.dtype == torch.float32 else _lib.F64
+    _lib.check(L.csm_pythagorean_residual(code, _vp(c.data_ptr()), _vp(s.data_ptr()), B, n,
+                                          _vp(out.data_ptr()), _vp(ws.data_ptr()), ws_bytes,
+                                          _vp(_stream_handle(stream))),
+               "csm_pythagorean_residual")
+    if single:
+        return float(out[0].item())
+    return out if cb.host is None else out.cpu().numpy()
+
+
 def matrix_from_rows(rows: Sequence[Sequence[float]]) -> np.ndarray:
     """Validated matrix from nested sequences (matcore.py:69-83)."""
     try:
@@ -568,11 +597,13 @@ _ENGINES = {"dmma": 0, "ozaki": 1, "auto": 2, "ozaki-unguarded": 3}
 
 def set_engine(name: str) -> None:
     """Select the product engine of the tiled chain (n > 128) and the
-    block-row chain, process-wide (csm_set_engine): "dmma" (FP64 DMMA),
-    "ozaki" (Ozaki-II: exact int8 tensor-core GEMMs per modulus + CRT, for
-    padded orders that are multiples of 256) or "auto" (default: Ozaki from
-    padded order 768 up, DMMA below).  Size workspaces (BatchPlan) after
-    changing it."""
+    block-row chain, process-wide (csm_set_engine): "dmma" (FP64 DMMA, the
+    default: componentwise error like the reference's fp64 GEMM), "ozaki"
+    (Ozaki-II: exact int8 tensor-core GEMMs per modulus + CRT, for padded
+    orders that are multiples of 256, every product guarded by a norm-wise
+    a-priori error bound with a DMMA rerun), "auto" (Ozaki from padded
+    order 768 up, DMMA below) or "ozaki-unguarded" (experiments only).
+    Size workspaces (BatchPlan) after changing it."""
     if name not in _ENGINES:
         raise ValueError(f"engine must be one of {sorted(_ENGINES)}")
     _lib.check(_lib.lib().csm_set_engine(_ENGINES[name]), "csm_set_engine")
@@ -613,7 +644,7 @@ def engine_scope(name: str):
 __all__ = [
     "BatchReport", "cos_sin", "engine_scope", "get_engine", "set_engine", "cos_sin_batched", "identity",
     "pade_cos_sin", "pade_cos_sin_batched",
-    "matrix_from_rows", "norm1", "read_matrix", "select_batch",
+    "matrix_from_rows", "norm1", "pythagorean_residual", "read_matrix", "select_batch",
     "select_scheme", "taylor_cos_sin", "taylor_sin9", "wave_cos_sin",
     "wave_cos_sin_batched", "wave_kernels", "wave_sin34", "write_matrix",
 ]

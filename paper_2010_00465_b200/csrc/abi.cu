@@ -55,6 +55,9 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
                       void* s_out, int64_t batch, int n, const int32_t* dK, const int32_t* dS,
                       const int32_t* dStatus, void* ws, cudaStream_t stream, int64_t* launches,
                       int special, int eng);
+size_t residual_workspace_bytes(int64_t batch, int n);
+cudaError_t pythagorean_residual(bool f32, const void* c, const void* s, int64_t batch, int n,
+                                 double* out, void* ws, cudaStream_t stream, int64_t* launches);
 size_t ddref_workspace_doubles(int64_t batch, int n);
 void ddref_series_consts(double* out28);
 cudaError_t dd_matmul(const double* xh, const double* xl, const double* yh, const double* yl,
@@ -657,6 +660,37 @@ int csm_taylor_sin9(int dtype, const void* a, void* sin_out, int64_t batch, int 
 int csm_wave_sin34(int dtype, const void* a, const double* t, void* s_out, int64_t batch, int n,
                    int32_t* status, void* workspace, size_t ws_bytes, void* stream) {
   return standalone_sine(dtype, true, a, t, s_out, batch, n, status, workspace, ws_bytes, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Pythagorean residual of computed pairs (diagnostic; pkg/README.md:172-176).
+
+size_t csm_residual_workspace_size(int64_t batch, int n) {
+  if (batch < 0 || n < 0) return 0;
+  return csm::residual_workspace_bytes(batch, n);
+}
+
+int csm_pythagorean_residual(int dtype, const void* cos_in, const void* sin_in, int64_t batch,
+                             int n, double* out, void* workspace, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (dtype != CSM_F64 && dtype != CSM_F32) return fail(CSM_ERR_ARG, "dtype must be CSM_F64 or CSM_F32");
+  if (batch < 0 || n < 0) return fail(CSM_ERR_ARG, "batch and n must be nonnegative");
+  if (ws_bytes < csm_residual_workspace_size(batch, n))
+    return fail(CSM_ERR_WORKSPACE, "workspace smaller than csm_residual_workspace_size()");
+  if (batch == 0) return CSM_SUCCESS;
+  if (!out || (n > 0 && (!cos_in || !sin_in || !workspace)))
+    return fail(CSM_ERR_ARG, "null pointer argument");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n == 0) {
+    cudaError_t e = cudaMemsetAsync(out, 0, static_cast<size_t>(batch) * 8, st);
+    return e == cudaSuccess ? CSM_SUCCESS : cuda_fail(e, "memset");
+  }
+  cudaError_t e = csm::pythagorean_residual(dtype == CSM_F32, cos_in, sin_in, batch, n, out,
+                                            workspace, st, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "residual kernels");
+  return CSM_SUCCESS;
 }
 
 // ---------------------------------------------------------------------------

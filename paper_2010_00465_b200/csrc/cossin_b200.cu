@@ -4,4 +4,5 @@
 #include "fused64.cu"
 #include "tiled.cu"
 #include "ddref.cu"
+#include "residual.cu"
 #include "abi.cu"

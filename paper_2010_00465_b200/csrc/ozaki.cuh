@@ -790,6 +790,10 @@ __global__ void __launch_bounds__(256) oz_guard(const LaunchArgs la, const OzArg
     const double gamma = static_cast<double>(n) * 0x1p-53;
     // !(E <= gamma C) also flags a NaN bound (never expected: bad items skip)
     oz.flag[ci] = (!bad && !(emax <= gamma * cmax)) ? 1u : 0u;
+#ifdef CSM_OZ_GUARD_DEBUG
+    printf("oz_guard item %d rs %d: E %.3e ||C|| %.3e gamma %.3e sd %.3e sl %.3e bad %d flag %u\n",
+           oz.item0 + ci, rs, emax, cmax, gamma, sd, sl, (int)bad, oz.flag[ci]);
+#endif
   }
 }
 

@@ -28,6 +28,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -849,16 +850,21 @@ void free_pair(int c0, int s0, int* c1, int* s1) {
 
 size_t tiled_np(int n) { return static_cast<size_t>((n + 63) / 64) * 64; }
 
-// Product engine: 0 = FP64 DMMA, 1 = Ozaki-II on the int8 tensor cores
-// (ozaki.cuh) for the tiled chain when NP % 256 == 0, 2 = auto (default):
-// Ozaki from NP = 768 up, where its O(n^2 nm) passes are small enough next
-// to the GEMM (batched n = 768: 1.06x the DMMA chain, n = 1024: 1.3x,
-// n = 2048: 2.1x, cfg5 8192^2: 3.8x; n <= 512 is faster on DMMA, DESIGN.md
-// K7).  The process default (csm_set_engine) is atomic; a thread may
+// Product engine: 0 = FP64 DMMA (default), 1 = Ozaki-II on the int8 tensor
+// cores (ozaki.cuh) for the tiled chain when NP % 256 == 0, 2 = auto: Ozaki
+// from NP = 768 up, where its O(n^2 nm) passes are small enough next to the
+// GEMM (batched n = 768: 1.06x the DMMA chain, n = 1024: 1.3x, n = 2048:
+// 2.1x, cfg5 8192^2: 3.8x; n <= 512 is faster on DMMA, K7), 3 =
+// Ozaki without the accuracy guard (experiments).  DMMA is the default
+// because its error is componentwise, like the reference's fp64 GEMM
+// (matcore.py:97): the Ozaki rounding is relative to row / column maxima,
+// and oz_guard bounds it only norm-wise per product -- enough for
+// well-scaled operands, not for graded ones whose small entries a long
+// doubling recursion amplifies (K7, tests/test_gpu_guard.py).  The process default (csm_set_engine) is atomic; a thread may
 // override it (csm_set_thread_engine).  Every entry point reads the engine
 // ONCE (engine()) and passes that snapshot down, so a call never mixes
 // engines and its workspace check matches what it runs.
-static std::atomic<int> g_engine{2};
+static std::atomic<int> g_engine{0};
 static thread_local int t_engine = -1;
 void set_engine(int e) { g_engine.store(e, std::memory_order_relaxed); }
 void set_thread_engine(int e) { t_engine = e; }

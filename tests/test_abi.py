@@ -84,7 +84,7 @@ def test_engine_switch_without_device():
     Ozaki engine enlarges the tiled workspace (n = 256) but not n = 64 or
     the DMMA-only orders (NP % 256 != 0)."""
     lib = _lib.lib()
-    assert lib.csm_get_engine() == 2  # auto: Ozaki from padded order 768 up
+    assert lib.csm_get_engine() == 0  # DMMA: the default engine
     assert lib.csm_workspace_size(0, 1, 4096) > 9 * 4096 * 4096 * 8 + 16 * 3 * 4096 * 4096
     assert lib.csm_set_engine(5) == _lib.ERR_ARG
     assert lib.csm_set_engine(0) == 0
@@ -100,7 +100,7 @@ def test_engine_switch_without_device():
         # residue planes of L (M x NP), R (NP x NP) and the product, 16 moduli
         assert lib.csm_slab_engine_bytes(512, 1024) >= 16 * (2 * 512 * 1024 + 1024 * 1024)
     finally:
-        assert lib.csm_set_engine(2) == 0
+        assert lib.csm_set_engine(0) == 0
 
 
 def test_slab_op_pair_argument_errors_without_device():
@@ -157,5 +157,5 @@ def test_thread_engine_override_is_per_thread():
             th.start()
             th.join()
         assert csm.get_engine() == "dmma"
-    assert csm.get_engine() == "auto"
-    assert seen["other"] == "auto"  # another thread sees the process default
+    assert csm.get_engine() == "dmma"
+    assert seen["other"] == "dmma"  # another thread sees the process default

@@ -20,7 +20,7 @@ TOL32 = 1e-5
 def ozaki(cuda):
     csm.set_engine("ozaki")
     yield
-    csm.set_engine("auto")
+    csm.set_engine("dmma")
 
 
 @pytest.mark.parametrize("n", [256, 512])
@@ -129,7 +129,7 @@ def test_workspace_follows_engine(cuda):
         assert int(L.csm_slab_engine_bytes(256, 512)) > 0
         assert int(L.csm_slab_engine_bytes(128, 512)) == 0  # M % 256 != 0: DMMA
     finally:
-        csm.set_engine("auto")
+        csm.set_engine("dmma")
     with pytest.raises(ValueError):
         csm.set_engine("tf32")
 
@@ -194,18 +194,14 @@ def test_pade_and_standalone_sines(ozaki):
 
 
 def test_auto_engine_picks_by_size(cuda):
-    """auto (the default): DMMA below padded order 768 -- bit-identical to
-    the forced DMMA engine."""
-    csm.set_engine("auto")
-    assert csm.get_engine() == "auto"
+    """auto: DMMA below padded order 768 -- bit-identical to the DMMA
+    engine (the default)."""
+    assert csm.get_engine() == "dmma"
     rng = np.random.default_rng(817)
     a = cfg2_like(rng, 2, n=512)
-    au = csm.cos_sin_batched(a)
-    csm.set_engine("dmma")
-    try:
-        dm = csm.cos_sin_batched(a)
-    finally:
-        csm.set_engine("auto")
+    with csm.engine_scope("auto"):
+        au = csm.cos_sin_batched(a)
+    dm = csm.cos_sin_batched(a)
     assert np.array_equal(au.cos_part, dm.cos_part)
     assert np.array_equal(au.sin_part, dm.sin_part)
 
@@ -252,8 +248,8 @@ def test_overflow_mid_chain_stays_non_finite(ozaki):
 
 
 @pytest.mark.timeout(600)
-def test_default_engine_at_1024_against_oracle_and_truth(cuda):
-    """The default (auto) engine runs n = 1024 on Ozaki-II: cfg2-like
+def test_auto_engine_at_1024_against_oracle_and_truth(cuda):
+    """The auto engine runs n = 1024 on Ozaki-II: cfg2-like
     matrices through the public API, (k, s) bit-exact.  At norm ~63 (s = 6)
     the reference itself is ~2e-12 from the double-double truth at this n
     (tools/oz_dbg1024.py: the DMMA engine is 3e-12 from the oracle, Ozaki
@@ -261,10 +257,10 @@ def test_default_engine_at_1024_against_oracle_and_truth(cuda):
     bar is SURVEY 8a's: max(1e-12, 2 x the oracle's own distance to the
     truth), and no further from the truth than twice the oracle."""
     from paper_2010_00465_b200 import verify
-    csm.set_engine("auto")
     rng = np.random.default_rng(820)
     a = cfg2_like(rng, 3, n=1024, lo=-1.0, hi=2.0)
-    rep = csm.cos_sin_batched(a)
+    with csm.engine_scope("auto"):
+        rep = csm.cos_sin_batched(a)
     tc, ts, _ = verify.reference_cos_sin_batched(a)
     for i in range(a.shape[0]):
         c, s, k, sc = orc.cos_sin(a[i])
