@@ -85,7 +85,12 @@ def test_engine_switch_without_device():
     the DMMA-only orders (NP % 256 != 0)."""
     lib = _lib.lib()
     assert lib.csm_get_engine() == 0  # DMMA: the default engine
-    assert lib.csm_workspace_size(0, 1, 4096) > 9 * 4096 * 4096 * 8 + 16 * 3 * 4096 * 4096
+    assert lib.csm_workspace_size(0, 1, 4096) < 9 * 4096 * 4096 * 8 + 16 * 3 * 4096 * 4096
+    assert lib.csm_set_thread_engine(2) == 0  # auto: Ozaki scratch from padded order 768 up
+    try:
+        assert lib.csm_workspace_size(0, 1, 4096) > 9 * 4096 * 4096 * 8 + 16 * 3 * 4096 * 4096
+    finally:
+        assert lib.csm_set_thread_engine(-1) == 0
     assert lib.csm_set_engine(5) == _lib.ERR_ARG
     assert lib.csm_set_engine(0) == 0
     assert "engine" in _lib.last_error()
