@@ -75,16 +75,22 @@ __device__ __forceinline__ int& trace_count() {
 
 // Geometry: CL = CTAs per matrix (1: K1, 4: K1c).  BAND rows of NP columns
 // per CTA and slot; each warp owns an (8 MI) x (8 NI) accumulator tile.
+// K1 runs 16 warps (4 per SMSP, 16 x 16 warp tiles, <= 128 registers) by
+// default; CSM_K1_THREADS=256 builds the 8-warp form (16 x 32 tiles).
+#ifndef CSM_K1_THREADS
+#define CSM_K1_THREADS 512
+#endif
 template <int CL> struct Geo;
 template <> struct Geo<1> {
-  static constexpr int NP = 64, BAND = 64, MI = 2, NI = 4;
+  static constexpr int NP = 64, BAND = 64, THREADS = CSM_K1_THREADS, MI = 2,
+                       NI = THREADS == 512 ? 2 : 4;
 };
 template <> struct Geo<4> {
-  static constexpr int NP = 128, BAND = 32, MI = 4, NI = 2;
+  static constexpr int NP = 128, BAND = 32, THREADS = 256, MI = 4, NI = 2;
 };
+static_assert(Geo<1>::THREADS == 256 || Geo<1>::THREADS == 512, "K1: 8 or 16 warps");
 constexpr int SLOT = 4096;  // doubles per slot band (64 x 64 or 32 x 128)
 constexpr int NSLOTS = 7;
-constexpr int THREADS = 256;
 
 __host__ __device__ constexpr int swz_f(int r) { return ((r & 1) << 2) | (r & 2); }
 template <int NP>
@@ -209,7 +215,10 @@ template <int CL>
 __device__ __forceinline__ void make_lane(Lane<CL>& ln, int rank) {
   constexpr int NP = Geo<CL>::NP, MI = Geo<CL>::MI, NI = Geo<CL>::NI;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (CL == 1) {
+  if (CL == 1 && Geo<CL>::THREADS == 512) {
+    ln.rb = (warp >> 2) * 16;
+    ln.cb = (warp & 3) * 16;
+  } else if (CL == 1) {
     ln.rb = (warp >> 1) * 16;
     ln.cb = (warp & 1) * 32;
   } else {
@@ -658,10 +667,10 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // n < 64 the padding is rewritten with zeros (the slot may hold a previous
 // chain's intermediate).
 // NaN-fill this CTA's rows [r0, r0 + rows) of an n x n output.
-template <typename TOut>
+template <int NT, typename TOut>
 __device__ __forceinline__ void store_nan(TOut* __restrict__ dst, int n, int r0, int rows) {
   const int lo = r0 * n, hi = min(n, r0 + rows) * n;
-  for (int p = lo + threadIdx.x; p < hi; p += THREADS)
+  for (int p = lo + threadIdx.x; p < hi; p += NT)
     dst[p] = static_cast<TOut>(__longlong_as_double(0x7ff8000000000000ll));
 }
 
@@ -704,13 +713,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 }
 
 template <int CL, typename TIn, typename TOut, bool WAVE>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(Geo<CL>::THREADS, 1)
 fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
              TOut* __restrict__ Sout, const double* __restrict__ T,
              const int32_t* __restrict__ K, const int32_t* __restrict__ Sx,
              const int32_t* __restrict__ ST, const int32_t* __restrict__ order,
              int64_t batch, int n, int tma) {
-  constexpr int NP = Geo<CL>::NP, BAND = Geo<CL>::BAND;
+  constexpr int NP = Geo<CL>::NP, BAND = Geo<CL>::BAND, THREADS = Geo<CL>::THREADS;
   extern __shared__ __align__(128) double smem[];
   // Static schedule: cluster c takes order[] positions c, 2G-1-c, 2G+c, ...
   // (a snake over the cost-sorted list).  Thread 0 stages the matrix ids two
@@ -792,8 +801,8 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
     TOut* cdst = Cout + static_cast<size_t>(b) * nn;
     TOut* sdst = Sout + static_cast<size_t>(b) * nn;
     if (status != 0) {  // uniform across the cluster (same matrix)
-      store_nan(cdst, n, row0, BAND);
-      store_nan(sdst, n, row0, BAND);
+      store_nan<THREADS>(cdst, n, row0, BAND);
+      store_nan<THREADS>(sdst, n, row0, BAND);
       __syncthreads();
       if (tid == 0) prefetch(bn);
       continue;
@@ -889,7 +898,7 @@ static cudaError_t launch_one(const void* a, void* c, void* s, const double* t,
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
-  cfg.blockDim = dim3(f64k::THREADS);
+  cfg.blockDim = dim3(f64k::Geo<CL>::THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   int clusters = sms;
@@ -955,7 +964,7 @@ int k1c_resident_sms() {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cfg.blockDim = dim3(f64k::THREADS);
+  cfg.blockDim = dim3(f64k::Geo<4>::THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.gridDim = dim3(4 * 32);
   int active = 0;

@@ -163,6 +163,8 @@ def test_guard_keeps_well_scaled_products_on_ozaki(cuda):
     assert np.array_equal(oz.cos_part, ung.cos_part)
     assert np.array_equal(oz.sin_part, ung.sin_part)
     assert not np.array_equal(oz.cos_part, dm.cos_part)
+    prng = np.random.default_rng(7)
     for i in range(a.shape[0]):
-        c, s, _, _ = orc.cos_sin(a[i])
-        assert rel1(oz.cos_part[i], c) <= 1e-12 and rel1(oz.sin_part[i], s) <= 1e-12, i
+        (c, s, _, _), noise = permuted_noise(orc.cos_sin, a[i], prng)
+        gate = max(1e-12, 4.0 * noise)  # norm 300: s = 8, the oracle's own noise ~1e-12
+        assert rel1(oz.cos_part[i], c) <= gate and rel1(oz.sin_part[i], s) <= gate, (i, gate)
