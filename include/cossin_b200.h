@@ -192,6 +192,13 @@ int csm_pade_cos_sin(int dtype, int precision, const void* a, void* cos_out,
                      int32_t* status, void* workspace, size_t ws_bytes,
                      void* stream);
 
+/* The Pade base pair alone (schemes.py:446-464 pade8_cos_sin): no
+ * selection and no scaling (k = 5, s = 0 for every matrix), the same five
+ * products, LU and two solves as csm_pade_cos_sin.  status[] reports
+ * CSM_SINGULAR per matrix; workspace: csm_pade_workspace_size(). */
+int csm_pade_core(int dtype, const void* a, void* cos_out, void* sin_out, int64_t batch, int n,
+                  int32_t* status, void* workspace, size_t ws_bytes, void* stream);
+
 /* Copy the built-in theta table of (family, precision) -- the reference's
  * TAYLOR_TABLE / WAVE_TABLE (theta_tables.py:79-144) -- into host arrays of
  * `capacity` entries; returns the entry count (or a negative error). */

@@ -17,6 +17,7 @@ from .api import (
     identity,
     matrix_from_rows,
     norm1,
+    pade8_cos_sin,
     pade_cos_sin,
     pade_cos_sin_batched,
     pythagorean_residual,
@@ -32,8 +33,10 @@ from .api import (
     write_matrix,
 )
 from . import corpus, plan, verify
+from .verify import reference_cos_sin, reference_cos_sin_batched
 from .plan import BatchPlan
 from .records import (
+    PADE8,
     PADE_TABLE,
     TAYLOR_TABLE,
     UNIT_ROUNDOFF,
@@ -67,6 +70,7 @@ __all__ = [
     "SchemeFamily",
     "SchemeId",
     "SingularMatrixError",
+    "PADE8",
     "PADE_TABLE",
     "TAYLOR_TABLE",
     "ThetaEntry",
@@ -82,10 +86,13 @@ __all__ = [
     "identity",
     "matrix_from_rows",
     "norm1",
+    "pade8_cos_sin",
     "pade_cos_sin",
     "pade_cos_sin_batched",
     "pythagorean_residual",
     "read_matrix",
+    "reference_cos_sin",
+    "reference_cos_sin_batched",
     "select_batch",
     "select_scheme",
     "table_for",

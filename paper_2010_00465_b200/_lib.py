@@ -50,6 +50,7 @@ SIGNATURES = {
     "csm_wave_sin34": (_i32, [_i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _sz, _vp]),
     "csm_pade_workspace_size": (_sz, [_i32, _i64, _i32]),
     "csm_pade_cos_sin": (_i32, [_i32, _i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "csm_pade_core": (_i32, [_i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _sz, _vp]),
     "csm_residual_workspace_size": (_sz, [_i64, _i32]),
     "csm_pythagorean_residual": (_i32, [_i32, _vp, _vp, _i64, _i32, _vp, _vp, _sz, _vp]),
     "csm_ddref_workspace_size": (_sz, [_i64, _i32]),

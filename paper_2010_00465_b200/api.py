@@ -283,6 +283,41 @@ def pade_cos_sin(a, precision: Precision = Precision.DOUBLE
     return _single(_pade(batch, precision, True))
 
 
+def pade8_cos_sin(a, ledger: CostLedger) -> CosSinResult:
+    """The order-8 Pade base pair at a, no scaling (schemes.py:446-464):
+    five products, one LU with partial pivoting shared by two solves, all on
+    the device (csm_pade_core).  Charges 5 products and one LU with two
+    solves (7 + 1/3 product-equivalents), raising SingularMatrixError like
+    lu_solve_pair (matcore.py:124-151) after the products are charged."""
+    torch = _torch()
+    L = _lib.lib()
+    batch = _as_batch(a, batched=False, f32_out=False)
+    x = batch.dev
+    n = int(x.shape[-1])
+    dev = x.device
+    c = torch.empty((1, n, n), dtype=batch.out_dtype, device=dev)
+    s = torch.empty_like(c)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
+    ws_bytes = int(L.csm_pade_workspace_size(batch.code, 1, n))
+    ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
+    if n > 0:
+        _lib.check(L.csm_pade_core(batch.code, _vp(x.data_ptr()), _vp(c.data_ptr()),
+                                   _vp(s.data_ptr()), 1, n, _vp(status.data_ptr()),
+                                   _vp(ws.data_ptr()), ws_bytes, _vp(_stream_handle())),
+                   "csm_pade_core")
+    ledger.charge_product(5)
+    if n == 0 or int(status.item()) == _lib.SINGULAR:
+        raise _status_error(_lib.SINGULAR, 0.0)
+    ledger.charge_lu(solves=2)
+    if batch.host == "numpy":
+        c, s = c[0].cpu().numpy(), s[0].cpu().numpy()
+    elif batch.host == "torch":
+        c, s = c[0].cpu(), s[0].cpu()
+    else:
+        c, s = c[0], s[0]
+    return CosSinResult(cos_part=c, sin_part=s, cost=ledger)
+
+
 def _t_vector(t, B: int, dev):
     torch = _torch()
     if isinstance(t, torch.Tensor):

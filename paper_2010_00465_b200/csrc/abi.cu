@@ -831,6 +831,34 @@ int csm_pade_cos_sin(int dtype, int precision, const void* a, void* cos_out, voi
   return CSM_SUCCESS;
 }
 
+// The Pade base pair alone (schemes.py:446-464 pade8_cos_sin): k = 5,
+// s = 0 for every matrix, no selection, then the same chain as above.
+int csm_pade_core(int dtype, const void* a, void* cos_out, void* sin_out, int64_t batch, int n,
+                  int32_t* status, void* ws, size_t ws_bytes, void* stream_v) {
+  g_launches = 0;
+  if (dtype != CSM_F64 && dtype != CSM_F32 && dtype != CSM_F32_IN_F64_OUT)
+    return fail(CSM_ERR_ARG, "bad dtype");
+  if (batch < 0 || n < 0) return fail(CSM_ERR_ARG, "batch and n must be nonnegative");
+  const int eng = csm::engine();
+  if (ws_bytes < common_bytes(batch) + csm::tiled_workspace_bytes(batch, n, eng) + 256)
+    return fail(CSM_ERR_WORKSPACE, "workspace smaller than csm_pade_workspace_size()");
+  if (batch == 0) return CSM_SUCCESS;
+  if (!status || !ws || (n > 0 && (!a || !cos_out || !sin_out)))
+    return fail(CSM_ERR_ARG, "null pointer argument");
+  int rc = check_device();
+  if (rc) return rc;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  CommonWs w = carve(ws, batch);
+  cudaError_t e = csm::launch_fill_ks(w.kbuf, w.sbuf, status, batch, 5, stream);
+  if (e != cudaSuccess) return cuda_fail(e, "fill kernel");
+  ++g_launches;
+  if (n == 0) return CSM_SUCCESS;
+  e = csm::run_tiled(dtype, false, a, nullptr, cos_out, sin_out, batch, n, w.kbuf, w.sbuf, status,
+                     w.tiled, stream, &g_launches, 3, eng);
+  if (e != cudaSuccess) return cuda_fail(e, "pade chain");
+  return CSM_SUCCESS;
+}
+
 int csm_graph_safe(int dtype, int64_t batch, int n) {
   (void)dtype;
   if (batch < 0 || n < 0) return 0;

@@ -92,6 +92,10 @@ class CostLedger:
                 + self.lu_solves)
 
 
+# the Pade baseline's scheme id (schemes.py:87)
+PADE8 = SchemeId(SchemeFamily.PADE8, 5)
+
+
 @dataclass
 class CosSinResult:
     cos_part: DenseMatrix
