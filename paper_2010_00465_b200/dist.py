@@ -86,21 +86,92 @@ def gather_shards(local, group=None):
     return torch.cat([p[:s] for p, s in zip(parts, sizes)], dim=0)
 
 
-def cos_sin_sharded(a_full, precision=None, *, group=None, gather=True):
-    """cos/sin of a batch spread over the ranks of `group`: each rank computes
-    its contiguous shard on its own GPU (cos_sin_batched), and with
-    gather=True every rank receives the full results.  Returns
-    (cos, sin, k, s) -- full or this rank's shard."""
+def batch_costs(a_full, family=None, precision=None, t=None):
+    """Per-matrix product counts k + 2s of a batch, for load balancing only
+    (the results always use the device's own selection): induced 1-norms
+    (column sums) on whatever device holds the batch, then the library's
+    host-twin selection (csm_select_host, driver.py:64-88)."""
+    import torch
+
+    from .api import select_batch
+    from .records import Precision, SchemeFamily
+    family = family or SchemeFamily.COS_SIN_TAYLOR
+    precision = precision or Precision.DOUBLE
+    x = a_full if isinstance(a_full, torch.Tensor) else torch.from_numpy(np.asarray(a_full))
+    if x.shape[0] == 0:
+        return np.zeros(0)
+    if x.shape[-1] == 0:
+        return np.zeros(x.shape[0])
+    nrm = x.abs().to(torch.float64).sum(dim=-2).amax(dim=-1).cpu().numpy()
+    if t is not None:
+        tv = np.broadcast_to(np.asarray(t.cpu() if isinstance(t, torch.Tensor) else t,
+                                        dtype=np.float64).reshape(-1), nrm.shape)
+        nrm = tv * tv * nrm
+    k, sc, st = select_batch(nrm, family, precision)
+    return np.where(st == 0, k + 2 * sc, 0).astype(np.float64)
+
+
+def _rank_device():
+    import torch
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _sharded(a_full, t, precision, group, gather, balance, device, compute):
+    import torch
     import torch.distributed as dist
 
-    from .api import cos_sin_batched
-    from .records import Precision
+    from .records import Precision, SchemeFamily
     precision = precision or Precision.DOUBLE
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    lo, hi = shard_bounds(a_full.shape[0], world, rank)
-    rep = cos_sin_batched(a_full[lo:hi], precision)
-    if not gather:
-        return rep.cos_part, rep.sin_part, rep.k, rep.s
-    return (gather_shards(rep.cos_part, group), gather_shards(rep.sin_part, group),
-            gather_shards(rep.k, group), gather_shards(rep.s, group))
+    host_numpy = not isinstance(a_full, torch.Tensor)
+    B = int(a_full.shape[0])
+    if balance == "cost":
+        fam = SchemeFamily.WAVE_KERNEL if t is not None else SchemeFamily.COS_SIN_TAYLOR
+        lo, hi = cost_balanced_bounds(batch_costs(a_full, fam, precision, t), world)[rank]
+    elif balance == "count":
+        lo, hi = shard_bounds(B, world, rank)
+    else:
+        raise ValueError(f"balance must be 'cost' or 'count', got {balance!r}")
+    dev = torch.device(device) if device is not None else _rank_device()
+    shard = a_full[lo:hi]
+    shard = (torch.from_numpy(np.ascontiguousarray(shard)) if host_numpy else shard).to(dev)
+    t_shard = None
+    if t is not None:
+        tv = t if isinstance(t, torch.Tensor) else torch.as_tensor(
+            np.asarray(t, dtype=np.float64).reshape(-1))
+        if tv.numel() == 1:
+            tv = tv.reshape(1).expand(B)
+        t_shard = tv[lo:hi].to(device=dev, dtype=torch.float64)
+    rep = compute(shard, t_shard, precision)
+    out = [rep.cos_part, rep.sin_part,
+           torch.as_tensor(rep.k, device=dev), torch.as_tensor(rep.s, device=dev)]
+    if gather:
+        out = [gather_shards(x, group) for x in out]
+    if host_numpy:
+        out = [x.cpu().numpy() for x in out]
+    return tuple(out)
+
+
+def cos_sin_sharded(a_full, precision=None, *, group=None, gather=True, balance="cost",
+                    device=None):
+    """cos/sin of a batch (B, n, n) replicated on every rank of `group`:
+    each rank computes one contiguous shard on its own GPU (cos_sin_batched)
+    with no collective on the data path.  balance='cost' cuts the batch at
+    equal total product count k + 2s (batch_costs), 'count' at equal matrix
+    count.  With gather=True every rank receives the full results (one
+    all-gather per output).  Returns (cos, sin, k, s) -- full or this
+    rank's shard -- as numpy arrays for numpy input, else tensors on the
+    rank's device."""
+    from .api import cos_sin_batched
+    return _sharded(a_full, None, precision, group, gather, balance, device,
+                    lambda x, _t, p: cos_sin_batched(x, p))
+
+
+def wave_cos_sin_sharded(a_full, t, precision=None, *, group=None, gather=True,
+                         balance="cost", device=None):
+    """The wave pair c(t^2 A), s(t, A) of a batch sharded like
+    cos_sin_sharded (t: one scalar or one value per matrix)."""
+    from .api import wave_cos_sin_batched
+    return _sharded(a_full, t, precision, group, gather, balance, device,
+                    lambda x, tt, p: wave_cos_sin_batched(x, tt, p))
