@@ -261,6 +261,50 @@ int csm_slab_op_peer(const void* op, double* slab, int M, int NP, int row0,
                      void* cos_out, void* sin_out, int out_f32, void* scratch,
                      size_t scratch_bytes, void* stream);
 
+/* ---- The distributed chain driven from C (cfg5 across GPUs) -------------
+ * csm_dist_cos_sin: cos / sin of ONE n x n float64 matrix `a` (device,
+ * replicated on every rank) over the ranks of an NCCL communicator, block
+ * row: rank r computes rows [r M, r M + M), M = n / W, into cos_rows /
+ * sin_rows (device, M x n).  Selection, the Taylor chain and the doubling
+ * steps run as in csm_cos_sin (driver.py:108-123); every product is
+ * out_rows = L_rows R_full on the FP64 DMMA tiled kernel, with R_full
+ * all-gathered by ncclAllGather on a side stream while the rank contracts
+ * its own rows of R (K-split), and a gathered operand is reused until its
+ * slot is rewritten (distchain.py's schedule).  comm = NULL runs W = 1.
+ * n must be a multiple of 64 W.  k / s / status: host outputs (status as
+ * in csm_cos_sin; on a non-zero status nothing is computed).  Stream
+ * ordered; the call synchronises `stream` twice (selection read-back and
+ * op-table staging).  NCCL is resolved at run time from the process (or
+ * libnccl.so.2); it is not a link dependency.  All ranks must call with
+ * the same a, n and precision.  workspace: csm_dist_workspace_size(n, W,
+ * flags) bytes per rank.
+ *   flags: CSM_DIST_FORCE_GATHER gathers every non-A right operand even at
+ *   W = 1 (exercises the NCCL path on one GPU).
+ * csm_dist_cos_sin_virtual: the same schedule for W virtual ranks in this
+ * process (every slab on the current device, the all-gather as device
+ * copies) -- the K-split products and the gather cache on one GPU.
+ * cos / sin: full n x n outputs; workspace: W x csm_dist_workspace_size(n,
+ * W, CSM_DIST_FORCE_GATHER).
+ * csm_dist_last_stats: gathers and products of the calling thread's last
+ * distributed call. */
+#if !defined(NCCL_H_)
+typedef struct ncclComm* ncclComm_t;
+#endif
+#define CSM_DIST_FORCE_GATHER 1
+size_t csm_dist_workspace_size(int n, int world, int flags);
+int csm_dist_cos_sin(int precision, const double* a, double* cos_rows, double* sin_rows, int n,
+                     ncclComm_t comm, int flags, int32_t* k, int32_t* s, int32_t* status,
+                     void* workspace, size_t ws_bytes, void* stream);
+int csm_dist_cos_sin_virtual(int precision, const double* a, double* cos_out, double* sin_out,
+                             int n, int world, int32_t* k, int32_t* s, int32_t* status,
+                             void* workspace, size_t ws_bytes, void* stream);
+int csm_dist_last_stats(int32_t* gathers, int32_t* products);
+/* NCCL communicator helpers for callers without their own NCCL setup
+ * (id: 128 bytes, made on one rank and shared out of band). */
+int csm_nccl_get_unique_id(void* id);
+int csm_nccl_comm_init_rank(ncclComm_t* comm, int nranks, const void* id, int rank);
+int csm_nccl_comm_destroy(ncclComm_t comm);
+
 /* 1 when csm_cos_sin / csm_wave for (dtype, batch, n) never synchronises
  * the host (K1, or K1c without the side chain), so the call can be
  * captured in a CUDA graph; 0 for the tiled chain (it reads (k, s) back to

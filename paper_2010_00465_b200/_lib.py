@@ -70,6 +70,15 @@ SIGNATURES = {
                                 _vp, _vp, _i32, _vp, _sz, _vp]),
     "csm_slab_op_pair": (_i32, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _dp, _i32,
                                 _vp, _vp, _i32, _vp, _sz, _vp]),
+    "csm_dist_workspace_size": (_sz, [_i32, _i32, _i32]),
+    "csm_dist_cos_sin": (_i32, [_i32, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _sz,
+                                _vp]),
+    "csm_dist_cos_sin_virtual": (_i32, [_i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp, _sz,
+                                        _vp]),
+    "csm_dist_last_stats": (_i32, [_vp, _vp]),
+    "csm_nccl_get_unique_id": (_i32, [_vp]),
+    "csm_nccl_comm_init_rank": (_i32, [_vp, _i32, _vp, _i32]),
+    "csm_nccl_comm_destroy": (_i32, [_vp]),
     "csm_graph_safe": (_i32, [_i32, _i64, _i32]),
     "csm_set_engine": (_i32, [_i32]),
     "csm_get_engine": (_i32, []),

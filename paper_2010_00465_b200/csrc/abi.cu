@@ -859,6 +859,127 @@ int csm_pade_core(int dtype, const void* a, void* cos_out, void* sin_out, int64_
   return CSM_SUCCESS;
 }
 
+// ---- distributed chain (distchain.cu) ------------------------------------
+namespace {
+thread_local int32_t g_dist_gathers = 0, g_dist_products = 0;
+
+int dist_common(int precision, const double* a, int n, int world, size_t ws_bytes, size_t need) {
+  if (precision != CSM_PREC_DOUBLE && precision != CSM_PREC_SINGLE)
+    return fail(CSM_ERR_ARG, "bad precision");
+  if (world < 1) return fail(CSM_ERR_ARG, "world must be >= 1");
+  if (n <= 0 || n % (64 * world)) return fail(CSM_ERR_ARG, "n must be a positive multiple of 64 x world");
+  if (!a) return fail(CSM_ERR_ARG, "null pointer argument");
+  if (ws_bytes < need) return fail(CSM_ERR_WORKSPACE, "workspace smaller than csm_dist_workspace_size()");
+  return check_device();
+}
+}  // namespace
+
+size_t csm_dist_workspace_size(int n, int world, int flags) {
+  if (n <= 0 || world < 1 || n % world) return 0;
+  return csm::dc::rank_bytes(n, world, world > 1 || (flags & CSM_DIST_FORCE_GATHER));
+}
+
+int csm_dist_cos_sin(int precision, const double* a, double* cos_rows, double* sin_rows, int n,
+                     ncclComm_t comm, int flags, int32_t* k, int32_t* s, int32_t* status,
+                     void* ws, size_t ws_bytes, void* stream_v) {
+  g_launches = 0;
+  g_dist_gathers = g_dist_products = 0;
+  int world = 1, rank = 0;
+  const bool force = (flags & CSM_DIST_FORCE_GATHER) != 0;
+  if (comm) {
+    if (!csm::dc::nccl().ok) return fail(CSM_ERR_ARG, "NCCL entry points not found in the process or libnccl.so.2");
+    if (csm::dc::nccl().comm_count(comm, &world) != 0 ||
+        csm::dc::nccl().comm_user_rank(comm, &rank) != 0)
+      return fail(CSM_ERR_ARG, "invalid NCCL communicator");
+  } else if (force) {
+    return fail(CSM_ERR_ARG, "CSM_DIST_FORCE_GATHER needs a communicator");
+  }
+  int rc = dist_common(precision, a, n, world, ws_bytes, csm_dist_workspace_size(n, world, flags));
+  if (rc) return rc;
+  if (!cos_rows || !sin_rows || !k || !s || !status || !ws) return fail(CSM_ERR_ARG, "null pointer argument");
+  csm::dc::Exchange ex;
+  ex.comm = comm;
+  ex.world = world;
+  csm::dc::Result res;
+  std::string why;
+  void* wsv[1] = {ws};
+  double* cr[1] = {cos_rows};
+  double* sr[1] = {sin_rows};
+  cudaError_t e = csm::dc::run(precision, a, n, world, rank, 1, wsv, cr, sr, ex, force,
+                               static_cast<cudaStream_t>(stream_v), &res, &g_launches, &why);
+  *k = res.k;
+  *s = res.s;
+  *status = res.status;
+  g_dist_gathers = res.gathers;
+  g_dist_products = res.products;
+  if (e != cudaSuccess) return why.empty() ? cuda_fail(e, "distributed chain") : fail(CSM_ERR_CUDA, why);
+  return CSM_SUCCESS;
+}
+
+int csm_dist_cos_sin_virtual(int precision, const double* a, double* cos_out, double* sin_out,
+                             int n, int world, int32_t* k, int32_t* s, int32_t* status, void* ws,
+                             size_t ws_bytes, void* stream_v) {
+  g_launches = 0;
+  g_dist_gathers = g_dist_products = 0;
+  const size_t per = csm_dist_workspace_size(n, world, CSM_DIST_FORCE_GATHER);
+  int rc = dist_common(precision, a, n, world, ws_bytes, per * static_cast<size_t>(world));
+  if (rc) return rc;
+  if (!cos_out || !sin_out || !k || !s || !status || !ws) return fail(CSM_ERR_ARG, "null pointer argument");
+  std::vector<void*> wsv(world);
+  std::vector<double*> cr(world), sr(world);
+  const size_t M = static_cast<size_t>(n) / world;
+  for (int q = 0; q < world; ++q) {
+    wsv[q] = static_cast<char*>(ws) + q * per;
+    cr[q] = cos_out + q * M * n;
+    sr[q] = sin_out + q * M * n;
+  }
+  csm::dc::Exchange ex;
+  ex.world = world;
+  csm::dc::Result res;
+  std::string why;
+  cudaError_t e = csm::dc::run(precision, a, n, world, 0, world, wsv.data(), cr.data(), sr.data(),
+                               ex, world == 1, static_cast<cudaStream_t>(stream_v), &res,
+                               &g_launches, &why);
+  *k = res.k;
+  *s = res.s;
+  *status = res.status;
+  g_dist_gathers = res.gathers;
+  g_dist_products = res.products;
+  if (e != cudaSuccess) return why.empty() ? cuda_fail(e, "virtual distributed chain") : fail(CSM_ERR_CUDA, why);
+  return CSM_SUCCESS;
+}
+
+int csm_dist_last_stats(int32_t* gathers, int32_t* products) {
+  if (!gathers || !products) return fail(CSM_ERR_ARG, "null pointer argument");
+  *gathers = g_dist_gathers;
+  *products = g_dist_products;
+  return CSM_SUCCESS;
+}
+
+int csm_nccl_get_unique_id(void* id) {
+  if (!id) return fail(CSM_ERR_ARG, "null pointer argument");
+  if (!csm::dc::nccl().ok) return fail(CSM_ERR_ARG, "NCCL entry points not found");
+  const int rc = csm::dc::nccl_unique_id(id);
+  return rc ? fail(CSM_ERR_CUDA, "ncclGetUniqueId failed: " + std::to_string(rc)) : CSM_SUCCESS;
+}
+
+int csm_nccl_comm_init_rank(ncclComm_t* comm, int nranks, const void* id, int rank) {
+  if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail(CSM_ERR_ARG, "bad argument");
+  if (!csm::dc::nccl().ok) return fail(CSM_ERR_ARG, "NCCL entry points not found");
+  void* c = nullptr;
+  const int rc = csm::dc::nccl_comm_init(&c, nranks, id, rank);
+  if (rc) return fail(CSM_ERR_CUDA, "ncclCommInitRank failed: " + std::to_string(rc));
+  *comm = static_cast<ncclComm_t>(c);
+  return CSM_SUCCESS;
+}
+
+int csm_nccl_comm_destroy(ncclComm_t comm) {
+  if (!comm) return CSM_SUCCESS;
+  if (!csm::dc::nccl().ok) return fail(CSM_ERR_ARG, "NCCL entry points not found");
+  const int rc = csm::dc::nccl().comm_destroy(comm);
+  return rc ? fail(CSM_ERR_CUDA, "ncclCommDestroy failed: " + std::to_string(rc)) : CSM_SUCCESS;
+}
+
 int csm_graph_safe(int dtype, int64_t batch, int n) {
   (void)dtype;
   if (batch < 0 || n < 0) return 0;

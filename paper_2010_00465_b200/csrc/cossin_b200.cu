@@ -3,6 +3,7 @@
 #include "k0_select.cu"
 #include "fused64.cu"
 #include "tiled.cu"
+#include "distchain.cu"
 #include "ddref.cu"
 #include "residual.cu"
 #include "abi.cu"

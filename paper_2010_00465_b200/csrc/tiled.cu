@@ -116,6 +116,14 @@ struct LaunchArgs {
   // (flag index = item - only_base); the others leave at once.
   const unsigned* only;
   int only_base;
+  // K-split of a slab product, so the all-gather of its right operand
+  // overlaps compute (csm_dist_cos_sin): ksplit 1 contracts only k in this
+  // rank's own rows [row0, row0 + M), reading them from its own slab slot
+  // op.rhs, and stores the raw product to part; ksplit 2 contracts the
+  // complementary k range from rhs_full and adds part before the epilogue;
+  // 0 is the whole contraction.  part: M x NP doubles per launch item y.
+  int ksplit;
+  double* part;
 };
 
 // Slot sl of matrix b (slot 0 may alias the caller's input).
@@ -285,6 +293,9 @@ __global__ void __launch_bounds__(THREADS, CSM_TILED_MINB) gemm_epi_kernel(const
     const double* R = (args.rhs_full ? args.rhs_full : slot(op.rhs)) + static_cast<size_t>(tn) * BN;
     // row k0 of the right operand (a BK-row stage never crosses a part: M % 64 == 0)
     auto rhs_rows = [&](int k0) -> const double* {
+      if (args.ksplit == 1)  // own rows of the (not yet gathered) right operand
+        return slot(op.rhs) + static_cast<size_t>(k0 - args.row0) * NP +
+               static_cast<size_t>(tn) * BN;
       if (args.rhs_parts) {
         const int part = k0 / M;
         return args.rhs_parts[part] + static_cast<size_t>(op.rhs) * slotsz +
@@ -317,10 +328,17 @@ __global__ void __launch_bounds__(THREADS, CSM_TILED_MINB) gemm_epi_kernel(const
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    const int nk = NP / BK;
+    // k-stage j -> contraction index (K-split: own rows, or all but them)
+    const int nk = (args.ksplit == 0 ? NP : (args.ksplit == 1 ? M : NP - M)) / BK;
+    auto kof = [&](int j) -> int {
+      const int k = j * BK;
+      if (args.ksplit == 1) return args.row0 + k;
+      if (args.ksplit == 2 && k >= args.row0) return k + M;
+      return k;
+    };
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
-      if (s < nk) load_stage(s, s * BK);
+      if (s < nk) load_stage(s, kof(s));
       commit();
     }
     for (int kt = 0; kt < nk; ++kt) {
@@ -328,7 +346,7 @@ __global__ void __launch_bounds__(THREADS, CSM_TILED_MINB) gemm_epi_kernel(const
       __syncthreads();
       {
         const int nxt = kt + STAGES - 1;
-        if (nxt < nk) load_stage(nxt % STAGES, nxt * BK);
+        if (nxt < nk) load_stage(nxt % STAGES, kof(nxt));
         commit();
       }
       const double* as = As + (kt % STAGES) * A_STAGE;
@@ -358,6 +376,23 @@ __global__ void __launch_bounds__(THREADS, CSM_TILED_MINB) gemm_epi_kernel(const
             make_double2(acc[mi][ni][0], acc[mi][ni][1]);
     __syncthreads();
 
+    if (args.ksplit != 0) {  // partial product: raw tile out, or added in
+      double* pt = args.part + static_cast<size_t>(blockIdx.y) * slotsz +
+                   static_cast<size_t>(tm) * BM * NP + static_cast<size_t>(tn) * BN;
+      for (int p = tid; p < BM * BN / 2; p += THREADS) {
+        const int rr = p >> 5, cc = (p & 31) * 2;
+        double2* e = reinterpret_cast<double2*>(E + rr * LDE + cc);
+        double2* g = reinterpret_cast<double2*>(pt + static_cast<size_t>(rr) * NP + cc);
+        if (args.ksplit == 1) {
+          *g = *e;
+        } else {
+          const double2 x = *g;
+          *e = make_double2(e->x + x.x, e->y + x.y);
+        }
+      }
+      if (args.ksplit == 1) return;
+      __syncthreads();
+    }
     epilogue_tile(args, op, b, tm, tn, E);
   }
 }

@@ -392,3 +392,132 @@ def cos_sin_distributed_peer(a, precision: Precision = Precision.DOUBLE, *, grou
     dist.all_gather_into_tensor(cfull, cos_rows, group=group)
     dist.all_gather_into_tensor(sfull, sin_rows, group=group)
     return cfull, sfull, stats
+
+
+# ---------------------------------------------------------------------------
+# The C driver (csm_dist_cos_sin, csrc/distchain.cu): the same schedule run
+# from C++ over an NCCL communicator, with every first gather of an operand
+# overlapped with the rank's own-rows part of its product (K-split).
+
+_NCCL_COMMS: dict = {}
+
+
+def nccl_comm(group=None):
+    """An NCCL communicator (ncclComm_t) over the ranks of `group` for the C
+    driver: rank 0 makes the unique id (csm_nccl_get_unique_id),
+    torch.distributed broadcasts its 128 bytes, every rank joins
+    (csm_nccl_comm_init_rank).  Cached per group; None at world 1."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return None
+    grp = group if group is not None else dist.group.WORLD
+    key = grp.group_name
+    if key not in _NCCL_COMMS:
+        L = _lib.lib()
+        uid = ctypes.create_string_buffer(128)
+        if dist.get_rank(group) == 0:
+            _lib.check(L.csm_nccl_get_unique_id(uid), "csm_nccl_get_unique_id")
+        box = [uid.raw]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(grp, 0), group=group)
+        uid = ctypes.create_string_buffer(box[0], 128)
+        comm = ctypes.c_void_p()
+        _lib.check(L.csm_nccl_comm_init_rank(ctypes.byref(comm), dist.get_world_size(group),
+                                             uid, dist.get_rank(group)),
+                   "csm_nccl_comm_init_rank")
+        _NCCL_COMMS[key] = comm
+    return _NCCL_COMMS[key]
+
+
+_DIST_FORCE_GATHER = 1  # CSM_DIST_FORCE_GATHER
+
+
+def _dist_stats(k, s):
+    g, p = ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(_lib.lib().csm_dist_last_stats(ctypes.byref(g), ctypes.byref(p)),
+               "csm_dist_last_stats")
+    return DistStats(int(k), int(s), g.value, p.value, int(_lib.lib().csm_last_launch_count()))
+
+
+def _status_raise(st: int):
+    from .api import _status_error
+    if st != 0:
+        raise _status_error(st, float("nan"))
+
+
+def cos_sin_distributed_c(a, precision: Precision = Precision.DOUBLE, *, group=None,
+                          comm=None, gather_outputs: bool = True, force_gather: bool = False):
+    """cos_sin_distributed through the C driver csm_dist_cos_sin: `a`
+    replicated on every rank (CUDA float64, n a multiple of 64 W), the
+    communicator from nccl_comm(group) unless given.  force_gather makes
+    even W = 1 gather through NCCL (tests the NCCL path on one GPU).
+    Returns (cos, sin, stats) like cos_sin_distributed."""
+    import torch
+    import torch.distributed as dist
+    n = int(a.shape[0])
+    if a.shape != (n, n) or a.dtype != torch.float64 or not a.is_cuda:
+        raise ValueError("expected a square float64 CUDA tensor")
+    if comm is None:
+        comm = nccl_comm(group)
+        if comm is None and force_gather:  # a one-rank communicator
+            L = _lib.lib()
+            uid = ctypes.create_string_buffer(128)
+            _lib.check(L.csm_nccl_get_unique_id(uid), "csm_nccl_get_unique_id")
+            comm = ctypes.c_void_p()
+            _lib.check(L.csm_nccl_comm_init_rank(ctypes.byref(comm), 1, uid, 0),
+                       "csm_nccl_comm_init_rank")
+            _NCCL_COMMS.setdefault("__single__", comm)
+            comm = _NCCL_COMMS["__single__"]
+    world = dist.get_world_size(group) if (comm is not None and dist.is_initialized()) else 1
+    flags = _DIST_FORCE_GATHER if force_gather else 0
+    a = a.contiguous()
+    M = n // world
+    L = _lib.lib()
+    dev = a.device
+    cos_rows = torch.empty((M, n), dtype=torch.float64, device=dev)
+    sin_rows = torch.empty_like(cos_rows)
+    ws_bytes = int(L.csm_dist_workspace_size(n, world, flags))
+    ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=dev)
+    k, s, st = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    vp = ctypes.c_void_p
+    _lib.check(L.csm_dist_cos_sin(_PREC_CODE[precision], vp(a.data_ptr()),
+                                  vp(cos_rows.data_ptr()), vp(sin_rows.data_ptr()), n, comm,
+                                  flags, ctypes.byref(k), ctypes.byref(s), ctypes.byref(st),
+                                  vp(ws.data_ptr()), ws_bytes,
+                                  vp(int(torch.cuda.current_stream().cuda_stream))),
+               "csm_dist_cos_sin")
+    _status_raise(st.value)
+    stats = _dist_stats(k.value, s.value)
+    if not gather_outputs or world == 1:
+        return cos_rows, sin_rows, stats
+    cfull = torch.empty((n, n), dtype=torch.float64, device=dev)
+    sfull = torch.empty_like(cfull)
+    dist.all_gather_into_tensor(cfull, cos_rows, group=group)
+    dist.all_gather_into_tensor(sfull, sin_rows, group=group)
+    return cfull, sfull, stats
+
+
+def cos_sin_virtual_gather(a, world: int, precision: Precision = Precision.DOUBLE):
+    """The C driver's schedule for `world` virtual ranks on this GPU
+    (csm_dist_cos_sin_virtual): K-split products, the gather cache and
+    the all-gathers (as device copies) of the multi-GPU run, on one device.
+    Returns (cos, sin, stats)."""
+    import torch
+    n = int(a.shape[0])
+    if a.shape != (n, n) or a.dtype != torch.float64 or not a.is_cuda:
+        raise ValueError("expected a square float64 CUDA tensor")
+    a = a.contiguous()
+    L = _lib.lib()
+    cos = torch.empty((n, n), dtype=torch.float64, device=a.device)
+    sin = torch.empty_like(cos)
+    ws_bytes = world * int(L.csm_dist_workspace_size(n, world, _DIST_FORCE_GATHER))
+    ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device=a.device)
+    k, s, st = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    vp = ctypes.c_void_p
+    _lib.check(L.csm_dist_cos_sin_virtual(_PREC_CODE[precision], vp(a.data_ptr()),
+                                          vp(cos.data_ptr()), vp(sin.data_ptr()), n, world,
+                                          ctypes.byref(k), ctypes.byref(s), ctypes.byref(st),
+                                          vp(ws.data_ptr()), ws_bytes,
+                                          vp(int(torch.cuda.current_stream().cuda_stream))),
+               "csm_dist_cos_sin_virtual")
+    _status_raise(st.value)
+    return cos, sin, _dist_stats(k.value, s.value)

@@ -164,3 +164,32 @@ def test_thread_engine_override_is_per_thread():
         assert csm.get_engine() == "dmma"
     assert csm.get_engine() == "dmma"
     assert seen["other"] == "dmma"  # another thread sees the process default
+
+
+def test_dist_workspace_sizes_and_argument_errors():
+    """csm_dist_workspace_size (host arithmetic, no device): slab + partial
+    products + staging, plus the gather pool only when ranks gather; and
+    argument errors are reported before any device work."""
+    import ctypes
+
+    from paper_2010_00465_b200 import _lib
+    L = _lib.lib()
+    n, w = 8192, 8
+    M = n // w
+    base = L.csm_dist_workspace_size(n, w, 0)
+    assert base > (9 + 2) * M * n * 8
+    one = L.csm_dist_workspace_size(n, 1, 0)
+    assert (9 + 2) * n * n * 8 < one < (9 + 2) * n * n * 8 + (1 << 20)  # no pool at W = 1
+    forced = L.csm_dist_workspace_size(n, 1, 1)
+    pool = forced - one
+    assert pool % (n * n * 8) == 0 and 1 <= pool // (n * n * 8) <= 5
+    assert L.csm_dist_workspace_size(100, 3, 0) == 0
+    k = ctypes.c_int32()
+    for n_bad in (0, 100):
+        rc = L.csm_dist_cos_sin_virtual(0, ctypes.c_void_p(1), ctypes.c_void_p(1),
+                                        ctypes.c_void_p(1), n_bad, 2, ctypes.byref(k),
+                                        ctypes.byref(k), ctypes.byref(k), ctypes.c_void_p(1),
+                                        1 << 40, None)
+        assert rc == _lib.ERR_ARG
+    g, p = ctypes.c_int32(), ctypes.c_int32()
+    assert L.csm_dist_last_stats(ctypes.byref(g), ctypes.byref(p)) == 0

@@ -186,3 +186,89 @@ def test_peer_mode_symmetric_memory_single_rank(cuda):
     out = subprocess.run([sys.executable, os.path.join(root, "tools", "peer_smoke.py")],
                          capture_output=True, text=True, timeout=300, env=env, cwd=root)
     assert "peer == gather: True True" in out.stdout, out.stdout + out.stderr[-2000:]
+
+
+# -- the C driver (csm_dist_cos_sin, csrc/distchain.cu) ----------------------
+
+def _cfg5_like(n, seed=0):
+    g = np.random.default_rng(seed).standard_normal((n, n))
+    return 20.0 * (g + g.T) / (2.0 * np.sqrt(n))
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_c_driver_world1_bitwise_python_driver(cuda):
+    """csm_dist_cos_sin at W = 1 (no communicator) runs the same products
+    as the Python gather-mode driver: bit-identical outputs, same (k, s),
+    gathers and product count."""
+    from paper_2010_00465_b200 import distchain
+    a = torch.from_numpy(_cfg5_like(1024)).to(cuda)
+    c, s, st = distchain.cos_sin_distributed_c(a)
+    c1, s1, st1 = distchain.cos_sin_distributed(a)
+    assert (st.k, st.s) == (st1.k, st1.s)
+    assert st.products == st1.products == st.k + 2 * st.s
+    assert st.gathers == 0  # W = 1 reads the slab itself
+    assert torch.equal(c, c1) and torch.equal(s, s1)
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_c_driver_nccl_forced_gathers_world1(cuda):
+    """The NCCL path of the C driver on one GPU: a one-rank communicator
+    (csm_nccl_get_unique_id / csm_nccl_comm_init_rank) and every non-A
+    right operand all-gathered by ncclAllGather into the gather pool, with
+    the cache of distchain.py (same gather count): bit-identical."""
+    from paper_2010_00465_b200 import distchain
+    a = torch.from_numpy(_cfg5_like(1024, seed=1)).to(cuda)
+    c, s, st = distchain.cos_sin_distributed_c(a, force_gather=True)
+    c1, s1, st1 = distchain.cos_sin_distributed(a)
+    assert st.gathers == st1.gathers > 0
+    assert torch.equal(c, c1) and torch.equal(s, s1)
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_c_driver_virtual_ranks_k_split(cuda, world):
+    """W virtual ranks on this GPU (csm_dist_cos_sin_virtual): every first
+    gather of an operand is overlapped with the K-split product (own rows
+    first, then the rest plus the partial sum).  Same schedule (gathers,
+    products) as the Python driver; outputs within the reference's own
+    noise of the oracle and of the unsplit chain."""
+    from paper_2010_00465_b200 import distchain
+    from tests._util import permuted_noise
+    n = 1024
+    a_np = _cfg5_like(n, seed=2)
+    a = torch.from_numpy(a_np).to(cuda)
+    c, s, st = distchain.cos_sin_virtual_gather(a, world)
+    c1, s1, st1 = distchain.cos_sin_distributed(a)
+    assert (st.k, st.s, st.gathers, st.products) == (st1.k, st1.s, st1.gathers, st1.products)
+    (rc, rs, k, sc), noise = permuted_noise(orc.cos_sin, a_np, np.random.default_rng(3))
+    assert (st.k, st.s) == (k, sc)
+    gate = max(1e-12, 4.0 * noise)
+    assert rel1(c.cpu().numpy(), rc) <= gate and rel1(s.cpu().numpy(), rs) <= gate
+    assert rel1(c.cpu().numpy(), c1.cpu().numpy()) <= gate
+    # K-split changes only the summation order: symmetric input, symmetric cos
+    assert float((c - c.T).abs().max() / c.abs().max()) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_c_driver_errors(cuda):
+    import ctypes
+
+    from paper_2010_00465_b200 import _lib, distchain
+    with pytest.raises(ValueError):
+        distchain.cos_sin_virtual_gather(torch.zeros((64, 64), device=cuda), 2)  # not f64
+    with pytest.raises(RuntimeError, match="multiple of 64"):
+        distchain.cos_sin_virtual_gather(torch.zeros((192, 192), dtype=torch.float64,
+                                                     device=cuda), 2)
+    bad = torch.from_numpy(_cfg5_like(128)).to(cuda)
+    bad[3, 5] = float("nan")
+    import paper_2010_00465_b200 as csm
+    with pytest.raises(csm.MatrixInputError):
+        distchain.cos_sin_distributed_c(bad)
+    L = _lib.lib()
+    k = ctypes.c_int32()
+    rc = L.csm_dist_cos_sin(0, ctypes.c_void_p(bad.data_ptr()), None, None, 128, None, 1,
+                            ctypes.byref(k), ctypes.byref(k), ctypes.byref(k), None, 0, None)
+    assert rc == _lib.ERR_ARG  # CSM_DIST_FORCE_GATHER without a communicator
