@@ -214,8 +214,9 @@ cudaError_t launch(const tk::Op* d_ops, const Staged* d_st, int op, int nops, do
   A.row0 = row0;
   A.ksplit = ksplit;
   A.part = part;
+  tk::set_tma(A, static_cast<size_t>(tk::NSLOT) * M, static_cast<size_t>(M));
   dim3 grid(static_cast<unsigned>((M / tk::BM) * (n / tk::BN)), static_cast<unsigned>(nops), 1);
-  tk::gemm_epi_kernel<<<grid, tk::THREADS, tk::SMEM, st>>>(A);
+  tk::gemm_epi_kernel<<<grid, tk::GTHREADS, tk::SMEM, st>>>(A);
   ++*launches;
   return cudaGetLastError();
 }

@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la,
 template <int NM>
 __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, const OzArgs oz,
                                                       const OzConst C) {
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(1024) double sm[];
   __shared__ Op op;
   __shared__ int sh_b;
   const int tid = threadIdx.x;
@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, co
       for (int rr = 0; rr < BM && tm * BM + rr < la.n; ++rr) sum += fabs(E[rr * LDE + tid]);
     oz.csumC[(static_cast<size_t>(ci) * (M / BM) + tm) * NP + c] = sum;
   }
-  epilogue_tile(la, op, sh_b, tm, tn, E);
+  epilogue_tile<THREADS>(la, op, sh_b, tm, tn, E);
 }
 
 // Accuracy guard of one product item (grid (nitems), 256 threads).  The

@@ -24,6 +24,8 @@
 // Reference mapping: schemes.py:264-361 (chains), :376-395 / :411-430
 // (trig / wave use), driver.py:91-98 (doubling), driver.py:115/:139
 // (scaling), matcore.py:107-121 (linear combinations, fused here).
+#include <cuda.h>  // CUtensorMap (types only; the encoder is fetched at run time)
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -124,6 +126,14 @@ struct LaunchArgs {
   // 0 is the whole contraction.  part: M x NP doubles per launch item y.
   int ksplit;
   double* part;
+  // TMA staging (tma = 1): 2-D tensor maps over the slots (rows of every
+  // slot of every matrix stacked: row (b mat_stride + sl M NP) / NP + r),
+  // the slot-0 alias in0 and the gathered rhs_full.  *L: 64 x 16 boxes with
+  // the 128-byte swizzle (left-operand tile); *R: 16 x 8 boxes with the
+  // 64-byte swizzle (8 per right-operand tile), both conflict-free for the
+  // DMMA fragment loads.  tma = 0 keeps the cp.async staging (peer mode).
+  int tma;
+  CUtensorMap tm_wsL, tm_wsR, tm_in0L, tm_in0R, tm_rhsR;
 };
 
 // Slot sl of matrix b (slot 0 may alias the caller's input).
@@ -137,6 +147,7 @@ __device__ __forceinline__ double* slot_ptr(const LaunchArgs& args, int b, int s
 // The op's linear combinations for output tile (tm, tn) of matrix b, from
 // the product tile E ([BM][LDE] in shared memory): row-contiguous
 // (coalesced) global reads of the slot terms and writes of the outputs.
+template <int NT>
 __device__ __forceinline__ void epilogue_tile(const LaunchArgs& args, const Op& op, int b,
                                               int tm, int tn, const double* E) {
   const int tid = threadIdx.x;
@@ -156,14 +167,14 @@ __device__ __forceinline__ void epilogue_tile(const LaunchArgs& args, const Op& 
   // independent loads before its FMAs, so the workspace reads (HBM for
   // large batches) overlap instead of exposing one latency per term.
   constexpr int PB = CSM_TILED_PB;
-  static_assert((BM * BN / 2) % (PB * THREADS) == 0, "pair groups tile the output");
-  for (int p0 = tid; p0 < BM * BN / 2; p0 += PB * THREADS) {
+  static_assert((BM * BN / 2) % (PB * NT) == 0, "pair groups tile the output");
+  for (int p0 = tid; p0 < BM * BN / 2; p0 += PB * NT) {
     size_t off[PB];
     int ecol[PB];
     double o0[PB][2], o1[PB][2];  // outputs 0 and 1 (OUTj terms of later outputs)
 #pragma unroll
     for (int m = 0; m < PB; ++m) {
-      const int p = p0 + m * THREADS;
+      const int p = p0 + m * NT;
       const int rr = p >> 5, cc = (p & 31) * 2;  // 32 pairs per tile row
       off[m] = static_cast<size_t>(r0 + rr) * NP + c0 + cc;
       ecol[m] = rr * LDE + cc;
@@ -195,7 +206,7 @@ __device__ __forceinline__ void epilogue_tile(const LaunchArgs& args, const Op& 
               const double2 av = *reinterpret_cast<const double2*>(E + ecol[m]);
               x0 = av.x; x1 = av.y;
             } else if (src == SRC_I) {
-              const int p = p0 + m * THREADS;
+              const int p = p0 + m * NT;
               const int rg = r0 + (p >> 5) + args.row0, c = c0 + (p & 31) * 2;
               x0 = (rg == c) ? 1.0 : 0.0;
               x1 = (rg == c + 1) ? 1.0 : 0.0;
@@ -225,7 +236,7 @@ __device__ __forceinline__ void epilogue_tile(const LaunchArgs& args, const Op& 
         void* dst = os.final == FIN_COS ? args.cout : args.sout;
 #pragma unroll
         for (int m = 0; m < PB; ++m) {
-          const int p = p0 + m * THREADS;
+          const int p = p0 + m * NT;
           const int r = r0 + (p >> 5), c = c0 + (p & 31) * 2;
           if (r >= n) continue;
           const double v0 = v[m][0], v1 = v[m][1];
@@ -249,18 +260,96 @@ __device__ __forceinline__ void epilogue_tile(const LaunchArgs& args, const Op& 
   }
 }
 
+// After the product: a K-split partial tile goes out raw (ksplit 1) or is
+// added in (ksplit 2) before the epilogue.
+template <int NT>
+__device__ __forceinline__ void finish_tile(const LaunchArgs& args, const Op& op, int b, int tm,
+                                            int tn, double* E, size_t slotsz) {
+  const int tid = threadIdx.x;
+  if (args.ksplit != 0) {  // partial product: raw tile out, or added in
+    const int NP = args.NP;
+    double* pt = args.part + static_cast<size_t>(blockIdx.y) * slotsz +
+                 static_cast<size_t>(tm) * BM * NP + static_cast<size_t>(tn) * BN;
+    for (int p = tid; p < BM * BN / 2; p += NT) {
+      const int rr = p >> 5, cc = (p & 31) * 2;
+      double2* e = reinterpret_cast<double2*>(E + rr * LDE + cc);
+      double2* g = reinterpret_cast<double2*>(pt + static_cast<size_t>(rr) * NP + cc);
+      if (args.ksplit == 1) {
+        *g = *e;
+      } else {
+        const double2 x = *g;
+        *e = make_double2(e->x + x.x, e->y + x.y);
+      }
+    }
+    if (args.ksplit == 1) return;
+    __syncthreads();
+  }
+  epilogue_tile<NT>(args, op, b, tm, tn, E);
+}
+
 // One 64x64 output tile of one matrix: acc = L R over the full NP-deep
 // contraction, then the op's linear combinations from the staged
 // accumulator tile with row-contiguous (coalesced) global reads and writes.
 #ifndef CSM_TILED_MINB
 #define CSM_TILED_MINB 4  // resident CTAs per SM the register budget targets
 #endif
-__global__ void __launch_bounds__(THREADS, CSM_TILED_MINB) gemm_epi_kernel(const LaunchArgs args) {
-  extern __shared__ __align__(16) double sm[];
+__device__ __forceinline__ unsigned tk_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tk_mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(tk_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 2-D tiled TMA load of one box into shared memory, completing on `bar`.
+__device__ __forceinline__ void tk_tma2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(tk_smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(tk_smem_u32(bar))
+      : "memory");
+}
+
+// CTA of the GEMM: GWARPS warps over the 64 x 64 tile.  8 warps of 32 x 16
+// (default; 16 accumulator doubles per thread leave room for the blocked
+// summation below at 2 CTAs = 16 warps per SM) or 4 warps of 32 x 32.
+#ifndef CSM_TILED_WARPS
+#define CSM_TILED_WARPS 8
+#endif
+constexpr int GWARPS = CSM_TILED_WARPS, GTHREADS = 32 * GWARPS, WNI = GWARPS == 8 ? 2 : 4;
+static_assert(GWARPS == 4 || GWARPS == 8, "4 or 8 warps");
+// Blocked summation: the contraction is accumulated in chunks of KFLUSH
+// stages (KFLUSH x 16 = 256 terms) that are then added into an outer
+// accumulator.  A single sequential FMA chain over K = 8192 carries ~5x the
+// rounding error of a blocked BLAS GEMM (tests/test_gpu_fullsize.py: cfg5
+// measured 5x the reference's own noise); chunks of 256 match it.  Bitwise
+// unchanged for NP <= 256 (one chunk).
+#ifndef CSM_TILED_KFLUSH
+#define CSM_TILED_KFLUSH 16
+#endif
+#ifndef CSM_TILED_GMINB
+#define CSM_TILED_GMINB (GWARPS == 8 ? 2 : CSM_TILED_MINB)
+#endif
+
+__global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
+    gemm_epi_kernel(const __grid_constant__ LaunchArgs args) {
+  extern __shared__ __align__(1024) double sm[];
   __shared__ Op op;
   __shared__ int sh_b;
+  __shared__ __align__(8) uint64_t full[STAGES];  // TMA stage barriers
   double* As = sm;
   double* Bs = sm + STAGES * A_STAGE;
+  // TMA stages: the swizzle patterns need 1024-byte aligned boxes; the TMA
+  // layout (48 KB) leaves room for the shift inside SMEM (56.8 KB)
+  double* const tb = sm + (((1024u - (tk_smem_u32(sm) & 1023u)) & 1023u) >> 3);
+  static_assert(STAGES * (BM * BK + BK * BN) * sizeof(double) + 1024 <= SMEM, "TMA stages fit");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int item = static_cast<int>(blockIdx.y) + args.item_base;
   if (args.only && args.only[item - args.only_base] == 0u) return;  // not a fallback item
@@ -268,9 +357,17 @@ __global__ void __launch_bounds__(THREADS, CSM_TILED_MINB) gemm_epi_kernel(const
 #pragma unroll
   for (int i = 1; i < MAXSEG; ++i)
     if (i < args.nseg && item >= args.seg[i].start) sg = args.seg[i];
-  for (int i = tid; i < static_cast<int>(sizeof(Op) / 4); i += THREADS)
+  for (int i = tid; i < static_cast<int>(sizeof(Op) / 4); i += GTHREADS)
     reinterpret_cast<int*>(&op)[i] = reinterpret_cast<const int*>(args.ops + sg.op)[i];
-  if (tid == 0) sh_b = args.idx[sg.idx_off + item - sg.start];
+  if (tid == 0) {
+    sh_b = args.idx[sg.idx_off + item - sg.start];
+    if (args.tma) {
+#pragma unroll
+      for (int s = 0; s < STAGES; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tk_smem_u32(&full[s])));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+  }
   __syncthreads();
   const int b = sh_b;
   const int NP = args.NP;
@@ -278,123 +375,169 @@ __global__ void __launch_bounds__(THREADS, CSM_TILED_MINB) gemm_epi_kernel(const
   const int tiles_n = NP / BN;
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x - tm * tiles_n;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  const int n = args.n;
-  const size_t nn = static_cast<size_t>(n) * n;
+  const int wm = GWARPS == 8 ? (warp >> 2) * 32 : (warp >> 1) * 32;
+  const int wn = GWARPS == 8 ? (warp & 3) * 16 : (warp & 1) * 32;
   const size_t slotsz = static_cast<size_t>(M) * NP;
-  {
-    double* base = args.ws + static_cast<size_t>(b) * args.mat_stride;
-    auto slot = [&](int sl) -> double* {
-      if (sl == 0 && args.in0)
-        return const_cast<double*>(args.in0) + static_cast<size_t>(b) * slotsz;
-      return base + sl * slotsz;
-    };
-    const double* L = slot(op.lhs) + static_cast<size_t>(tm) * BM * NP;
-    const double* R = (args.rhs_full ? args.rhs_full : slot(op.rhs)) + static_cast<size_t>(tn) * BN;
-    // row k0 of the right operand (a BK-row stage never crosses a part: M % 64 == 0)
-    auto rhs_rows = [&](int k0) -> const double* {
-      if (args.ksplit == 1)  // own rows of the (not yet gathered) right operand
-        return slot(op.rhs) + static_cast<size_t>(k0 - args.row0) * NP +
-               static_cast<size_t>(tn) * BN;
-      if (args.rhs_parts) {
-        const int part = k0 / M;
-        return args.rhs_parts[part] + static_cast<size_t>(op.rhs) * slotsz +
-               static_cast<size_t>(k0 - part * M) * NP + static_cast<size_t>(tn) * BN;
-      }
-      return R + static_cast<size_t>(k0) * NP;
-    };
+  double* base = args.ws + static_cast<size_t>(b) * args.mat_stride;
+  auto slot = [&](int sl) -> double* {
+    if (sl == 0 && args.in0)
+      return const_cast<double*>(args.in0) + static_cast<size_t>(b) * slotsz;
+    return base + sl * slotsz;
+  };
+  // k-stage j -> contraction index (K-split: own rows, or all but them)
+  const int nk = (args.ksplit == 0 ? NP : (args.ksplit == 1 ? M : NP - M)) / BK;
+  auto kof = [&](int j) -> int {
+    const int k = j * BK;
+    if (args.ksplit == 1) return args.row0 + k;
+    if (args.ksplit == 2 && k >= args.row0) return k + M;
+    return k;
+  };
 
-    auto load_stage = [&](int stage, int k0) {
-      double* as = As + stage * A_STAGE;
-      double* bs = Bs + stage * B_STAGE;
-#pragma unroll
-      for (int i = 0; i < (BM * BK / 2) / THREADS; ++i) {
-        const int p = tid + i * THREADS;
-        const int r = p / (BK / 2), c = (p - r * (BK / 2)) * 2;
-        cp16(as + r * LDA + c, L + static_cast<size_t>(r) * NP + k0 + c);
-      }
-      const double* Rk = rhs_rows(k0);
-#pragma unroll
-      for (int i = 0; i < (BK * BN / 2) / THREADS; ++i) {
-        const int p = tid + i * THREADS;
-        const int r = p / (BN / 2), c = (p - r * (BN / 2)) * 2;
-        cp16(bs + r * LDB + c, Rk + static_cast<size_t>(r) * NP + c);
-      }
-    };
-
-    double acc[4][4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    // k-stage j -> contraction index (K-split: own rows, or all but them)
-    const int nk = (args.ksplit == 0 ? NP : (args.ksplit == 1 ? M : NP - M)) / BK;
-    auto kof = [&](int j) -> int {
-      const int k = j * BK;
-      if (args.ksplit == 1) return args.row0 + k;
-      if (args.ksplit == 2 && k >= args.row0) return k + M;
-      return k;
-    };
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-      if (s < nk) load_stage(s, kof(s));
-      commit();
+  // -- staging: TMA (tensor maps, swizzled boxes) or cp.async (padded rows)
+  const double* L = slot(op.lhs) + static_cast<size_t>(tm) * BM * NP;
+  const double* R = (args.rhs_full ? args.rhs_full : slot(op.rhs)) + static_cast<size_t>(tn) * BN;
+  // row k0 of the right operand (a BK-row stage never crosses a part: M % 64 == 0)
+  auto rhs_rows = [&](int k0) -> const double* {
+    if (args.ksplit == 1)  // own rows of the (not yet gathered) right operand
+      return slot(op.rhs) + static_cast<size_t>(k0 - args.row0) * NP + static_cast<size_t>(tn) * BN;
+    if (args.rhs_parts) {
+      const int part = k0 / M;
+      return args.rhs_parts[part] + static_cast<size_t>(op.rhs) * slotsz +
+             static_cast<size_t>(k0 - part * M) * NP + static_cast<size_t>(tn) * BN;
     }
-    for (int kt = 0; kt < nk; ++kt) {
-      wait_group<STAGES - 2>();
-      __syncthreads();
-      {
-        const int nxt = kt + STAGES - 1;
-        if (nxt < nk) load_stage(nxt % STAGES, kof(nxt));
-        commit();
-      }
-      const double* as = As + (kt % STAGES) * A_STAGE;
-      const double* bs = Bs + (kt % STAGES) * B_STAGE;
-#pragma unroll
-      for (int kk = 0; kk < BK; kk += 4) {
-        double a[4], bf[4];
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) a[mi] = as[(wm + mi * 8 + g) * LDA + kk + t];
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) bf[ni] = bs[(kk + t) * LDB + wn + ni * 8 + g];
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], bf[ni]);
-      }
+    return R + static_cast<size_t>(k0) * NP;
+  };
+  auto ws_row = [&](int sl) -> int {
+    return static_cast<int>((static_cast<size_t>(b) * args.mat_stride + sl * slotsz) / NP);
+  };
+  const CUtensorMap* mapL = nullptr;
+  const CUtensorMap* mapR = nullptr;
+  int rowL = 0, rowR = 0;  // rowR: map row holding contraction index 0
+  if (args.tma) {
+    const bool l_in0 = op.lhs == 0 && args.in0;
+    mapL = l_in0 ? &args.tm_in0L : &args.tm_wsL;
+    rowL = (l_in0 ? b * M : ws_row(op.lhs)) + tm * BM;
+    if (args.ksplit == 1) {
+      mapR = &args.tm_wsR;
+      rowR = ws_row(op.rhs) - args.row0;
+    } else if (args.rhs_full) {
+      mapR = &args.tm_rhsR;
+    } else if (op.rhs == 0 && args.in0) {
+      mapR = &args.tm_in0R;
+      rowR = b * M;
+    } else {
+      mapR = &args.tm_wsR;
+      rowR = ws_row(op.rhs);
     }
-    wait_group<0>();
-    __syncthreads();  // pipeline buffers are free: stage the accumulator tile
-
-    double* E = sm;  // [BM][LDE]
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-        *reinterpret_cast<double2*>(E + (wm + mi * 8 + g) * LDE + wn + ni * 8 + 2 * t) =
-            make_double2(acc[mi][ni][0], acc[mi][ni][1]);
-    __syncthreads();
-
-    if (args.ksplit != 0) {  // partial product: raw tile out, or added in
-      double* pt = args.part + static_cast<size_t>(blockIdx.y) * slotsz +
-                   static_cast<size_t>(tm) * BM * NP + static_cast<size_t>(tn) * BN;
-      for (int p = tid; p < BM * BN / 2; p += THREADS) {
-        const int rr = p >> 5, cc = (p & 31) * 2;
-        double2* e = reinterpret_cast<double2*>(E + rr * LDE + cc);
-        double2* g = reinterpret_cast<double2*>(pt + static_cast<size_t>(rr) * NP + cc);
-        if (args.ksplit == 1) {
-          *g = *e;
-        } else {
-          const double2 x = *g;
-          *e = make_double2(e->x + x.x, e->y + x.y);
-        }
-      }
-      if (args.ksplit == 1) return;
-      __syncthreads();
-    }
-    epilogue_tile(args, op, b, tm, tn, E);
   }
+  auto load_stage = [&](int stage, int k0) {
+    if (args.tma) {  // thread 0: one 64 x 16 box of L, eight 16 x 8 boxes of R
+      if (tid != 0) return;
+      asm volatile("fence.proxy.async.shared::cta;\n" ::);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                       tk_smem_u32(&full[stage])),
+                   "r"(static_cast<unsigned>((BM * BK + BK * BN) * sizeof(double))));
+      tk_tma2d(tb + stage * BM * BK, mapL, k0, rowL, &full[stage]);
+#pragma unroll
+      for (int j = 0; j < BN / 8; ++j)
+        tk_tma2d(tb + STAGES * BM * BK + stage * BK * BN + j * BK * 8, mapR, tn * BN + 8 * j,
+                 rowR + k0, &full[stage]);
+      return;
+    }
+    double* as = As + stage * A_STAGE;
+    double* bs = Bs + stage * B_STAGE;
+#pragma unroll
+    for (int i = 0; i < (BM * BK / 2) / GTHREADS; ++i) {
+      const int p = tid + i * GTHREADS;
+      const int r = p / (BK / 2), c = (p - r * (BK / 2)) * 2;
+      cp16(as + r * LDA + c, L + static_cast<size_t>(r) * NP + k0 + c);
+    }
+    const double* Rk = rhs_rows(k0);
+#pragma unroll
+    for (int i = 0; i < (BK * BN / 2) / GTHREADS; ++i) {
+      const int p = tid + i * GTHREADS;
+      const int r = p / (BN / 2), c = (p - r * (BN / 2)) * 2;
+      cp16(bs + r * LDB + c, Rk + static_cast<size_t>(r) * NP + c);
+    }
+  };
+  // fragments of k-step kk of stage st
+  auto frags = [&](int st, int kk, double (&a)[4], double (&bf)[WNI]) {
+    const int k = kk + t;
+    if (args.tma) {
+      const double* as = tb + st * BM * BK;
+      const double* bs = tb + STAGES * BM * BK + st * BK * BN;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)  // (r, k) -> 16 r + 2 ((k / 2) ^ (r % 8)) + k % 2, r % 8 = g
+        a[mi] = as[(wm + mi * 8 + g) * BK + (((k >> 1) ^ g) << 1) + (k & 1)];
+#pragma unroll
+      for (int ni = 0; ni < WNI; ++ni)  // box j, (k, c) -> 8 k + 2 ((c / 2) ^ (k / 2 % 4)) + c % 2
+        bf[ni] = bs[((wn >> 3) + ni) * (BK * 8) + k * 8 + (((g >> 1) ^ ((k >> 1) & 3)) << 1) +
+                    (g & 1)];
+    } else {
+      const double* as = As + st * A_STAGE;
+      const double* bs = Bs + st * B_STAGE;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = as[(wm + mi * 8 + g) * LDA + k];
+#pragma unroll
+      for (int ni = 0; ni < WNI; ++ni) bf[ni] = bs[k * LDB + wn + ni * 8 + g];
+    }
+  };
+
+  double acc[4][WNI][2], outer[4][WNI][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < WNI; ++j) acc[i][j][0] = acc[i][j][1] = outer[i][j][0] = outer[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, kof(s));
+    if (!args.tma) commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    const int st = kt % STAGES;
+    if (args.tma)
+      tk_mbar_wait(&full[st], static_cast<unsigned>((kt / STAGES) & 1));
+    else
+      wait_group<STAGES - 2>();
+    __syncthreads();  // every warp is done with the stage refilled next
+    {
+      const int nxt = kt + STAGES - 1;
+      if (nxt < nk) load_stage(nxt % STAGES, kof(nxt));
+      if (!args.tma) commit();
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[4], bf[WNI];
+      frags(st, kk, a, bf);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < WNI; ++ni) dmma(acc[mi][ni], a[mi], bf[ni]);
+    }
+    if (CSM_TILED_KFLUSH > 0 && (kt + 1) % CSM_TILED_KFLUSH == 0 && kt + 1 < nk) {
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < WNI; ++ni) {
+          outer[mi][ni][0] += acc[mi][ni][0];
+          outer[mi][ni][1] += acc[mi][ni][1];
+          acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        }
+    }
+  }
+  if (!args.tma) wait_group<0>();
+  __syncthreads();  // pipeline buffers are free: stage the accumulator tile
+
+  double* E = sm;  // [BM][LDE]
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < WNI; ++ni)
+      *reinterpret_cast<double2*>(E + (wm + mi * 8 + g) * LDE + wn + ni * 8 + 2 * t) =
+          make_double2(outer[mi][ni][0] + acc[mi][ni][0], outer[mi][ni][1] + acc[mi][ni][1]);
+  __syncthreads();
+  finish_tile<GTHREADS>(args, op, b, tm, tn, E, slotsz);
 }
 
 #include "ozaki.cuh"
@@ -443,6 +586,60 @@ __global__ void nan_fill_kernel(TOut* __restrict__ Cout, TOut* __restrict__ Sout
     Cout[b * nn + p] = static_cast<TOut>(qnan);
     Sout[b * nn + p] = static_cast<TOut>(qnan);
   }
+}
+
+// ---- TMA tensor maps of the GEMM operands --------------------------------
+// cuTensorMapEncodeTiled is fetched from the driver at run time (no -lcuda).
+typedef CUresult (*PfnEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+inline PfnEncodeTiled encode_tiled() {
+  static PfnEncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<PfnEncodeTiled>(nullptr);
+    return reinterpret_cast<PfnEncodeTiled>(p);
+  }();
+  return fn;
+}
+// float64 rows x NP (row stride NP), boxes of box_r rows x box_c columns.
+inline bool encode2d(CUtensorMap* m, const double* base, int NP, size_t rows, int box_c,
+                     int box_r, CUtensorMapSwizzle sw) {
+  PfnEncodeTiled fn = encode_tiled();
+  if (!fn || !base || rows == 0 || rows > 0x7fffffffull ||
+      (reinterpret_cast<uintptr_t>(base) & 15))
+    return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(NP), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(NP) * sizeof(double)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_c), static_cast<cuuint32_t>(box_r)};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// TMA staging for A when every operand can be described (tma = 0 keeps the
+// cp.async staging: peer mode, or CSM_TILED_TMA=0 for A/B measurements).
+// ws_rows / in0_rows: rows of the slot stack and of the slot-0 alias.
+inline void set_tma(LaunchArgs& A, size_t ws_rows, size_t in0_rows) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("CSM_TILED_TMA");
+    return !(e && e[0] == '0');
+  }();
+  A.tma = 0;
+  if (!enabled || A.rhs_parts) return;
+  const CUtensorMapSwizzle L128 = CU_TENSOR_MAP_SWIZZLE_128B, R64 = CU_TENSOR_MAP_SWIZZLE_64B;
+  bool ok = encode2d(&A.tm_wsL, A.ws, A.NP, ws_rows, BK, BM, L128) &&
+            encode2d(&A.tm_wsR, A.ws, A.NP, ws_rows, 8, BK, R64);
+  if (ok && A.in0)
+    ok = encode2d(&A.tm_in0L, A.in0, A.NP, in0_rows, BK, BM, L128) &&
+         encode2d(&A.tm_in0R, A.in0, A.NP, in0_rows, 8, BK, R64);
+  if (ok && A.rhs_full)
+    ok = encode2d(&A.tm_rhsR, A.rhs_full, A.NP, static_cast<size_t>(A.NP), 8, BK, R64);
+  A.tma = ok ? 1 : 0;
 }
 
 // Opt the tiled kernel into its dynamic shared memory, once per device.
@@ -1157,7 +1354,7 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
       R.item_base = done;
       R.only = O.flag;
       R.only_base = done;
-      tk::gemm_epi_kernel<<<dim3(tiles, static_cast<unsigned>(cnt), 1), tk::THREADS, tk::SMEM,
+      tk::gemm_epi_kernel<<<dim3(tiles, static_cast<unsigned>(cnt), 1), tk::GTHREADS, tk::SMEM,
                             stream>>>(R);
       *launches += 2;
     }
@@ -1329,6 +1526,8 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
     A.row0 = 0;
     A.rhs_full = nullptr;
     A.rhs_parts = nullptr;
+    tk::set_tma(A, static_cast<size_t>(batch) * (mat_stride / NP),
+                fold ? static_cast<size_t>(batch) * NP : 0);
     const bool use_oz = oz_applies(NP, eng);
     const tk::OzConst ozc = use_oz ? oz_const(oz_moduli(out_f32), NP) : tk::OzConst{};
     size_t lu_smem = 0;
@@ -1364,7 +1563,7 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
         A.item_base = done;
         const int cnt = std::min(65535, L.total - done);
         dim3 grid(tiles, static_cast<unsigned>(cnt), 1);
-        tk::gemm_epi_kernel<<<grid, tk::THREADS, tk::SMEM, stream>>>(A);
+        tk::gemm_epi_kernel<<<grid, tk::GTHREADS, tk::SMEM, stream>>>(A);
         ++*launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
       }
@@ -1499,6 +1698,7 @@ cudaError_t slab_op(const void* const* op_host, int nops, double* slab, int M, i
   A.rhs_parts = nparts > 0 ? d->parts : nullptr;
   A.M = M;
   A.row0 = row0;
+  tk::set_tma(A, static_cast<size_t>(tk::NSLOT) * M, static_cast<size_t>(M));
   if (nparts == 0 && oz_slab_applies(M, NP, eng)) {  // Ozaki engine (gathered right operand)
     char* p = reinterpret_cast<char*>(
         (reinterpret_cast<uintptr_t>(scratch) + slab_scratch_bytes() + 255) & ~uintptr_t(255));
@@ -1507,7 +1707,7 @@ cudaError_t slab_op(const void* const* op_host, int nops, double* slab, int M, i
     return run_oz_launch(A, O, nops, oz_const(oz_moduli(out_f32), NP), stream, launches, eng != 3);
   }
   dim3 grid(static_cast<unsigned>((M / tk::BM) * (NP / tk::BN)), static_cast<unsigned>(nops), 1);
-  tk::gemm_epi_kernel<<<grid, tk::THREADS, tk::SMEM, stream>>>(A);
+  tk::gemm_epi_kernel<<<grid, tk::GTHREADS, tk::SMEM, stream>>>(A);
   ++*launches;
   return cudaGetLastError();
 }
