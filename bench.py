@@ -439,9 +439,9 @@ def cfg5_parity(a_np, c, s, st, args):
 
 def parity_block(kind, a_np, t_np, prec, dt, plan, ks, ss, rank):
     """Parity summary carried in the bench line (computed outside the timed
-    region): the oracle on a spot-check sample at the parity gate (1e-12
-    fp64 / 1e-5 fp32; for the wave config max(1e-12, 4 x the oracle's own
-    permuted-order noise)), (k, s) of EVERY matrix against the
+    region): the oracle on a spot-check sample at the parity gate (1e-5
+    fp32; 1e-12 fp64, or for the wave config and n >= 256 max(1e-12, 4 x
+    the oracle's own permuted-order noise)), (k, s) of EVERY matrix against the
     oracle's selection, and the Pythagorean residual ||C^2 + S^2 - I||_1 /
     max(1, ||C||_1^2) over the whole batch (csm_pythagorean_residual)."""
     import numpy as np
@@ -471,9 +471,16 @@ def parity_block(kind, a_np, t_np, prec, dt, plan, ks, ss, rank):
             fn = lambda x: orc.wave_cos_sin(x, float(t_np[i]), prec)  # noqa: E731
             (c, s, k, sc), noise = permuted_noise(fn, a_np[i], rng)
             gate = max(1e-12, 4.0 * noise)
+        elif dt == "f32":
+            c, s, k, sc = orc.cos_sin(a_np[i].astype(np.float64), prec)
+            gate = 1e-5
+        elif n >= 256:  # the reference's own noise can exceed 1e-12 here
+            fn = lambda x: orc.cos_sin(x, prec)  # noqa: E731
+            (c, s, k, sc), noise = permuted_noise(fn, a_np[i], rng)
+            gate = max(1e-12, 4.0 * noise)
         else:
             c, s, k, sc = orc.cos_sin(a_np[i].astype(np.float64), prec)
-            gate = 1e-5 if dt == "f32" else 1e-12
+            gate = 1e-12
         assert (int(ks[i]), int(ss[i])) == (k, sc), (i, ks[i], ss[i], k, sc)
         okc, ec = pair_close(plan.cos[i].double().cpu().numpy(), c, s, gate)
         oks, es = pair_close(plan.sin[i].double().cpu().numpy(), s, c, gate)

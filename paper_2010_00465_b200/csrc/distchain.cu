@@ -216,7 +216,7 @@ cudaError_t launch(const tk::Op* d_ops, const Staged* d_st, int op, int nops, do
   A.part = part;
   tk::set_tma(A, static_cast<size_t>(tk::NSLOT) * M, static_cast<size_t>(M));
   dim3 grid(static_cast<unsigned>((M / tk::BM) * (n / tk::BN)), static_cast<unsigned>(nops), 1);
-  tk::gemm_epi_kernel<<<grid, tk::GTHREADS, tk::SMEM, st>>>(A);
+  tk::launch_gemm(grid, A, st);
   ++*launches;
   return cudaGetLastError();
 }
@@ -295,7 +295,7 @@ cudaError_t run(int precision, const double* a, int n, int world, int rank0, int
       for (int q = 0; q < nlocal && e == cudaSuccess; ++q) e = fn(q, (rank0 + q) * M);
     };
     auto prod = [&](int q, int row0, const double* rhs, int ksplit) {
-      res->products += ksplit == 1 ? 0 : act.nops;
+      if (q == 0 && ksplit != 1) res->products += act.nops;  // per rank
       return launch(d_ops, d_st, act.op, act.nops, R[q].slab, M, n, row0, a + row0 * size_t(n),
                     rhs, ksplit, R[q].part, act.dbl_step, cos_rows[q], sin_rows[q], st,
                     launches);

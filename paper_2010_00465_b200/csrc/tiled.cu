@@ -317,29 +317,29 @@ __device__ __forceinline__ void tk_tma2d(void* dst, const CUtensorMap* map, int 
       : "memory");
 }
 
-// CTA of the GEMM: GWARPS warps over the 64 x 64 tile.  8 warps of 32 x 16
-// (default; 16 accumulator doubles per thread leave room for the blocked
-// summation below at 2 CTAs = 16 warps per SM) or 4 warps of 32 x 32.
-#ifndef CSM_TILED_WARPS
-#define CSM_TILED_WARPS 8
-#endif
-constexpr int GWARPS = CSM_TILED_WARPS, GTHREADS = 32 * GWARPS, WNI = GWARPS == 8 ? 2 : 4;
-static_assert(GWARPS == 4 || GWARPS == 8, "4 or 8 warps");
-// Blocked summation: the contraction is accumulated in chunks of KFLUSH
-// stages (KFLUSH x 16 = 256 terms) that are then added into an outer
+// CTA of the GEMM over the 64 x 64 tile: W = 4 warps of 32 x 32 (4 CTAs
+// per SM; the product of each 256-deep contraction chunk is summed in one
+// FMA chain) or W = 8 warps of 32 x 16 (2 CTAs per SM; 16 accumulator
+// doubles per thread leave room for the blocked summation below).  TMA:
+// operands staged by tensor-map TMA (true) or cp.async (false, peer mode).
+//
+// Blocked summation (W = 8): the contraction is accumulated in chunks of
+// KFLUSH stages (KFLUSH x 16 = 256 terms) that are then added into an outer
 // accumulator.  A single sequential FMA chain over K = 8192 carries ~5x the
 // rounding error of a blocked BLAS GEMM (tests/test_gpu_fullsize.py: cfg5
-// measured 5x the reference's own noise); chunks of 256 match it.  Bitwise
-// unchanged for NP <= 256 (one chunk).
+// measured 5x the reference's own noise); chunks of 256 match it.  W = 8
+// serves NP > kWideNP (launch_gemm), where the epilogue is a small share of
+// the tile and 2 CTAs per SM suffice.
 #ifndef CSM_TILED_KFLUSH
 #define CSM_TILED_KFLUSH 16
 #endif
-#ifndef CSM_TILED_GMINB
-#define CSM_TILED_GMINB (GWARPS == 8 ? 2 : CSM_TILED_MINB)
-#endif
+constexpr int kWideNP = 1024;
 
-__global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
+template <bool TMA, int W>
+__global__ void __launch_bounds__(32 * W, W == 8 ? 2 : CSM_TILED_MINB)
     gemm_epi_kernel(const __grid_constant__ LaunchArgs args) {
+  static_assert(W == 4 || W == 8, "4 or 8 warps");
+  constexpr int GTHREADS = 32 * W, WNI = W == 8 ? 2 : 4;
   extern __shared__ __align__(1024) double sm[];
   __shared__ Op op;
   __shared__ int sh_b;
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
     reinterpret_cast<int*>(&op)[i] = reinterpret_cast<const int*>(args.ops + sg.op)[i];
   if (tid == 0) {
     sh_b = args.idx[sg.idx_off + item - sg.start];
-    if (args.tma) {
+    if (TMA) {
 #pragma unroll
       for (int s = 0; s < STAGES; ++s)
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tk_smem_u32(&full[s])));
@@ -375,8 +375,8 @@ __global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
   const int tiles_n = NP / BN;
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x - tm * tiles_n;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = GWARPS == 8 ? (warp >> 2) * 32 : (warp >> 1) * 32;
-  const int wn = GWARPS == 8 ? (warp & 3) * 16 : (warp & 1) * 32;
+  const int wm = W == 8 ? (warp >> 2) * 32 : (warp >> 1) * 32;
+  const int wn = W == 8 ? (warp & 3) * 16 : (warp & 1) * 32;
   const size_t slotsz = static_cast<size_t>(M) * NP;
   double* base = args.ws + static_cast<size_t>(b) * args.mat_stride;
   auto slot = [&](int sl) -> double* {
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
   const CUtensorMap* mapL = nullptr;
   const CUtensorMap* mapR = nullptr;
   int rowL = 0, rowR = 0;  // rowR: map row holding contraction index 0
-  if (args.tma) {
+  if constexpr (TMA) {
     const bool l_in0 = op.lhs == 0 && args.in0;
     mapL = l_in0 ? &args.tm_in0L : &args.tm_wsL;
     rowL = (l_in0 ? b * M : ws_row(op.lhs)) + tm * BM;
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
     }
   }
   auto load_stage = [&](int stage, int k0) {
-    if (args.tma) {  // thread 0: one 64 x 16 box of L, eight 16 x 8 boxes of R
+    if constexpr (TMA) {  // thread 0: one 64 x 16 box of L, eight 16 x 8 boxes of R
       if (tid != 0) return;
       asm volatile("fence.proxy.async.shared::cta;\n" ::);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
@@ -442,8 +442,7 @@ __global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
       for (int j = 0; j < BN / 8; ++j)
         tk_tma2d(tb + STAGES * BM * BK + stage * BK * BN + j * BK * 8, mapR, tn * BN + 8 * j,
                  rowR + k0, &full[stage]);
-      return;
-    }
+    } else {
     double* as = As + stage * A_STAGE;
     double* bs = Bs + stage * B_STAGE;
 #pragma unroll
@@ -459,11 +458,12 @@ __global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
       const int r = p / (BN / 2), c = (p - r * (BN / 2)) * 2;
       cp16(bs + r * LDB + c, Rk + static_cast<size_t>(r) * NP + c);
     }
+    }
   };
   // fragments of k-step kk of stage st
   auto frags = [&](int st, int kk, double (&a)[4], double (&bf)[WNI]) {
     const int k = kk + t;
-    if (args.tma) {
+    if constexpr (TMA) {
       const double* as = tb + st * BM * BK;
       const double* bs = tb + STAGES * BM * BK + st * BK * BN;
 #pragma unroll
@@ -492,11 +492,11 @@ __global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk) load_stage(s, kof(s));
-    if (!args.tma) commit();
+    if constexpr (!TMA) commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     const int st = kt % STAGES;
-    if (args.tma)
+    if constexpr (TMA)
       tk_mbar_wait(&full[st], static_cast<unsigned>((kt / STAGES) & 1));
     else
       wait_group<STAGES - 2>();
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
     {
       const int nxt = kt + STAGES - 1;
       if (nxt < nk) load_stage(nxt % STAGES, kof(nxt));
-      if (!args.tma) commit();
+      if constexpr (!TMA) commit();
     }
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
@@ -515,7 +515,7 @@ __global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
 #pragma unroll
         for (int ni = 0; ni < WNI; ++ni) dmma(acc[mi][ni], a[mi], bf[ni]);
     }
-    if (CSM_TILED_KFLUSH > 0 && (kt + 1) % CSM_TILED_KFLUSH == 0 && kt + 1 < nk) {
+    if (W == 8 && CSM_TILED_KFLUSH > 0 && (kt + 1) % CSM_TILED_KFLUSH == 0 && kt + 1 < nk) {
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
         }
     }
   }
-  if (!args.tma) wait_group<0>();
+  if constexpr (!TMA) wait_group<0>();
   __syncthreads();  // pipeline buffers are free: stage the accumulator tile
 
   double* E = sm;  // [BM][LDE]
@@ -535,9 +535,31 @@ __global__ void __launch_bounds__(GTHREADS, CSM_TILED_GMINB)
 #pragma unroll
     for (int ni = 0; ni < WNI; ++ni)
       *reinterpret_cast<double2*>(E + (wm + mi * 8 + g) * LDE + wn + ni * 8 + 2 * t) =
-          make_double2(outer[mi][ni][0] + acc[mi][ni][0], outer[mi][ni][1] + acc[mi][ni][1]);
+          W == 8 ? make_double2(outer[mi][ni][0] + acc[mi][ni][0], outer[mi][ni][1] + acc[mi][ni][1])
+                 : make_double2(acc[mi][ni][0], acc[mi][ni][1]);
   __syncthreads();
   finish_tile<GTHREADS>(args, op, b, tm, tn, E, slotsz);
+}
+
+// Launch the GEMM variant for A: TMA staging when A.tma, the 8-warp
+// blocked-summation CTA for NP > kWideNP (CSM_TILED_W=4|8 forces one).
+inline int gemm_warps(int NP) {
+  static const int forced = [] {
+    const char* e = std::getenv("CSM_TILED_W");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 4 || forced == 8) return forced;
+  return NP > kWideNP ? 8 : 4;
+}
+inline void launch_gemm(dim3 grid, const LaunchArgs& A, cudaStream_t st) {
+  const bool wide = gemm_warps(A.NP) == 8;
+  if (A.tma) {
+    if (wide) gemm_epi_kernel<true, 8><<<grid, 256, SMEM, st>>>(A);
+    else gemm_epi_kernel<true, 4><<<grid, 128, SMEM, st>>>(A);
+  } else {
+    if (wide) gemm_epi_kernel<false, 8><<<grid, 256, SMEM, st>>>(A);
+    else gemm_epi_kernel<false, 4><<<grid, 128, SMEM, st>>>(A);
+  }
 }
 
 #include "ozaki.cuh"
@@ -649,8 +671,17 @@ inline cudaError_t ensure_smem_attr() {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 32 && ((done_mask >> dev) & 1u)) return cudaSuccess;
-  e = cudaFuncSetAttribute(gemm_epi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(gemm_epi_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(SMEM));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm_epi_kernel<false, 8>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm_epi_kernel<true, 4>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm_epi_kernel<true, 8>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(oz_crt_epi<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(SMEM));
@@ -1354,8 +1385,7 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
       R.item_base = done;
       R.only = O.flag;
       R.only_base = done;
-      tk::gemm_epi_kernel<<<dim3(tiles, static_cast<unsigned>(cnt), 1), tk::GTHREADS, tk::SMEM,
-                            stream>>>(R);
+      tk::launch_gemm(dim3(tiles, static_cast<unsigned>(cnt), 1), R, stream);
       *launches += 2;
     }
     *launches += 6;
@@ -1563,7 +1593,7 @@ cudaError_t run_tiled(int dtype, bool wave, const void* a, const double* t, void
         A.item_base = done;
         const int cnt = std::min(65535, L.total - done);
         dim3 grid(tiles, static_cast<unsigned>(cnt), 1);
-        tk::gemm_epi_kernel<<<grid, tk::GTHREADS, tk::SMEM, stream>>>(A);
+        tk::launch_gemm(grid, A, stream);
         ++*launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
       }
@@ -1707,7 +1737,7 @@ cudaError_t slab_op(const void* const* op_host, int nops, double* slab, int M, i
     return run_oz_launch(A, O, nops, oz_const(oz_moduli(out_f32), NP), stream, launches, eng != 3);
   }
   dim3 grid(static_cast<unsigned>((M / tk::BM) * (NP / tk::BN)), static_cast<unsigned>(nops), 1);
-  tk::gemm_epi_kernel<<<grid, tk::GTHREADS, tk::SMEM, stream>>>(A);
+  tk::launch_gemm(grid, A, stream);
   ++*launches;
   return cudaGetLastError();
 }

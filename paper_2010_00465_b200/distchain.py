@@ -180,13 +180,36 @@ class DistStats:
     launches: int = 0  # library kernels launched by the gather-mode products
 
 
+def _use_c_driver(a, group) -> bool:
+    """The C driver (csm_dist_cos_sin, gathers overlapped with the K-split
+    products) runs CUDA inputs on the FP64 DMMA engine over NCCL; the
+    Python schedule below runs everything else (the Ozaki engine's slab
+    products, and the CPU test doubles of the gloo tests)."""
+    import torch.distributed as dist
+
+    from .api import get_engine
+    if not getattr(a, "is_cuda", False) or get_engine() != "dmma":
+        return False
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return True
+    return dist.get_backend(group) == "nccl"
+
+
 def cos_sin_distributed(a, precision: Precision = Precision.DOUBLE, *,
-                        group=None, gather_outputs: bool = True):
+                        group=None, gather_outputs: bool = True, driver: str = "auto"):
     """cos(a), sin(a) for one n x n float64 matrix replicated on every rank
     of `group`, computed block-row over the ranks.  Returns (cos, sin,
-    stats): the full matrices if gather_outputs, else this rank's rows."""
+    stats): the full matrices if gather_outputs, else this rank's rows.
+    driver: 'c' (csm_dist_cos_sin), 'python' (this module's schedule over
+    torch.distributed all-gathers and csm_slab_op) or 'auto' (the C driver
+    whenever it applies, see _use_c_driver)."""
     import torch
     import torch.distributed as dist
+    if driver not in ("auto", "c", "python"):
+        raise ValueError(f"driver must be 'auto', 'c' or 'python', got {driver!r}")
+    if driver == "c" or (driver == "auto" and slab_op is _device_slab_op
+                         and _use_c_driver(a, group)):
+        return cos_sin_distributed_c(a, precision, group=group, gather_outputs=gather_outputs)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     n = int(a.shape[0])

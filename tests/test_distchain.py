@@ -204,7 +204,7 @@ def test_c_driver_world1_bitwise_python_driver(cuda):
     from paper_2010_00465_b200 import distchain
     a = torch.from_numpy(_cfg5_like(1024)).to(cuda)
     c, s, st = distchain.cos_sin_distributed_c(a)
-    c1, s1, st1 = distchain.cos_sin_distributed(a)
+    c1, s1, st1 = distchain.cos_sin_distributed(a, driver="python")
     assert (st.k, st.s) == (st1.k, st1.s)
     assert st.products == st1.products == st.k + 2 * st.s
     assert st.gathers == 0  # W = 1 reads the slab itself
@@ -221,7 +221,7 @@ def test_c_driver_nccl_forced_gathers_world1(cuda):
     from paper_2010_00465_b200 import distchain
     a = torch.from_numpy(_cfg5_like(1024, seed=1)).to(cuda)
     c, s, st = distchain.cos_sin_distributed_c(a, force_gather=True)
-    c1, s1, st1 = distchain.cos_sin_distributed(a)
+    c1, s1, st1 = distchain.cos_sin_distributed(a, driver="python")
     assert st.gathers == st1.gathers > 0
     assert torch.equal(c, c1) and torch.equal(s, s1)
 
@@ -241,7 +241,7 @@ def test_c_driver_virtual_ranks_k_split(cuda, world):
     a_np = _cfg5_like(n, seed=2)
     a = torch.from_numpy(a_np).to(cuda)
     c, s, st = distchain.cos_sin_virtual_gather(a, world)
-    c1, s1, st1 = distchain.cos_sin_distributed(a)
+    c1, s1, st1 = distchain.cos_sin_distributed(a, driver="python")
     assert (st.k, st.s, st.gathers, st.products) == (st1.k, st1.s, st1.gathers, st1.products)
     (rc, rs, k, sc), noise = permuted_noise(orc.cos_sin, a_np, np.random.default_rng(3))
     assert (st.k, st.s) == (k, sc)
