@@ -13,6 +13,16 @@
 #include "cossin_constants.h"
 #undef CSM_CONST
 
+// Device-side bounds checks of the debug build (-DCSM_DEBUG_CHECKS; built by
+// tools/build_debug.py and run over the GPU suite in place of compute-sanitizer,
+// which is closed on this pool): a failed check traps with its location.
+#ifdef CSM_DEBUG_CHECKS
+#include <cassert>
+#define CSM_DCHECK(cond) assert(cond)
+#else
+#define CSM_DCHECK(cond) do { } while (0)
+#endif
+
 namespace csm {
 
 // ---------------------------------------------------------------------------

@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la,
 template <int NM>
 __global__ void __launch_bounds__(THREADS, 3) oz_crt_epi(const LaunchArgs la, const OzArgs oz,
                                                       const OzConst C) {
-  extern __shared__ __align__(1024) double sm[];
+  extern __shared__ __align__(16) double sm[];
   __shared__ Op op;
   __shared__ int sh_b;
   const int tid = threadIdx.x;

@@ -182,12 +182,14 @@ __device__ __forceinline__ void epilogue_tile(const LaunchArgs& args, const Op& 
     }
     for (int q = 0; q < nout; ++q) {
       const OutSpec& os = op.out[q];
+      CSM_DCHECK(os.slot >= 1 && os.slot < NSLOT && os.nterms >= 0 && os.nterms <= MAXT);
       double v[PB][2];
 #pragma unroll
       for (int m = 0; m < PB; ++m) v[m][0] = v[m][1] = 0.0;
       for (int tt = 0; tt < os.nterms; ++tt) {
         const int src = os.t[tt].src;
         const double cf = os.t[tt].c;
+        CSM_DCHECK(src < NSLOT && src >= SRC_OUT0 - 1 && (src > SRC_OUT0 - q || src >= SRC_I));
         if (src >= 0) {
           const double* sp = slot(src);
           double2 x[PB];
@@ -335,12 +337,12 @@ __device__ __forceinline__ void tk_tma2d(void* dst, const CUtensorMap* map, int 
 #endif
 constexpr int kWideNP = 1024;
 
-template <bool TMA, int W>
-__global__ void __launch_bounds__(32 * W, W == 8 ? 2 : CSM_TILED_MINB)
+template <bool TMA, int W, bool BLK>
+__global__ void __launch_bounds__(32 * W, W == 8 ? 2 : (BLK ? 3 : CSM_TILED_MINB))
     gemm_epi_kernel(const __grid_constant__ LaunchArgs args) {
   static_assert(W == 4 || W == 8, "4 or 8 warps");
   constexpr int GTHREADS = 32 * W, WNI = W == 8 ? 2 : 4;
-  extern __shared__ __align__(1024) double sm[];
+  extern __shared__ __align__(16) double sm[];
   __shared__ Op op;
   __shared__ int sh_b;
   __shared__ __align__(8) uint64_t full[STAGES];  // TMA stage barriers
@@ -374,6 +376,10 @@ __global__ void __launch_bounds__(32 * W, W == 8 ? 2 : CSM_TILED_MINB)
   const int M = args.M;
   const int tiles_n = NP / BN;
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x - tm * tiles_n;
+  CSM_DCHECK(b >= 0 && op.lhs >= 0 && op.lhs < NSLOT && op.rhs >= 0 && op.rhs < NSLOT);
+  CSM_DCHECK(op.nout >= 1 && op.nout <= 3 && tm * BM < M && tn * BN < NP);
+  CSM_DCHECK(args.ksplit == 0 || (args.part && args.row0 % BK == 0 && args.row0 + M <= NP));
+  CSM_DCHECK(!args.rhs_parts || args.ksplit == 0);
   const int g = lane >> 2, t = lane & 3;
   const int wm = W == 8 ? (warp >> 2) * 32 : (warp >> 1) * 32;
   const int wn = W == 8 ? (warp & 3) * 16 : (warp & 1) * 32;
@@ -515,7 +521,7 @@ __global__ void __launch_bounds__(32 * W, W == 8 ? 2 : CSM_TILED_MINB)
 #pragma unroll
         for (int ni = 0; ni < WNI; ++ni) dmma(acc[mi][ni], a[mi], bf[ni]);
     }
-    if (W == 8 && CSM_TILED_KFLUSH > 0 && (kt + 1) % CSM_TILED_KFLUSH == 0 && kt + 1 < nk) {
+    if (BLK && CSM_TILED_KFLUSH > 0 && (kt + 1) % CSM_TILED_KFLUSH == 0 && kt + 1 < nk) {
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -535,31 +541,35 @@ __global__ void __launch_bounds__(32 * W, W == 8 ? 2 : CSM_TILED_MINB)
 #pragma unroll
     for (int ni = 0; ni < WNI; ++ni)
       *reinterpret_cast<double2*>(E + (wm + mi * 8 + g) * LDE + wn + ni * 8 + 2 * t) =
-          W == 8 ? make_double2(outer[mi][ni][0] + acc[mi][ni][0], outer[mi][ni][1] + acc[mi][ni][1])
+          BLK ? make_double2(outer[mi][ni][0] + acc[mi][ni][0], outer[mi][ni][1] + acc[mi][ni][1])
                  : make_double2(acc[mi][ni][0], acc[mi][ni][1]);
   __syncthreads();
   finish_tile<GTHREADS>(args, op, b, tm, tn, E, slotsz);
 }
 
-// Launch the GEMM variant for A: TMA staging when A.tma, the 8-warp
-// blocked-summation CTA for NP > kWideNP (CSM_TILED_W=4|8 forces one).
-inline int gemm_warps(int NP) {
+// Launch the GEMM variant for A: TMA staging when A.tma; for NP > kWideNP
+// the blocked-summation CTA (4 warps at 3 CTAs per SM; CSM_TILED_W=8 picks
+// the 8-warp one, CSM_TILED_W=4 the unblocked 4-warp CTA at every size).
+inline int gemm_variant(int NP) {
   static const int forced = [] {
     const char* e = std::getenv("CSM_TILED_W");
     return e ? std::atoi(e) : 0;
   }();
-  if (forced == 4 || forced == 8) return forced;
-  return NP > kWideNP ? 8 : 4;
+  if (forced == 4) return 0;      // 4 warps, one FMA chain
+  if (forced == 8) return 2;      // 8 warps, blocked
+  return NP > kWideNP ? 1 : 0;    // 1: 4 warps, blocked
+}
+template <bool TMA>
+inline void launch_gemm_t(dim3 grid, const LaunchArgs& A, cudaStream_t st) {
+  switch (gemm_variant(A.NP)) {
+    case 0: gemm_epi_kernel<TMA, 4, false><<<grid, 128, SMEM, st>>>(A); break;
+    case 1: gemm_epi_kernel<TMA, 4, true><<<grid, 128, SMEM, st>>>(A); break;
+    default: gemm_epi_kernel<TMA, 8, true><<<grid, 256, SMEM, st>>>(A); break;
+  }
 }
 inline void launch_gemm(dim3 grid, const LaunchArgs& A, cudaStream_t st) {
-  const bool wide = gemm_warps(A.NP) == 8;
-  if (A.tma) {
-    if (wide) gemm_epi_kernel<true, 8><<<grid, 256, SMEM, st>>>(A);
-    else gemm_epi_kernel<true, 4><<<grid, 128, SMEM, st>>>(A);
-  } else {
-    if (wide) gemm_epi_kernel<false, 8><<<grid, 256, SMEM, st>>>(A);
-    else gemm_epi_kernel<false, 4><<<grid, 128, SMEM, st>>>(A);
-  }
+  if (A.tma) launch_gemm_t<true>(grid, A, st);
+  else launch_gemm_t<false>(grid, A, st);
 }
 
 #include "ozaki.cuh"
@@ -671,17 +681,13 @@ inline cudaError_t ensure_smem_attr() {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 32 && ((done_mask >> dev) & 1u)) return cudaSuccess;
-  e = cudaFuncSetAttribute(gemm_epi_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(SMEM));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(gemm_epi_kernel<false, 8>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(gemm_epi_kernel<true, 4>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(gemm_epi_kernel<true, 8>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(SMEM));
+  e = cudaSuccess;
+  for (auto k : {gemm_epi_kernel<false, 4, false>, gemm_epi_kernel<false, 4, true>,
+                 gemm_epi_kernel<false, 8, true>, gemm_epi_kernel<true, 4, false>,
+                 gemm_epi_kernel<true, 4, true>, gemm_epi_kernel<true, 8, true>})
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(SMEM));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(oz_crt_epi<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(SMEM));
