@@ -839,11 +839,8 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
     const int nsteps = ch.nsteps, pf_after = ch.pf_after;
     CSM_DCHECK(nsteps >= 1 && nsteps <= 7 && ch.cos_slot >= 0 && ch.cos_slot < NSLOTS);
     CSM_DCHECK(ch.cos_slot != 6 && ch.sin_slot != 6 && ch.free1 != 6 && ch.free2 != 6);
-    // step i's descriptor is read before the barrier that ends step i - 1,
-    // so no warp starts a product behind a shared-memory load issued into
-    // the burst of fragment loads that follows the barrier
-    Step st = ch.step[0];
     for (int i = 0; i < nsteps; ++i) {
+      const Step st = ch.step[i];
       CSM_DCHECK(st.l1 >= 0 && st.l1 < NSLOTS && st.r >= 0 && st.r < NSLOTS &&
                  st.o0 >= 0 && st.o0 < NSLOTS && (!st.dual || (st.l2 >= 0 && st.l2 < NSLOTS)));
       // slot 6 is the next matrix's landing buffer after step pf_after
@@ -873,12 +870,10 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
               : st.scale == SC_TP ? tp : 1.0;
       E.n = n;
       epilogue<CL>(st.epi, E, acc, acc2, keep, ln);
-      const Step nxt = ch.step[i + 1 < nsteps ? i + 1 : i];
       TRACE_T(4);
       step_sync<CL>();
       TRACE_T(5);
       if (i == pf_after && tid == 0) prefetch(bn);
-      st = nxt;
     }
     double* C = slotp(ch.cos_slot);
     double* S = slotp(ch.sin_slot);

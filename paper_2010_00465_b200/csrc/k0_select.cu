@@ -231,10 +231,25 @@ __global__ void cost_scatter_kernel(const int32_t* __restrict__ K, const int32_t
 size_t schedule_ws_bytes() { return kCostBins * sizeof(int); }
 
 // bins: device scratch of schedule_ws_bytes(); order: device int32[batch].
+__global__ void iota_kernel(int32_t* __restrict__ order, int64_t batch) {
+  for (int64_t i = threadIdx.x; i < batch; i += blockDim.x) order[i] = static_cast<int32_t>(i);
+}
+
+// Largest batch scheduled unsorted (order = identity, one launch instead of a
+// memset and three): at most one matrix per CTA of the persistent fused grid
+// (K1: 148 CTAs, K1c: >= 33 resident 4-CTA clusters), so no balancing is
+// needed -- the latency-bound single-matrix path of configs[0].
+constexpr int64_t kUnsortedMax = 32;
+
 cudaError_t launch_schedule(const int32_t* K, const int32_t* S, const int32_t* status,
                             int64_t batch, int* bins, int32_t* order, cudaStream_t stream,
                             int64_t* launches) {
   if (batch == 0) return cudaSuccess;
+  if (batch <= kUnsortedMax) {
+    iota_kernel<<<1, 32, 0, stream>>>(order, batch);
+    *launches += 1;
+    return cudaGetLastError();
+  }
   cudaError_t e = cudaMemsetAsync(bins, 0, schedule_ws_bytes(), stream);
   if (e != cudaSuccess) return e;
   cost_hist_kernel<<<blocks_for(batch, 256), 256, 0, stream>>>(K, S, status, batch, bins);
