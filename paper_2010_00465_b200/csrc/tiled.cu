@@ -125,7 +125,6 @@ struct LaunchArgs {
   // complementary k range from rhs_full and adds part before the epilogue;
   // 0 is the whole contraction.  part: M x NP doubles per launch item y.
   int ksplit;
-  int l2pf;  // bulk-prefetch the epilogue's slot terms into L2 when the tile starts
   double* part;
   // TMA staging (tma = 1): 2-D tensor maps over the slots (rows of every
   // slot of every matrix stacked: row (b mat_stride + sl M NP) / NP + r),
@@ -414,25 +413,6 @@ __global__ void __launch_bounds__(32 * W, W == 8 ? 2 : (BLK ? 3 : CSM_TILED_MINB
     }
     return R + static_cast<size_t>(k0) * NP;
   };
-  // The epilogue reads its slot terms from the workspace (HBM for a large
-  // batch) after the product; one bulk L2 prefetch per term row, issued
-  // now, lets those reads hit L2 instead of exposing HBM latency.
-  if (args.l2pf && args.ksplit != 1) {
-    int nt = 0;
-    for (int q = 0; q < op.nout; ++q)
-      for (int tt = 0; tt < op.out[q].nterms; ++tt) nt += op.out[q].t[tt].src >= 0;
-    for (int j = tid; j < nt * BM; j += GTHREADS) {
-      int want = j / BM, src = -1;
-      for (int q = 0; q < op.nout && src < 0; ++q)
-        for (int tt = 0; tt < op.out[q].nterms && src < 0; ++tt)
-          if (op.out[q].t[tt].src >= 0 && want-- == 0) src = op.out[q].t[tt].src;
-      const double* row = slot(src) + static_cast<size_t>(tm * BM + j % BM) * NP +
-                          static_cast<size_t>(tn) * BN;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(row),
-                   "r"(static_cast<unsigned>(BN * sizeof(double)))
-                   : "memory");
-    }
-  }
   auto ws_row = [&](int sl) -> int {
     return static_cast<int>((static_cast<size_t>(b) * args.mat_stride + sl * slotsz) / NP);
   };
@@ -681,11 +661,6 @@ inline void set_tma(LaunchArgs& A, size_t ws_rows, size_t in0_rows) {
     const char* e = std::getenv("CSM_TILED_TMA");
     return !(e && e[0] == '0');
   }();
-  static const int l2pf = [] {  // epilogue-term L2 prefetch (CSM_TILED_L2PF=0 disables)
-    const char* e = std::getenv("CSM_TILED_L2PF");
-    return (e && e[0] == '0') ? 0 : 1;
-  }();
-  A.l2pf = l2pf;
   A.tma = 0;
   if (!enabled || A.rhs_parts) return;
   const CUtensorMapSwizzle L128 = CU_TENSOR_MAP_SWIZZLE_128B, R64 = CU_TENSOR_MAP_SWIZZLE_64B;
