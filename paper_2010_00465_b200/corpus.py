@@ -10,7 +10,8 @@ matrices are grouped by order n, every group runs in one call per method
 LU, the double-double reference values on csrc/ddref.cu), and each
 record's ``wall_time`` is its group's device time divided by the group
 size.  The spectral-norm relative errors (cli.py:147-150,
-verify.py:524-534) are computed on the device as well.
+verify.py:524-534) are the reference's own metric, evaluated on the host
+with numpy exactly as verify.py does (scoring, not the cos/sin path).
 
 The corpus itself is the caller's (any list of square float64 matrices
 with class tags); tests/golden/corpus.npz holds the reference's own
@@ -46,19 +47,21 @@ class RunRecord:
 
 
 def _rel_err_2(approx, ref) -> "np.ndarray":
-    """relative_error_2 (verify.py:524-534) for a batch, on the device:
-    inf when either side is not finite, 0/0 -> 0, x/0 -> inf."""
-    torch = _torch()
-    fin = torch.isfinite(approx).flatten(1).all(1) & torch.isfinite(ref).flatten(1).all(1)
-    a = torch.where(fin[:, None, None], approx, torch.zeros_like(approx))
-    r = torch.where(fin[:, None, None], ref, torch.zeros_like(ref))
-    num = torch.linalg.matrix_norm(a - r, ord=2)
-    den = torch.linalg.matrix_norm(r, ord=2)
-    out = torch.where(den > 0, num / torch.where(den > 0, den, torch.ones_like(den)),
-                      torch.where(num == 0, torch.zeros_like(num),
-                                  torch.full_like(num, math.inf)))
-    out = torch.where(fin, out, torch.full_like(out, math.inf))
-    return out.cpu().numpy()
+    """relative_error_2 (verify.py:524-534) for a batch: the reference's own
+    metric, evaluated as it is -- numpy's spectral norm on the host (LAPACK
+    SVD) -- on the device results copied back.  It scores a corpus run; it
+    is not part of the cos/sin path, which stays on the device."""
+    a = approx.double().cpu().numpy() if hasattr(approx, "cpu") else np.asarray(approx)
+    r = ref.double().cpu().numpy() if hasattr(ref, "cpu") else np.asarray(ref)
+    out = np.empty(a.shape[0])
+    for i in range(a.shape[0]):
+        if not (np.all(np.isfinite(a[i])) and np.all(np.isfinite(r[i]))):
+            out[i] = math.inf
+            continue
+        den = float(np.linalg.norm(r[i], 2))
+        num = float(np.linalg.norm(a[i] - r[i], 2))
+        out[i] = (0.0 if num == 0.0 else math.inf) if den == 0.0 else num / den
+    return out
 
 
 def _timed(fn):

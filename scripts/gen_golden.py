@@ -12,6 +12,9 @@ Reference entry points exercised (paths under /root/reference):
   norm1          pkg/src/cossinm/matcore.py:100-104
   pade_cos_sin   pkg/src/cossinm/driver.py:149-164
   bench corpus   pkg/src/cossinm/gallery.py:186-220, cli.py:128-163
+  acceptance     pkg/tests/test_acceptance.py:160-254 (criteria 3-5 corpus)
+
+Usage: python scripts/gen_golden.py [acceptance]   (no argument: everything)
 """
 from __future__ import annotations
 
@@ -288,8 +291,47 @@ def gen_corpus():
     np.savez_compressed(os.path.join(OUT, "corpus.npz"), **out)
 
 
+def gen_acceptance():
+    """The corpus of the reference's acceptance criteria 3-5
+    (pkg/tests/test_acceptance.py:160-184: 500 entries, classes
+    162/220/109/9, norms in (1e-4, 1e4), seed 0) with the reference's own
+    per-entry Taylor / Pade (k, s, products) and spectral-norm errors against
+    reference_cos_sin, i.e. everything criteria 3-5 (:187-254) evaluate."""
+    from cossinm.gallery import CorpusSpec, generate_corpus
+    from cossinm.matcore import norm1
+    from cossinm.verify import reference_cos_sin, relative_error_2
+    spec = CorpusSpec(count_per_class=(162, 220, 109, 9), norm_range=(1e-4, 1e4), seed=0)
+    mats, tags, dims = [], [], []
+    rec = {k: [] for k in ("norm", "t_k", "t_s", "t_prod", "t_ec", "t_es", "p_s", "p_prod",
+                           "p_ec", "p_es")}
+    for m, tag in generate_corpus(spec):
+        mats.append(m.ravel())
+        tags.append(tag)
+        dims.append(m.shape[0])
+        with np.errstate(over="ignore", invalid="ignore"):
+            ref = reference_cos_sin(m)
+            t = cossinm.cos_sin(m)
+            p = cossinm.pade_cos_sin(m)
+        rec["norm"].append(norm1(m))
+        rec["t_k"].append(t.scheme_used.k_products)
+        rec["t_s"].append(t.scaling_exponent)
+        rec["t_prod"].append(float(t.total_products))
+        rec["t_ec"].append(relative_error_2(t.result.cos_part, ref.cos_part))
+        rec["t_es"].append(relative_error_2(t.result.sin_part, ref.sin_part))
+        rec["p_s"].append(p.scaling_exponent)
+        rec["p_prod"].append(float(p.total_products))
+        rec["p_ec"].append(relative_error_2(p.result.cos_part, ref.cos_part))
+        rec["p_es"].append(relative_error_2(p.result.sin_part, ref.sin_part))
+    out = {"data": np.concatenate(mats), "dims": np.array(dims), "tags": np.array(tags)}
+    out.update({k: np.array(v) for k, v in rec.items()})
+    np.savez_compressed(os.path.join(OUT, "acceptance_corpus.npz"), **out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if sys.argv[1:] == ["acceptance"]:
+        gen_acceptance()
+        return
     rng = np.random.default_rng(20100465)
     gen_selection(rng)
     gen_trig(rng)
@@ -299,6 +341,7 @@ def main():
     gen_ddref(np.random.default_rng(2010))
     gen_pade(np.random.default_rng(88))
     gen_corpus()
+    gen_acceptance()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 

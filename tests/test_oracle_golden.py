@@ -191,3 +191,19 @@ def test_pade_oracle_matches_reference(golden_dir):
         ref_s = d[f"{name}__sin"]
         if orc.norm1(ref_s) > 0:
             assert rel1(s, ref_s) <= 1e-13, name
+
+
+def test_oracle_selection_on_the_acceptance_corpus(golden_dir):
+    """The oracle's (k, s) for Taylor and s for Pade on the reference's
+    500-entry acceptance corpus (pkg/tests/test_acceptance.py:160-184) equal
+    the reference's own (tests/golden/acceptance_corpus.npz)."""
+    d = np.load(os.path.join(golden_dir, "acceptance_corpus.npz"))
+    off = 0
+    for i, n in enumerate(d["dims"]):
+        a = d["data"][off:off + n * n].reshape(n, n)
+        off += n * n
+        nrm = orc.norm1(a)
+        assert nrm == float(d["norm"][i])
+        k, s = orc.select(nrm, "taylor", "double")
+        assert (k, s) == (int(d["t_k"][i]), int(d["t_s"][i])), i
+        assert orc.select(nrm, "pade", "double")[1] == int(d["p_s"][i]), i
