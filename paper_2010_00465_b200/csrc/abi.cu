@@ -28,6 +28,11 @@ cudaError_t launch_select_norms(const double* norms, int64_t count, int family, 
                                 int32_t* K, int32_t* S, int32_t* status, cudaStream_t stream);
 cudaError_t launch_fill_ks(int32_t* K, int32_t* S, int32_t* status, int64_t batch, int k,
                            cudaStream_t stream);
+int64_t fused64_self_max(int n);
+cudaError_t launch_fused64_self(int dtype, int precision, bool wave, const void* a, void* c,
+                                void* s, const double* t, int32_t* k, int32_t* sx, int32_t* st,
+                                unsigned long long* normbits, int64_t batch, int n,
+                                cudaStream_t stream);
 cudaError_t launch_fused64(int dtype, bool wave, const void* a, void* c, void* s,
                            const double* t, const int32_t* k, const int32_t* sx,
                            const int32_t* st, const int32_t* order, int64_t batch, int n,
@@ -268,6 +273,16 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
   return CSM_SUCCESS;
 }
 
+// CSM_SELF_SELECT=0 keeps the separate K0 launches for small batches too
+// (A/B measurements and the cross-check test).
+bool self_select_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CSM_SELF_SELECT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int pipeline(int dtype, int precision, bool wave, const void* a, const double* t, void* c,
              void* s, int64_t batch, int n, int32_t* k, int32_t* sx, int32_t* status, void* ws,
              size_t ws_bytes, void* stream_v) {
@@ -283,7 +298,18 @@ int pipeline(int dtype, int precision, bool wave, const void* a, const double* t
   if ((rc = check_device())) return rc;
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   CommonWs w = carve(ws, batch);
-  cudaError_t e = cudaMemsetAsync(w.normbits, 0, static_cast<size_t>(batch) * 8, stream);
+  cudaError_t e;
+  if (n > 0 && n <= 64 && batch <= csm::fused64_self_max(n) && self_select_enabled()) {
+    // small batch: K1 selects per CTA, one launch for the whole call
+    csm::prof_begin(stream);
+    e = csm::launch_fused64_self(dtype, precision, wave, a, c, s, t, k, sx, status, w.normbits,
+                                 batch, n, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "fused64 (self-selecting) launch");
+    ++g_launches;
+    csm::prof_end(stream, 1);
+    return CSM_SUCCESS;
+  }
+  e = cudaMemsetAsync(w.normbits, 0, static_cast<size_t>(batch) * 8, stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, static_cast<size_t>(batch) * 4, stream);
   if (e != cudaSuccess) return cuda_fail(e, "memset");
   if (n > 0) {

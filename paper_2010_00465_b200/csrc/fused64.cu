@@ -712,13 +712,44 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
-template <int CL, typename TIn, typename TOut, bool WAVE>
+// The selection of one matrix from its column sums (thread 0 of a
+// self-selecting CTA; out of line so it does not weigh on the chain's
+// register allocation): max over columns, then select_one as select_kernel.
+__device__ __noinline__ void self_select(const double* colsum, int n, int fin, const double* t,
+                                         int family, int precision, int32_t* K, int32_t* S,
+                                         int32_t* ST, unsigned long long* normbits, int* meta) {
+  double norm = 0.0;
+  for (int j = 0; j < n; ++j) norm = fmax(norm, colsum[j]);
+  int st = fin ? kOk : kNonfiniteInput, kk = 0, ss = 0;
+  *normbits = static_cast<unsigned long long>(__double_as_longlong(norm));
+  if (st == kOk) {
+    const double sel = t ? (t[0] * t[0]) * norm : norm;  // driver.py:136
+    st = select_one(sel, dTables.theta[family][precision], dTables.kk[family][precision],
+                    dTables.nent[family], dTables.log2fix, &kk, &ss);
+  }
+  if (st != kOk) kk = ss = 0;
+  *K = kk;
+  *S = ss;
+  *ST = st;
+  meta[0] = kk;
+  meta[1] = ss;
+  meta[2] = st;
+}
+
+// SELF (K1 only, batch <= grid): no K0 launches before this one -- CTA b
+// takes matrix b, computes its 1-norm (column sums in row order, in the
+// input dtype, exactly as norm1_kernel), finiteness and (k, s) itself
+// (select_one), and writes K / Sx / ST / normbits for the caller.  The
+// latency-bound small-batch path (configs[0]) becomes a single launch.
+template <int CL, typename TIn, typename TOut, bool WAVE, bool SELF>
 __global__ void __launch_bounds__(Geo<CL>::THREADS, 1)
 fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
              TOut* __restrict__ Sout, const double* __restrict__ T,
              const int32_t* __restrict__ K, const int32_t* __restrict__ Sx,
              const int32_t* __restrict__ ST, const int32_t* __restrict__ order,
-             int64_t batch, int n, int tma) {
+             int64_t batch, int n, int tma, int precision,
+             unsigned long long* __restrict__ normbits) {
+  static_assert(!SELF || CL == 1, "self-selection is the K1 small-batch path");
   constexpr int NP = Geo<CL>::NP, BAND = Geo<CL>::BAND, THREADS = Geo<CL>::THREADS;
   extern __shared__ __align__(128) double smem[];
   // Static schedule: cluster c takes order[] positions c, 2G-1-c, 2G+c, ...
@@ -758,11 +789,13 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
   if (tid == 0) {
     mbar_init(&sh_bar, 1);
     const long long p0 = posof(0), p1 = posof(1);
-    const int b0 = p0 < batch ? order[p0] : -1;
+    const int b0 = p0 < batch ? (SELF ? static_cast<int>(p0) : order[p0]) : -1;
     sh_b[0] = b0;
-    sh_b[1] = p1 < batch ? order[p1] : -1;
+    sh_b[1] = (SELF || p1 >= batch) ? -1 : order[p1];
     if (b0 >= 0) {
-      sh_meta[0][0] = K[b0]; sh_meta[0][1] = Sx[b0]; sh_meta[0][2] = ST[b0];
+      if (!SELF) {
+        sh_meta[0][0] = K[b0]; sh_meta[0][1] = Sx[b0]; sh_meta[0][2] = ST[b0];
+      }
       sh_t[0] = WAVE ? T[b0] : 0.0;
       prefetch(b0);
     }
@@ -776,11 +809,42 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
     const int b = sh_b[it & 3], bn = sh_b[(it + 1) & 3];
     if (b < 0) break;
     if (tma_here) mbar_wait(&sh_bar, it & 1);  // this matrix's band has landed
+    if constexpr (SELF) {  // K0 in the CTA: norm1_kernel + select_kernel for matrix b
+      const TIn* src0 = Ain + static_cast<size_t>(b) * nn;
+      if (!tma_here) {  // unaligned: stage the matrix (the loop below does it otherwise)
+        for (int p = tid; p < n * n; p += THREADS) reinterpret_cast<TIn*>(land)[p] = src0[p];
+        __syncthreads();
+      }
+      double* colsum = reinterpret_cast<double*>(acc);  // scratch: acc is free here
+      (void)colsum;
+      __shared__ double sh_col[64];
+      __shared__ int sh_fin;
+      if (tid == 0) sh_fin = 1;
+      __syncthreads();
+      if (tid < n) {
+        const TIn* nat = reinterpret_cast<const TIn*>(land);
+        TIn sum = TIn(0);
+        bool fin = true;
+        for (int i = 0; i < n; ++i) {
+          const TIn x = nat[i * n + tid];
+          fin &= (x - x == TIn(0));
+          sum = sum + fabs(x);  // sequential in row order, as norm1_kernel
+        }
+        sh_col[tid] = static_cast<double>(sum);
+        if (!fin) sh_fin = 0;
+      }
+      __syncthreads();
+      if (tid == 0)
+        self_select(sh_col, n, sh_fin, WAVE ? T + b : nullptr, WAVE ? 1 : 0, precision,
+                    const_cast<int32_t*>(K) + b, const_cast<int32_t*>(Sx) + b,
+                    const_cast<int32_t*>(ST) + b, normbits + b, sh_meta[it & 1]);
+      __syncthreads();
+    }
     const int k = sh_meta[it & 1][0], s = sh_meta[it & 1][1], status = sh_meta[it & 1][2];
     const double tcur = sh_t[it & 1];
     TRACE_T(1);
     CSM_TRACE_EV(9, static_cast<unsigned long long>(k * 16 + s));
-    if (tid == 0) {  // stage ids and metadata for the coming turns
+    if (!SELF && tid == 0) {  // stage ids and metadata for the coming turns
       const long long p2 = posof(it + 2);
       if (p2 < batch) cp_async4(&sh_b[(it + 2) & 3], order + p2);
       else sh_b[(it + 2) & 3] = -1;
@@ -793,7 +857,7 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
       cp_async_commit();
     }
     const TIn* src = Ain + static_cast<size_t>(b) * nn + band_off;
-    if (!tma_here && rows_here > 0) {  // unaligned band: synchronous staging copy
+    if (!SELF && !tma_here && rows_here > 0) {  // unaligned band: synchronous staging copy
       for (int p = tid; p < rows_here * n; p += THREADS)
         reinterpret_cast<TIn*>(land)[p] = src[p];
       __syncthreads();
@@ -891,16 +955,25 @@ size_t fused64_smem_bytes() {
   return static_cast<size_t>(f64k::NSLOTS) * f64k::SLOT * sizeof(double);
 }
 
-template <int CL, typename TIn, typename TOut, bool WAVE>
-static cudaError_t launch_one(const void* a, void* c, void* s, const double* t,
-                              const int32_t* k, const int32_t* sx,
-                              const int32_t* st, const int32_t* order, int64_t batch,
-                              int n, int sms, cudaStream_t stream) {
-  auto kern = f64k::fused64_kernel<CL, TIn, TOut, WAVE>;
+// Launch arguments shared by every instantiation.
+struct FusedArgs {
+  const void* a;
+  void *c, *s;
+  const double* t;
+  const int32_t *k, *sx, *st, *order;
+  int64_t batch;
+  int n, sms, precision;
+  unsigned long long* normbits;  // self-selection only
+  cudaStream_t stream;
+};
+
+template <int CL, typename TIn, typename TOut, bool WAVE, bool SELF>
+static cudaError_t launch_one(const FusedArgs& F) {
+  auto kern = f64k::fused64_kernel<CL, TIn, TOut, WAVE, SELF>;
   const size_t smem = fused64_smem_bytes();
-  const size_t mat_bytes = static_cast<size_t>(n) * n * sizeof(TIn);
+  const size_t mat_bytes = static_cast<size_t>(F.n) * F.n * sizeof(TIn);
   // TMA needs 16-byte aligned matrix starts; K1c checks each band's size
-  const int tma = (mat_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0) ? 1 : 0;
+  const int tma = (mat_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(F.a) % 16 == 0) ? 1 : 0;
   cudaError_t e = cudaFuncSetAttribute(
       kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -908,8 +981,8 @@ static cudaError_t launch_one(const void* a, void* c, void* s, const double* t,
   cudaLaunchAttribute attr[1];
   cfg.blockDim = dim3(f64k::Geo<CL>::THREADS);
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  int clusters = sms;
+  cfg.stream = F.stream;
+  int clusters = F.sms;
   if (CL > 1) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL;
@@ -917,37 +990,38 @@ static cudaError_t launch_one(const void* a, void* c, void* s, const double* t,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3(CL * (sms / CL));
+    cfg.gridDim = dim3(CL * (F.sms / CL));
     int active = 0;
     e = cudaOccupancyMaxActiveClusters(&active, kern, &cfg);
     if (e != cudaSuccess) return e;
-    clusters = active > 0 ? active : sms / CL;  // persistent: every cluster resident
+    clusters = active > 0 ? active : F.sms / CL;  // persistent: every cluster resident
   }
-  if (clusters > batch) clusters = static_cast<int>(batch);
+  if (clusters > F.batch) clusters = static_cast<int>(F.batch);
   if (clusters < 1) return cudaSuccess;
+  if (SELF && clusters < F.batch) return cudaErrorInvalidValue;  // one matrix per CTA
   cfg.gridDim = dim3(CL * clusters);
-  return cudaLaunchKernelEx(&cfg, kern, static_cast<const TIn*>(a), static_cast<TOut*>(c),
-                            static_cast<TOut*>(s), t, k, sx, st, order, batch, n, tma);
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<const TIn*>(F.a), static_cast<TOut*>(F.c),
+                            static_cast<TOut*>(F.s), F.t, F.k, F.sx, F.st, F.order, F.batch, F.n,
+                            tma, F.precision, F.normbits);
 }
 
-template <int CL>
-static cudaError_t launch_fused(int dtype, bool wave, const void* a, void* c, void* s,
-                                const double* t, const int32_t* k, const int32_t* sx,
-                                const int32_t* st, const int32_t* order, int64_t batch, int n,
-                                cudaStream_t stream) {
+template <int CL, bool SELF>
+static cudaError_t launch_fused(int dtype, bool wave, const FusedArgs& F) {
+  if (dtype == 0)
+    return wave ? launch_one<CL, double, double, true, SELF>(F)
+                : launch_one<CL, double, double, false, SELF>(F);
+  if (dtype == 2)
+    return wave ? launch_one<CL, float, double, true, SELF>(F)
+                : launch_one<CL, float, double, false, SELF>(F);
+  return wave ? launch_one<CL, float, float, true, SELF>(F)
+              : launch_one<CL, float, float, false, SELF>(F);
+}
+
+static int device_sms() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (dtype == 0) {
-    return wave ? launch_one<CL, double, double, true>(a, c, s, t, k, sx, st, order, batch, n, sms, stream)
-                : launch_one<CL, double, double, false>(a, c, s, t, k, sx, st, order, batch, n, sms, stream);
-  }
-  if (dtype == 2) {
-    return wave ? launch_one<CL, float, double, true>(a, c, s, t, k, sx, st, order, batch, n, sms, stream)
-                : launch_one<CL, float, double, false>(a, c, s, t, k, sx, st, order, batch, n, sms, stream);
-  }
-  return wave ? launch_one<CL, float, float, true>(a, c, s, t, k, sx, st, order, batch, n, sms, stream)
-              : launch_one<CL, float, float, false>(a, c, s, t, k, sx, st, order, batch, n, sms, stream);
+  return sms;
 }
 
 // SMs the K1c grid occupies (4 x co-resident clusters; the rest of the GPU
@@ -959,7 +1033,7 @@ int k1c_resident_sms() {
   cudaGetDevice(&dev);
   dev = dev < 32 ? dev : 31;
   if (cached[dev] >= 0) return cached[dev];
-  auto kern = f64k::fused64_kernel<4, double, double, false>;
+  auto kern = f64k::fused64_kernel<4, double, double, false, false>;
   const size_t smem = fused64_smem_bytes();
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem)) != cudaSuccess)
@@ -987,8 +1061,24 @@ cudaError_t launch_fused64(int dtype, bool wave, const void* a, void* c,
                            void* s, const double* t, const int32_t* k,
                            const int32_t* sx, const int32_t* st, const int32_t* order,
                            int64_t batch, int n, cudaStream_t stream) {
-  if (n <= 64) return launch_fused<1>(dtype, wave, a, c, s, t, k, sx, st, order, batch, n, stream);
-  return launch_fused<4>(dtype, wave, a, c, s, t, k, sx, st, order, batch, n, stream);
+  const FusedArgs F{a, c, s, t, k, sx, st, order, batch, n, device_sms(), 0, nullptr, stream};
+  if (n <= 64) return launch_fused<1, false>(dtype, wave, F);
+  return launch_fused<4, false>(dtype, wave, F);
+}
+
+// Largest batch K1 runs self-selecting (one CTA per matrix, no K0 launches).
+int64_t fused64_self_max(int n) { return n <= 64 ? device_sms() : 0; }
+
+// K1 with the norm, finiteness and (k, s) selection done by each CTA for
+// its own matrix: writes k / sx / st / normbits; batch <= fused64_self_max.
+cudaError_t launch_fused64_self(int dtype, int precision, bool wave, const void* a, void* c,
+                                void* s, const double* t, int32_t* k, int32_t* sx, int32_t* st,
+                                unsigned long long* normbits, int64_t batch, int n,
+                                cudaStream_t stream) {
+  if (n > 64 || n < 1 || batch > fused64_self_max(n)) return cudaErrorInvalidValue;
+  const FusedArgs F{a, c, s, t, k, sx, st, nullptr, batch, n, device_sms(), precision,
+                    normbits, stream};
+  return launch_fused<1, true>(dtype, wave, F);
 }
 
 }  // namespace csm
