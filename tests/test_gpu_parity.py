@@ -660,9 +660,12 @@ def test_self_selecting_small_batches(cuda, n):
         assert np.array_equal(sub.k.cpu().numpy(), full.k.cpu().numpy()[idx])
         assert np.array_equal(sub.s.cpu().numpy(), full.s.cpu().numpy()[idx])
         assert np.array_equal(sub.status.cpu().numpy(), full.status.cpu().numpy()[idx])
-        ok = [j for j, i in enumerate(idx) if int(full.status[i]) == 0]
-        assert torch.equal(sub.cos_part[ok], full.cos_part[[idx[j] for j in ok]])
-        assert torch.equal(sub.sin_part[ok], full.sin_part[[idx[j] for j in ok]])
+        # matrix 5 (float64): finite norm ~1e308, s ~ 1000 doublings -> NaN in
+        # both paths, so compare with NaNs equal
+        assert np.array_equal(sub.cos_part.cpu().numpy(), full.cos_part[idx].cpu().numpy(),
+                              equal_nan=True)
+        assert np.array_equal(sub.sin_part.cpu().numpy(), full.sin_part[idx].cpu().numpy(),
+                              equal_nan=True)
         assert int(sub.status[3]) == 1
     t = 10.0 ** rng.uniform(-2, 0.5, 160)
     w = big[:, :, :] * 0.01
