@@ -42,6 +42,8 @@
 //
 // Reference mapping: chains schemes.py:264-361, trig use :376-395, wave use
 // :411-430, scaling driver.py:115/:139, doubling driver.py:91-98.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace csm {
@@ -80,13 +82,18 @@ __device__ __forceinline__ int& trace_count() {
 #ifndef CSM_K1_THREADS
 #define CSM_K1_THREADS 512
 #endif
-template <int CL> struct Geo;
+template <int V> struct Geo;  // V: the kernel variant (1: K1, 4: K1c, 5: K1s)
 template <> struct Geo<1> {
-  static constexpr int NP = 64, BAND = 64, THREADS = CSM_K1_THREADS, MI = 2,
+  static constexpr int CL = 1, NP = 64, BAND = 64, THREADS = CSM_K1_THREADS, MI = 2,
                        NI = THREADS == 512 ? 2 : 4;
 };
 template <> struct Geo<4> {
-  static constexpr int NP = 128, BAND = 32, THREADS = 256, MI = 4, NI = 2;
+  static constexpr int CL = 4, NP = 128, BAND = 32, THREADS = 256, MI = 4, NI = 2;
+};
+// K1s: one n <= 64 matrix over a 4-CTA cluster (16-row bands, 4 warps of
+// 16 x 16): the latency-bound small-batch path, a quarter product per SM.
+template <> struct Geo<5> {
+  static constexpr int CL = 4, NP = 64, BAND = 16, THREADS = 128, MI = 2, NI = 2;
 };
 static_assert(Geo<1>::THREADS == 256 || Geo<1>::THREADS == 512, "K1: 8 or 16 warps");
 constexpr int SLOT = 4096;  // doubles per slot band (64 x 64 or 32 x 128)
@@ -215,10 +222,10 @@ template <int CL>
 __device__ __forceinline__ void make_lane(Lane<CL>& ln, int rank) {
   constexpr int NP = Geo<CL>::NP, MI = Geo<CL>::MI, NI = Geo<CL>::NI;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (CL == 1 && Geo<CL>::THREADS == 512) {
+  if (Geo<CL>::CL == 1 && Geo<CL>::THREADS == 512) {
     ln.rb = (warp >> 2) * 16;
     ln.cb = (warp & 3) * 16;
-  } else if (CL == 1) {
+  } else if (Geo<CL>::CL == 1) {
     ln.rb = (warp >> 1) * 16;
     ln.cb = (warp & 1) * 32;
   } else {
@@ -255,19 +262,20 @@ __device__ __forceinline__ void zero(Acc& a) {
 // four different owners at any time instead of all hammering one.
 template <int CL>
 struct RView {
-  const double* p[CL];
-  int lcol[CL];
+  const double* p[Geo<CL>::CL];
+  int lcol[Geo<CL>::CL];
 };
 template <int CL>
 __device__ __forceinline__ RView<CL> rview(const double* R, int rank) {
   RView<CL> v;
-  if constexpr (CL == 1) {
+  constexpr int NC = Geo<CL>::CL;
+  if constexpr (NC == 1) {
     v.p[0] = R;
     v.lcol[0] = 0;
   } else {
 #pragma unroll
-    for (int i = 0; i < CL; ++i) {
-      const int o = (rank + i) & (CL - 1);
+    for (int i = 0; i < NC; ++i) {
+      const int o = (rank + i) & (NC - 1);
       // own band (i = 0) through the local shared window: no cluster
       // round trip for the k-steps right after the barrier
       v.p[i] = i == 0 ? R
@@ -289,7 +297,7 @@ __device__ __forceinline__ void gemm(const double* __restrict__ L,
   constexpr int NP = Geo<CL>::NP, BAND = Geo<CL>::BAND, MI = Geo<CL>::MI, NI = Geo<CL>::NI;
   zero(acc);
   if (DUAL) zero(acc2);
-  if constexpr (CL > 1) {
+  if constexpr (Geo<CL>::CL > 1) {
     // R arrives over DSMEM (hundreds of cycles): keep PF k-steps of B
     // fragments in flight in a register ring.
     constexpr int NK = NP / 4;
@@ -368,7 +376,7 @@ __device__ __forceinline__ void st2(double* p, int off, double x, double y) {
 // release/acquire so band writes are visible to the peers' DSMEM loads).
 template <int CL>
 __device__ __forceinline__ void step_sync() {
-  if constexpr (CL == 1) {
+  if constexpr (Geo<CL>::CL == 1) {
     __syncthreads();
   } else {
 #ifdef CSM_CLUSTER_RELAXED
@@ -717,20 +725,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // register allocation): max over columns, then select_one as select_kernel.
 __device__ __noinline__ void self_select(const double* colsum, int n, int fin, const double* t,
                                          int family, int precision, int32_t* K, int32_t* S,
-                                         int32_t* ST, unsigned long long* normbits, int* meta) {
+                                         int32_t* ST, unsigned long long* normbits, int* meta,
+                                         bool write_out) {
   double norm = 0.0;
   for (int j = 0; j < n; ++j) norm = fmax(norm, colsum[j]);
   int st = fin ? kOk : kNonfiniteInput, kk = 0, ss = 0;
-  *normbits = static_cast<unsigned long long>(__double_as_longlong(norm));
+  if (write_out) *normbits = static_cast<unsigned long long>(__double_as_longlong(norm));
   if (st == kOk) {
     const double sel = t ? (t[0] * t[0]) * norm : norm;  // driver.py:136
     st = select_one(sel, dTables.theta[family][precision], dTables.kk[family][precision],
                     dTables.nent[family], dTables.log2fix, &kk, &ss);
   }
   if (st != kOk) kk = ss = 0;
-  *K = kk;
-  *S = ss;
-  *ST = st;
+  if (write_out) {
+    *K = kk;
+    *S = ss;
+    *ST = st;
+  }
   meta[0] = kk;
   meta[1] = ss;
   meta[2] = st;
@@ -749,7 +760,8 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
              const int32_t* __restrict__ ST, const int32_t* __restrict__ order,
              int64_t batch, int n, int tma, int precision,
              unsigned long long* __restrict__ normbits) {
-  static_assert(!SELF || CL == 1, "self-selection is the K1 small-batch path");
+  static_assert(!SELF || CL == 1 || CL == 5, "self-selection: the small-batch variants");
+  constexpr int NC = Geo<CL>::CL;  // CTAs per matrix (a cluster when > 1)
   constexpr int NP = Geo<CL>::NP, BAND = Geo<CL>::BAND, THREADS = Geo<CL>::THREADS;
   extern __shared__ __align__(128) double smem[];
   // Static schedule: cluster c takes order[] positions c, 2G-1-c, 2G+c, ...
@@ -760,9 +772,10 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
   __shared__ int sh_meta[2][4];
   __shared__ double sh_t[2];
   __shared__ __align__(8) uint64_t sh_bar;
+  __shared__ __align__(8) uint64_t sh_bar2;  // K1s self-selection: the whole matrix
   __shared__ Chain sh_chain[7];
   const int tid = threadIdx.x;
-  const int G = gridDim.x / CL, cta = blockIdx.x / CL, rank = blockIdx.x % CL;
+  const int G = gridDim.x / NC, cta = blockIdx.x / NC, rank = blockIdx.x % NC;
   Lane<CL> ln;
   make_lane(ln, rank);
   const size_t nn = static_cast<size_t>(n) * n;
@@ -788,6 +801,7 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
     reinterpret_cast<int*>(sh_chain)[i] = reinterpret_cast<const int*>(kChains)[i];
   if (tid == 0) {
     mbar_init(&sh_bar, 1);
+    if (SELF && NC > 1) mbar_init(&sh_bar2, 1);
     const long long p0 = posof(0), p1 = posof(1);
     const int b0 = p0 < batch ? (SELF ? static_cast<int>(p0) : order[p0]) : -1;
     sh_b[0] = b0;
@@ -798,6 +812,9 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
       }
       sh_t[0] = WAVE ? T[b0] : 0.0;
       prefetch(b0);
+      if (SELF && NC > 1 && tma)
+        tma_load_1d(smem + 5 * SLOT, Ain + static_cast<size_t>(b0) * nn,
+                    static_cast<unsigned>(nn * sizeof(TIn)), &sh_bar2);
     }
   }
   __syncthreads();
@@ -810,19 +827,22 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
     if (b < 0) break;
     if (tma_here) mbar_wait(&sh_bar, it & 1);  // this matrix's band has landed
     if constexpr (SELF) {  // K0 in the CTA: norm1_kernel + select_kernel for matrix b
+      // the whole matrix: K1's band is the matrix; each K1s CTA holds a
+      // full copy in slot 5's region (free until the chain starts) and
+      // selects redundantly, so the cluster agrees without communication
       const TIn* src0 = Ain + static_cast<size_t>(b) * nn;
-      if (!tma_here) {  // unaligned: stage the matrix (the loop below does it otherwise)
-        for (int p = tid; p < n * n; p += THREADS) reinterpret_cast<TIn*>(land)[p] = src0[p];
+      TIn* whole = NC == 1 ? reinterpret_cast<TIn*>(land) : reinterpret_cast<TIn*>(smem + 5 * SLOT);
+      if (NC > 1 && tma) mbar_wait(&sh_bar2, it & 1);
+      if (NC == 1 ? !tma_here : !tma) {  // unaligned: stage the matrix
+        for (int p = tid; p < n * n; p += THREADS) whole[p] = src0[p];
         __syncthreads();
       }
-      double* colsum = reinterpret_cast<double*>(acc);  // scratch: acc is free here
-      (void)colsum;
       __shared__ double sh_col[64];
       __shared__ int sh_fin;
       if (tid == 0) sh_fin = 1;
       __syncthreads();
       if (tid < n) {
-        const TIn* nat = reinterpret_cast<const TIn*>(land);
+        const TIn* nat = whole;
         TIn sum = TIn(0);
         bool fin = true;
         for (int i = 0; i < n; ++i) {
@@ -837,7 +857,7 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
       if (tid == 0)
         self_select(sh_col, n, sh_fin, WAVE ? T + b : nullptr, WAVE ? 1 : 0, precision,
                     const_cast<int32_t*>(K) + b, const_cast<int32_t*>(Sx) + b,
-                    const_cast<int32_t*>(ST) + b, normbits + b, sh_meta[it & 1]);
+                    const_cast<int32_t*>(ST) + b, normbits + b, sh_meta[it & 1], rank == 0);
       __syncthreads();
     }
     const int k = sh_meta[it & 1][0], s = sh_meta[it & 1][1], status = sh_meta[it & 1][2];
@@ -857,7 +877,7 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
       cp_async_commit();
     }
     const TIn* src = Ain + static_cast<size_t>(b) * nn + band_off;
-    if (!SELF && !tma_here && rows_here > 0) {  // unaligned band: synchronous staging copy
+    if ((!SELF || NC > 1) && !tma_here && rows_here > 0) {  // unaligned band: synchronous copy
       for (int p = tid; p < rows_here * n; p += THREADS)
         reinterpret_cast<TIn*>(land)[p] = src[p];
       __syncthreads();
@@ -882,7 +902,7 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
       const double g = WAVE ? f : 1.0;
       const TIn* nat = reinterpret_cast<const TIn*>(land);
 #pragma unroll 2
-      for (int p = tid; p < SLOT / 2; p += THREADS) {
+      for (int p = tid; p < BAND * NP / 2; p += THREADS) {
         const int r = p / (NP / 2), c = (p % (NP / 2)) * 2;
         double v0 = 0.0, v1 = 0.0;
         if (n == NP) {
@@ -946,7 +966,7 @@ fused64_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout,
     doubling<CL>(C, S, F1, F2, s, ln, cdst, sdst, n);
   }
   // no CTA may leave while a peer can still read its bands
-  if (CL > 1) step_sync<CL>();
+  if (NC > 1) step_sync<CL>();
 }
 
 }  // namespace f64k
@@ -983,23 +1003,24 @@ static cudaError_t launch_one(const FusedArgs& F) {
   cfg.dynamicSmemBytes = smem;
   cfg.stream = F.stream;
   int clusters = F.sms;
-  if (CL > 1) {
+  constexpr int NC = f64k::Geo<CL>::CL;
+  if (NC > 1) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.x = NC;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3(CL * (F.sms / CL));
+    cfg.gridDim = dim3(NC * (F.sms / NC));
     int active = 0;
     e = cudaOccupancyMaxActiveClusters(&active, kern, &cfg);
     if (e != cudaSuccess) return e;
-    clusters = active > 0 ? active : F.sms / CL;  // persistent: every cluster resident
+    clusters = active > 0 ? active : F.sms / NC;  // persistent: every cluster resident
   }
   if (clusters > F.batch) clusters = static_cast<int>(F.batch);
   if (clusters < 1) return cudaSuccess;
   if (SELF && clusters < F.batch) return cudaErrorInvalidValue;  // one matrix per CTA
-  cfg.gridDim = dim3(CL * clusters);
+  cfg.gridDim = dim3(NC * clusters);
   return cudaLaunchKernelEx(&cfg, kern, static_cast<const TIn*>(F.a), static_cast<TOut*>(F.c),
                             static_cast<TOut*>(F.s), F.t, F.k, F.sx, F.st, F.order, F.batch, F.n,
                             tma, F.precision, F.normbits);
@@ -1066,6 +1087,41 @@ cudaError_t launch_fused64(int dtype, bool wave, const void* a, void* c,
   return launch_fused<4, false>(dtype, wave, F);
 }
 
+// Co-resident 4-CTA clusters of K1s (0 when CSM_K1S=0 disables it).
+static int k1s_clusters() {
+  static const bool on = [] {
+    const char* e = std::getenv("CSM_K1S");
+    return !(e && e[0] == '0');
+  }();
+  if (!on) return 0;
+  static int cached[32] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1,
+                           -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev = dev < 32 ? dev : 31;
+  if (cached[dev] >= 0) return cached[dev];
+  auto kern = f64k::fused64_kernel<5, double, double, false, true>;
+  const size_t smem = fused64_smem_bytes();
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess)
+    return 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 4;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(f64k::Geo<5>::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.gridDim = dim3(4 * 32);
+  int active = 0;
+  if (cudaOccupancyMaxActiveClusters(&active, kern, &cfg) != cudaSuccess) return 0;
+  cached[dev] = active;
+  return active;
+}
+
 // Largest batch K1 runs self-selecting (one CTA per matrix, no K0 launches).
 int64_t fused64_self_max(int n) { return n <= 64 ? device_sms() : 0; }
 
@@ -1078,6 +1134,9 @@ cudaError_t launch_fused64_self(int dtype, int precision, bool wave, const void*
   if (n > 64 || n < 1 || batch > fused64_self_max(n)) return cudaErrorInvalidValue;
   const FusedArgs F{a, c, s, t, k, sx, st, nullptr, batch, n, device_sms(), precision,
                     normbits, stream};
+  // a batch that fits the co-resident 4-CTA clusters runs on K1s: each
+  // matrix over four SMs, a quarter of every product per SM
+  if (batch <= k1s_clusters()) return launch_fused<5, true>(dtype, wave, F);
   return launch_fused<1, true>(dtype, wave, F);
 }
 

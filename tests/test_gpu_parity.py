@@ -644,16 +644,18 @@ def test_pade_errors(cuda):
 def test_self_selecting_small_batches(cuda, n):
     """Batches no larger than the K1 grid (<= 148 matrices, n <= 64) run as
     ONE launch whose CTAs compute their matrix's norm, finiteness and (k, s)
-    themselves.  Bitwise the same cos / sin / k / s / status as the K0 path
-    that a larger batch takes (position invariance), for float64, float32
-    storage, the wave family and bad inputs."""
+    themselves -- on K1s (each matrix over a 4-CTA cluster) while the batch
+    fits the co-resident clusters, else on K1 (one CTA per matrix).
+    Bitwise the same cos / sin / k / s / status as the K0 path that a
+    larger batch takes (position invariance), for float64, float32 storage,
+    the wave family and bad inputs."""
     import torch
     rng = np.random.default_rng(700 + n)
     big = cfg2_like(rng, 160, n=n)
     big[3, 0, 0] = np.nan                       # status 1
     big[5] *= 1e306                             # norm overflow paths
-    idx = [0, 1, 2, 3, 4, 5, 77, 159]
-    for a in (big, big.astype(np.float32)):
+    for idx in ([0, 1, 2, 3, 4, 5, 77, 159], list(range(100))):  # K1s, K1
+      for a in (big, big.astype(np.float32)):
         prec = csm.Precision.DOUBLE if a.dtype == np.float64 else csm.Precision.SINGLE
         full = csm.cos_sin_batched(torch.from_numpy(a).to(cuda), prec, raise_on_error=False)
         sub = csm.cos_sin_batched(torch.from_numpy(a[idx]).to(cuda), prec, raise_on_error=False)
@@ -670,12 +672,15 @@ def test_self_selecting_small_batches(cuda, n):
     t = 10.0 ** rng.uniform(-2, 0.5, 160)
     w = big[:, :, :] * 0.01
     w[3, 0, 0] = 1.0
+    w[5] = w[6]
     fw = csm.wave_cos_sin_batched(torch.from_numpy(w).to(cuda), torch.from_numpy(t).to(cuda))
-    sw = csm.wave_cos_sin_batched(torch.from_numpy(w[idx]).to(cuda),
-                                  torch.from_numpy(t[idx]).to(cuda))
-    assert np.array_equal(sw.k.cpu().numpy(), fw.k.cpu().numpy()[idx])
-    assert np.array_equal(sw.s.cpu().numpy(), fw.s.cpu().numpy()[idx])
-    assert torch.equal(sw.cos_part, fw.cos_part[idx]) and torch.equal(sw.sin_part, fw.sin_part[idx])
+    for idx in ([0, 1, 2, 3, 4, 5, 77, 159], list(range(100))):
+        sw = csm.wave_cos_sin_batched(torch.from_numpy(w[idx]).to(cuda),
+                                      torch.from_numpy(t[idx]).to(cuda))
+        assert np.array_equal(sw.k.cpu().numpy(), fw.k.cpu().numpy()[idx])
+        assert np.array_equal(sw.s.cpu().numpy(), fw.s.cpu().numpy()[idx])
+        assert torch.equal(sw.cos_part, fw.cos_part[idx])
+        assert torch.equal(sw.sin_part, fw.sin_part[idx])
     # the self-selecting path against the oracle, and the reference's
     # exception on a bad matrix
     sub = csm.cos_sin_batched(big[[0, 1, 77]])
