@@ -84,15 +84,18 @@ __device__ __forceinline__ int& trace_count() {
 #endif
 template <int V> struct Geo;  // V: the kernel variant (1: K1, 4: K1c, 5: K1s)
 template <> struct Geo<1> {
+  static constexpr bool ROTATE = false;
   static constexpr int CL = 1, NP = 64, BAND = 64, THREADS = CSM_K1_THREADS, MI = 2,
                        NI = THREADS == 512 ? 2 : 4;
 };
 template <> struct Geo<4> {
+  static constexpr bool ROTATE = true;  // each CTA starts the k loop at its own band
   static constexpr int CL = 4, NP = 128, BAND = 32, THREADS = 256, MI = 4, NI = 2;
 };
 // K1s: one n <= 64 matrix over a 4-CTA cluster (16-row bands, 4 warps of
 // 16 x 16): the latency-bound small-batch path, a quarter product per SM.
 template <> struct Geo<5> {
+  static constexpr bool ROTATE = false;
   static constexpr int CL = 4, NP = 64, BAND = 16, THREADS = 128, MI = 2, NI = 2;
 };
 static_assert(Geo<1>::THREADS == 256 || Geo<1>::THREADS == 512, "K1: 8 or 16 warps");
@@ -275,12 +278,13 @@ __device__ __forceinline__ RView<CL> rview(const double* R, int rank) {
   } else {
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
-      const int o = (rank + i) & (NC - 1);
-      // own band (i = 0) through the local shared window: no cluster
-      // round trip for the k-steps right after the barrier
-      v.p[i] = i == 0 ? R
-                      : static_cast<const double*>(
-                            __cluster_map_shared_rank(const_cast<double*>(R), o));
+      // K1c starts at its own band; K1s keeps the natural k order, so its
+      // accumulation order -- and every bit of its results -- is K1's
+      const int o = Geo<CL>::ROTATE ? (rank + i) & (NC - 1) : i;
+      // own band through the local shared window: no cluster round trip
+      v.p[i] = o == rank ? R
+                         : static_cast<const double*>(
+                               __cluster_map_shared_rank(const_cast<double*>(R), o));
       v.lcol[i] = Geo<CL>::BAND * o;  // L columns of band o (swizzle keeps 8-chunk blocks)
     }
   }
