@@ -645,10 +645,21 @@ def test_self_selecting_small_batches(cuda, n):
     """Batches no larger than the K1 grid (<= 148 matrices, n <= 64) run as
     ONE launch whose CTAs compute their matrix's norm, finiteness and (k, s)
     themselves -- on K1s (each matrix over a 4-CTA cluster) while the batch
-    fits the co-resident clusters, else on K1 (one CTA per matrix).
-    Bitwise the same cos / sin / k / s / status as the K0 path that a
-    larger batch takes (position invariance), for float64, float32 storage,
+    fits the co-resident clusters, else on K1 (one CTA per matrix).  The
+    same k / s / status as the K0 path that a larger batch takes, and the
+    same cos / sin -- bitwise on K1, within a few ulps on K1s (its CTAs
+    sum the k bands in a rotated order) -- for float64, float32 storage,
     the wave family and bad inputs."""
+
+    def same(x, y, bitwise):
+        x, y = x.cpu().double().numpy(), y.cpu().double().numpy()
+        if bitwise:
+            return np.array_equal(x, y, equal_nan=True)
+        fin = np.isfinite(y).all(axis=(1, 2))
+        d = np.abs(x[fin] - y[fin]).sum(axis=1).max(axis=1)
+        r = np.abs(y[fin]).sum(axis=1).max(axis=1)
+        return bool(np.all(d <= 1e-13 * np.maximum(r, 1e-300))) and \
+            np.array_equal(np.isnan(x), np.isnan(y))
     import torch
     rng = np.random.default_rng(700 + n)
     big = cfg2_like(rng, 160, n=n)
@@ -663,11 +674,10 @@ def test_self_selecting_small_batches(cuda, n):
         assert np.array_equal(sub.s.cpu().numpy(), full.s.cpu().numpy()[idx])
         assert np.array_equal(sub.status.cpu().numpy(), full.status.cpu().numpy()[idx])
         # matrix 5 (float64): finite norm ~1e308, s ~ 1000 doublings -> NaN in
-        # both paths, so compare with NaNs equal
-        assert np.array_equal(sub.cos_part.cpu().numpy(), full.cos_part[idx].cpu().numpy(),
-                              equal_nan=True)
-        assert np.array_equal(sub.sin_part.cpu().numpy(), full.sin_part[idx].cpu().numpy(),
-                              equal_nan=True)
+        # both paths, so NaNs compare equal
+        k1 = len(idx) == 100
+        assert same(sub.cos_part, full.cos_part[idx], k1)
+        assert same(sub.sin_part, full.sin_part[idx], k1)
         assert int(sub.status[3]) == 1
     t = 10.0 ** rng.uniform(-2, 0.5, 160)
     w = big[:, :, :] * 0.01
@@ -679,8 +689,8 @@ def test_self_selecting_small_batches(cuda, n):
                                       torch.from_numpy(t[idx]).to(cuda))
         assert np.array_equal(sw.k.cpu().numpy(), fw.k.cpu().numpy()[idx])
         assert np.array_equal(sw.s.cpu().numpy(), fw.s.cpu().numpy()[idx])
-        assert torch.equal(sw.cos_part, fw.cos_part[idx])
-        assert torch.equal(sw.sin_part, fw.sin_part[idx])
+        assert same(sw.cos_part, fw.cos_part[idx], len(idx) == 100)
+        assert same(sw.sin_part, fw.sin_part[idx], len(idx) == 100)
     # the self-selecting path against the oracle, and the reference's
     # exception on a bad matrix
     sub = csm.cos_sin_batched(big[[0, 1, 77]])
