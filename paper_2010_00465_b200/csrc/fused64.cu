@@ -95,7 +95,7 @@ template <> struct Geo<4> {
 // K1s: one n <= 64 matrix over a 4-CTA cluster (16-row bands, 4 warps of
 // 16 x 16): the latency-bound small-batch path, a quarter product per SM.
 template <> struct Geo<5> {
-  static constexpr bool ROTATE = true;
+  static constexpr bool ROTATE = false;
   static constexpr int CL = 4, NP = 64, BAND = 16, THREADS = 128, MI = 2, NI = 2;
 };
 static_assert(Geo<1>::THREADS == 256 || Geo<1>::THREADS == 512, "K1: 8 or 16 warps");
@@ -278,10 +278,11 @@ __device__ __forceinline__ RView<CL> rview(const double* R, int rank) {
   } else {
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
-      // each CTA starts at its own band, so the four CTAs read four
-      // different owners at a time (K1s: 24 us per cfg1 matrix against
-      // 29 us in the natural k order, whose results are bitwise K1's; the
-      // rotated order changes the last bits only, ~3e-15 relative)
+      // K1c: each CTA starts at its own band, so the four CTAs read four
+      // different owners at a time.  K1s keeps the natural k order: its
+      // accumulation order, and so every bit of its results, is K1's, and
+      // a matrix's result does not depend on the batch size (rotated, a
+      // cfg1 matrix takes 24 us instead of 29 us, ~3e-15 apart)
       const int o = Geo<CL>::ROTATE ? (rank + i) & (NC - 1) : i;
       // own band through the local shared window: no cluster round trip
       v.p[i] = o == rank ? R
