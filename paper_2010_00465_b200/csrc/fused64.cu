@@ -285,9 +285,10 @@ __device__ __forceinline__ RView<CL> rview(const double* R, int rank) {
       // cfg1 matrix takes 24 us instead of 29 us, ~3e-15 apart)
       const int o = Geo<CL>::ROTATE ? (rank + i) & (NC - 1) : i;
       // own band through the local shared window: no cluster round trip
-      v.p[i] = o == rank ? R
-                         : static_cast<const double*>(
-                               __cluster_map_shared_rank(const_cast<double*>(R), o));
+      const bool own = Geo<CL>::ROTATE ? i == 0 : o == rank;  // compile-time when rotated
+      v.p[i] = own ? R
+                   : static_cast<const double*>(
+                         __cluster_map_shared_rank(const_cast<double*>(R), o));
       v.lcol[i] = Geo<CL>::BAND * o;  // L columns of band o (swizzle keeps 8-chunk blocks)
     }
   }
