@@ -127,6 +127,46 @@ class BatchPlan:
         self._graph.replay()
         return self.cos, self.sin, self.k, self.s, self.status
 
+    def capture_host(self, a_host, cos_host, sin_host, t_host=None):
+        """Capture host -> device -> host in ONE CUDA graph: the H2D copy of
+        the pinned input, the (graph-safe) run and the D2H copies of cos and
+        sin into the pinned outputs.  For repeated small calls (latency
+        bound, configs[0]): refill a_host, replay_host(), synchronize, read."""
+        torch = self.torch
+        if not self.graph_safe:
+            raise RuntimeError("this plan synchronises the host (tiled chain); "
+                               "it cannot be captured in a CUDA graph")
+        for x in (a_host, cos_host, sin_host) + ((t_host,) if self.wave else ()):
+            if not x.is_pinned():
+                raise ValueError("capture_host needs pinned host tensors")
+        if self._a_dev is None:
+            self._a_dev = torch.empty((self.batch, self.n, self.n), dtype=self.dtype,
+                                      device=self.device)
+            if self.wave:
+                self._t_dev = torch.empty(self.batch, dtype=torch.float64,
+                                          device=self.device)
+
+        def body():
+            self._a_dev.copy_(a_host, non_blocking=True)
+            if self.wave:
+                self._t_dev.copy_(t_host, non_blocking=True)
+            self.run(self._a_dev, self._t_dev)
+            cos_host.copy_(self.cos, non_blocking=True)
+            sin_host.copy_(self.sin, non_blocking=True)
+
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up outside the capture
+            body()
+        torch.cuda.current_stream().wait_stream(side)
+        self._host_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._host_graph):
+            body()
+
+    def replay_host(self):
+        """Replay the captured host round trip on the current stream."""
+        self._host_graph.replay()
+
     def run_host(self, a_host, cos_host, sin_host, t_host=None,
                  chunks: int = 8) -> None:
         """Host->device->host run: pinned CPU tensors in and out, chunked
