@@ -147,6 +147,28 @@ __device__ __forceinline__ double* slot_ptr(const LaunchArgs& args, int b, int s
 // The op's linear combinations for output tile (tm, tn) of matrix b, from
 // the product tile E ([BM][LDE] in shared memory): row-contiguous
 // (coalesced) global reads of the slot terms and writes of the outputs.
+#ifndef CSM_TILED_DEDUP
+#define CSM_TILED_DEDUP 1
+#endif
+
+// One final (cos / sin) pair at flat index o of the caller's n x n output.
+__device__ __forceinline__ void store_final(void* dst, int out_f32, size_t o, int c, int n,
+                                            double v0, double v1) {
+  if (out_f32) {
+    float* d = static_cast<float*>(dst);
+    if (c < n) d[o] = static_cast<float>(v0);
+    if (c + 1 < n) d[o + 1] = static_cast<float>(v1);
+  } else {
+    double* d = static_cast<double*>(dst);
+    if (c + 1 < n && ((o & 1) == 0)) {
+      *reinterpret_cast<double2*>(d + o) = make_double2(v0, v1);
+    } else {
+      if (c < n) d[o] = v0;
+      if (c + 1 < n) d[o + 1] = v1;
+    }
+  }
+}
+
 template <int NT>
 __device__ __forceinline__ void epilogue_tile(const LaunchArgs& args, const Op& op, int b,
                                               int tm, int tn, const double* E) {
@@ -166,6 +188,107 @@ __device__ __forceinline__ void epilogue_tile(const LaunchArgs& args, const Op& 
   // PB pairs per thread at a time: every slot-sourced term issues PB
   // independent loads before its FMAs, so the workspace reads (HBM for
   // large batches) overlap instead of exposing one latency per term.
+  // Distinct slot sources of the op (the heaviest epilogues read y, y2, y3
+  // and mid in up to three outputs each): loaded ONCE per pair group, all
+  // up front, then every output sums its terms in its listed order from
+  // registers -- the same FMA sequence as per-term loads, so bitwise the
+  // same results, with all the group's workspace reads in flight at once.
+  constexpr int MAXD = 6, PD = 2;  // distinct slots, pairs per thread per group
+  int dsrc[MAXD], nd = 0;
+#pragma unroll
+  for (int d = 0; d < MAXD; ++d) dsrc[d] = -1;
+  for (int q = 0; q < nout; ++q)
+    for (int tt = 0; tt < op.out[q].nterms; ++tt) {
+      const int src = op.out[q].t[tt].src;
+      if (src < 0) continue;
+      bool seen = false;
+#pragma unroll
+      for (int d = 0; d < MAXD; ++d) seen |= dsrc[d] == src;
+      if (!seen && nd < MAXD) {
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d)
+          if (d == nd) dsrc[d] = src;
+      }
+      nd += seen ? 0 : 1;
+    }
+  if (CSM_TILED_DEDUP && nd <= MAXD) {
+    static_assert((BM * BN / 2) % (PD * NT) == 0, "pair groups tile the output");
+    for (int p0 = tid; p0 < BM * BN / 2; p0 += PD * NT) {
+      size_t off[PD];
+      double2 xs[MAXD][PD];
+#pragma unroll
+      for (int m = 0; m < PD; ++m) {
+        const int p = p0 + m * NT;
+        off[m] = static_cast<size_t>(r0 + (p >> 5)) * NP + c0 + (p & 31) * 2;
+      }
+#pragma unroll
+      for (int d = 0; d < MAXD; ++d)
+        if (d < nd) {
+          const double* sp = slot(dsrc[d]);
+#pragma unroll
+          for (int m = 0; m < PD; ++m) xs[d][m] = *reinterpret_cast<const double2*>(sp + off[m]);
+        }
+      double o0[PD][2], o1[PD][2];
+      for (int q = 0; q < nout; ++q) {
+        const OutSpec& os = op.out[q];
+        double v[PD][2];
+#pragma unroll
+        for (int m = 0; m < PD; ++m) v[m][0] = v[m][1] = 0.0;
+        for (int tt = 0; tt < os.nterms; ++tt) {
+          const int src = os.t[tt].src;
+          const double cf = os.t[tt].c;
+#pragma unroll
+          for (int m = 0; m < PD; ++m) {
+            const int p = p0 + m * NT;
+            double x0 = 0.0, x1 = 0.0;
+            if (src >= 0) {
+#pragma unroll
+              for (int d = 0; d < MAXD; ++d)
+                if (dsrc[d] == src) { x0 = xs[d][m].x; x1 = xs[d][m].y; }
+            } else if (src == SRC_ACC) {
+              const double2 av = *reinterpret_cast<const double2*>(
+                  E + (p >> 5) * LDE + (p & 31) * 2);
+              x0 = av.x; x1 = av.y;
+            } else if (src == SRC_I) {
+              const int rg = r0 + (p >> 5) + args.row0, c = c0 + (p & 31) * 2;
+              x0 = (rg == c) ? 1.0 : 0.0;
+              x1 = (rg == c + 1) ? 1.0 : 0.0;
+            } else if (src == SRC_OUT0) {
+              x0 = o0[m][0]; x1 = o0[m][1];
+            } else {
+              x0 = o1[m][0]; x1 = o1[m][1];
+            }
+            v[m][0] = fma(cf, x0, v[m][0]);
+            v[m][1] = fma(cf, x1, v[m][1]);
+          }
+        }
+        if (os.scale != SC_NONE) {
+          const double sc = os.scale == SC_TP ? sc_tp : (os.scale == SC_F ? sc_f : sc_f2);
+#pragma unroll
+          for (int m = 0; m < PD; ++m) { v[m][0] *= sc; v[m][1] *= sc; }
+        }
+#pragma unroll
+        for (int m = 0; m < PD; ++m) {
+          if (q == 0) { o0[m][0] = v[m][0]; o0[m][1] = v[m][1]; }
+          if (q == 1) { o1[m][0] = v[m][0]; o1[m][1] = v[m][1]; }
+          *reinterpret_cast<double2*>(base + os.slot * slotsz + off[m]) =
+              make_double2(v[m][0], v[m][1]);
+        }
+        if (os.final != FIN_NONE && final_now) {
+          void* dst = os.final == FIN_COS ? args.cout : args.sout;
+#pragma unroll
+          for (int m = 0; m < PD; ++m) {
+            const int p = p0 + m * NT;
+            const int r = r0 + (p >> 5), c = c0 + (p & 31) * 2;
+            if (r >= n) continue;
+            store_final(dst, args.out_f32, static_cast<size_t>(b) * nn +
+                        static_cast<size_t>(r) * n + c, c, n, v[m][0], v[m][1]);
+          }
+        }
+      }
+    }
+    return;
+  }
   constexpr int PB = CSM_TILED_PB;
   static_assert((BM * BN / 2) % (PB * NT) == 0, "pair groups tile the output");
   for (int p0 = tid; p0 < BM * BN / 2; p0 += PB * NT) {
