@@ -26,41 +26,7 @@ pytestmark = pytest.mark.gpu
 TOL64 = 1e-12
 
 
-def _cfg4_parts(count=512, n=512):
-    """oracle.cpu_pool._gen('cfg4', 0, count, n) without materialising the
-    whole batch: a[i] = lap + diag(v[i]) (same draws, same order)."""
-    rng = np.random.default_rng(0)
-    lap = (np.diag(2.0 * np.ones(n)) - np.diag(np.ones(n - 1), 1)
-           - np.diag(np.ones(n - 1), -1)) * float((n + 1) ** 2)
-    v = rng.uniform(0.0, 10.0, (count, n))
-    return lap, v, 10.0 ** rng.uniform(-4.0, -1.0, count)
-
-
-def _cfg4_worker(args):
-    """Oracle side of one chunk of cfg4: per matrix (k, s, gpu-vs-oracle
-    errors, the oracle's permuted-order noise, and both distances to the
-    eigendecomposition answer)."""
-    lo, hi, c_path, s_path, seed = args
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    import numpy as np
-
-    from oracle import cossin_oracle as orc
-    from tests._util import permuted_noise, rel1
-    lap, v_all, t_all = _cfg4_parts()
-    cg = np.load(c_path, mmap_mode="r")
-    sg = np.load(s_path, mmap_mode="r")
-    rng = np.random.default_rng(seed)
-    out = []
-    for i in range(lo, hi):
-        a, t = lap + np.diag(v_all[i]), float(t_all[i])
-        (c, s, k, sc), noise = permuted_noise(lambda x: orc.wave_cos_sin(x, t), a, rng)
-        lam, v = np.linalg.eigh(a)
-        w = np.sqrt(lam)
-        ce = (v * np.cos(t * w)) @ v.T
-        se = (v * (np.sin(t * w) / w)) @ v.T
-        out.append((i, k, sc, rel1(cg[i], c), rel1(sg[i], s), noise,
-                    rel1(cg[i], ce), rel1(c, ce), rel1(sg[i], se), rel1(s, se)))
-    return out
+from tests._fullsize_worker import cfg4_parts as _cfg4_parts, cfg4_worker as _cfg4_worker  # noqa: E402
 
 
 @pytest.mark.timeout(1500)
@@ -83,17 +49,24 @@ def test_full_cfg4_against_oracle(cuda, tmp_path):
     bounds = np.linspace(0, 512, 4 * workers + 1).astype(int)
     jobs = [(int(lo), int(hi), c_path, s_path, 7 + j)
             for j, (lo, hi) in enumerate(zip(bounds[:-1], bounds[1:]))]
+    # spawned workers inherit the environment at exec time: one BLAS thread
+    # each (set before numpy loads in them), and the repo on their path
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    old = os.environ.get("PYTHONPATH")
-    os.environ["PYTHONPATH"] = root + (os.pathsep + old if old else "")
+    keys = ("PYTHONPATH", "OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS")
+    saved = {k: os.environ.get(k) for k in keys}
+    os.environ["PYTHONPATH"] = root + (os.pathsep + saved["PYTHONPATH"]
+                                       if saved["PYTHONPATH"] else "")
+    for k in keys[1:]:
+        os.environ[k] = "1"
     try:
         with mp.get_context("spawn").Pool(workers) as pool:
             rows = [r for part in pool.map(_cfg4_worker, jobs) for r in part]
     finally:
-        if old is None:
-            os.environ.pop("PYTHONPATH", None)
-        else:
-            os.environ["PYTHONPATH"] = old
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     assert len(rows) == 512
     worst = 0.0
     for (i, k, sc, ec, es, noise, gce, oce, gse, ose) in rows:
