@@ -46,6 +46,9 @@ void set_engine(int e);
 void set_thread_engine(int e);
 int engine();
 int k1c_resident_sms();
+cudaError_t launch_fused64d(int dtype, const void* a, void* c, void* s, const int32_t* k,
+                            const int32_t* sx, const int32_t* st, const int32_t* order,
+                            int64_t batch, int n, cudaStream_t stream);
 size_t op_bytes();
 int chain_program(bool wave, int k, bool fold, void* ops_out, int max_ops, int32_t* step_nops,
                   int max_steps, int32_t* cos_slot, int32_t* sin_slot);
@@ -193,6 +196,17 @@ int fused_max() {
   return v;
 }
 
+// K1d (two CTAs per SM, fused64d.cu) runs the Taylor family at n <= 64;
+// CSM_K1D=0 (environment) keeps those batches on K1, for A/B measurements
+// and the bitwise cross-check test.
+bool k1d_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CSM_K1D");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Matrices of a 64 < n <= 128 batch given to the side tiled chain.
 int64_t side_count(int64_t batch) {
   static const double share = [] {
@@ -245,7 +259,10 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
     e = csm::launch_schedule(K, S, st, bf, w.bins, w.order, stream, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "schedule kernels");
     csm::prof_begin(stream);
-    e = csm::launch_fused64(dtype, wave, a, c, s, t, K, S, st, w.order, bf, n, stream);
+    if (!wave && n <= 64 && k1d_enabled())
+      e = csm::launch_fused64d(dtype, a, c, s, K, S, st, w.order, bf, n, stream);
+    else
+      e = csm::launch_fused64(dtype, wave, a, c, s, t, K, S, st, w.order, bf, n, stream);
     if (e != cudaSuccess) return cuda_fail(e, "fused64 launch");
     ++g_launches;
     if (bf < batch) {

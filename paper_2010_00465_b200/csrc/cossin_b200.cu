@@ -2,6 +2,7 @@
 // __constant__ tables shared by every kernel (no relocatable device code).
 #include "k0_select.cu"
 #include "fused64.cu"
+#include "fused64d.cu"
 #include "tiled.cu"
 #include "distchain.cu"
 #include "ddref.cu"
