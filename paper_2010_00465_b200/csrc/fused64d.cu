@@ -173,7 +173,8 @@ __device__ __forceinline__ void car_set(Car& c, int j, int e, double v) {
 
 template <typename TOut>
 struct DArgs {
-  double* o[3];   // shared-memory outputs (nullptr: not written)
+  double* sm;     // the CTA's slots
+  int o[3];       // shared-memory outputs as slot offsets in doubles (-1: not written)
   TOut* g;        // global destination of this step's final output (s == 0), or nullptr
   double scale;
   int n;
@@ -199,7 +200,7 @@ constexpr uint32_t kCarCols = 64;  // columns per carrier (8 warps: 2 per lane q
 
 template <typename TOut>
 __device__ __forceinline__ void dput(const DArgs<TOut>& E, int q, int off, double v0, double v1) {
-  if (E.o[q]) st2(E.o[q], off, v0, v1);
+  if (E.o[q] >= 0) st2(E.sm, E.o[q] + off, v0, v1);
 }
 
 template <typename TOut>
@@ -545,8 +546,10 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tm = sh_tmem + (static_cast<uint32_t>(32 * ((tid >> 5) & 3)) << 16) +
                       static_cast<uint32_t>(32 * (tid >> 7));
-  double* sl[3] = {smem, smem + SLOT, smem + 2 * SLOT};  // logical -> physical
-  fetch(sh_b[0], sl[0]);
+  // logical slot -> offset (in doubles) of its physical slot; pointers are
+  // formed as smem + offset at each use so that they stay shared-space
+  int so[3] = {0, SLOT, 2 * SLOT};
+  fetch(sh_b[0], smem + so[0]);
 
   Acc acc, unused;
   for (int it = 0;; ++it) {
@@ -567,7 +570,7 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
       cp_async_commit();
     }
     if (!is_fast) {
-      dload_sync(sl[0], Ain + static_cast<size_t>(b) * nn, n);
+      dload_sync(smem + so[0], Ain + static_cast<size_t>(b) * nn, n);
       __syncthreads();
     }
     TOut* cdst = Cout + static_cast<size_t>(b) * nn;
@@ -575,7 +578,7 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
     if (status != 0) {
       store_nan<256>(cdst, n, 0, 64);
       store_nan<256>(sdst, n, 0, 64);
-      fetch(bn, sl[0]);  // the unused input's slot takes the next one
+      fetch(bn, smem + so[0]);  // the unused input's slot takes the next one
       continue;
     }
     const double f = ldexp(1.0, -s);  // driver.py:115, a * 2**-s (folded into the products)
@@ -591,20 +594,21 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
         cp_async_wait_all();
         __syncthreads();
       }
-      gemm<7, false>(sl[st.l], nullptr, rview<7>(sl[st.r], 0), acc, unused, ln);
+      gemm<7, false>(smem + so[st.l], nullptr, rview<7>(smem + so[st.r], 0), acc, unused, ln);
       if (st.two_phase) __syncthreads();  // every warp has read the operands
       if (st.reload >= 0) {
         if (is_fast) {
-          fetch(b, sl[st.reload]);
+          fetch(b, smem + so[st.reload]);
         } else {
-          dload_sync(sl[st.reload], Ain + static_cast<size_t>(b) * nn, n);
+          dload_sync(smem + so[st.reload], Ain + static_cast<size_t>(b) * nn, n);
         }
       }
-      if (i == pf_step) fetch(bn, sl[2]);
+      if (i == pf_step) fetch(bn, smem + so[2]);
       DArgs<TOut> E;
-      E.o[0] = sl[st.o0 < 0 ? 0 : st.o0];
-      E.o[1] = st.o1 >= 0 ? sl[st.o1] : nullptr;
-      E.o[2] = st.o2 >= 0 ? sl[st.o2] : nullptr;
+      E.sm = smem;
+      E.o[0] = so[st.o0];
+      E.o[1] = st.o1 >= 0 ? so[st.o1] : -1;
+      E.o[2] = st.o2 >= 0 ? so[st.o2] : -1;
       E.g = nullptr;
       E.scale = 1.0;
       E.n = n;
@@ -612,11 +616,11 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
       const bool makes_cos = st.epi == D_DEG2 || st.epi == D_DEG4B || st.epi == D_DEG8C ||
                              st.epi == D_DEG12D;
       if (makes_cos) {
-        if (!cos_smem) E.o[0] = nullptr;
+        if (!cos_smem) E.o[0] = -1;
         if (s == 0) E.g = cdst;
       } else if (st.epi == D_SIN) {
         E.scale = f;
-        if (s == 0) { E.o[0] = nullptr; E.g = sdst; }
+        if (s == 0) { E.o[0] = -1; E.g = sdst; }
       } else if (st.epi == D_Y) {
         E.scale = f * f;
       }
@@ -624,27 +628,25 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
       __syncthreads();
     }
     // Doubling (driver.py:91-98): C = slot 2, S = slot 1, slot 0 free.
-    double *C = sl[2], *S = sl[1], *F = sl[0];
+    int C = so[2], S = so[1], F = so[0];
     for (int d = 0; d < s; ++d) {
       const bool last = d == s - 1;
-      if (last) fetch(bn, F);  // nothing is written to shared memory any more
-      gemm<7, false>(S, nullptr, rview<7>(C, 0), acc, unused, ln);
-      ddouble_out<TOut>(acc, false, F, last ? sdst : nullptr, n, ln);
-      gemm<7, false>(C, nullptr, rview<7>(C, 0), acc, unused, ln);
+      if (last) fetch(bn, smem + F);  // nothing is written to shared memory any more
+      gemm<7, false>(smem + S, nullptr, rview<7>(smem + C, 0), acc, unused, ln);
+      ddouble_out<TOut>(acc, false, smem + F, last ? sdst : nullptr, n, ln);
+      gemm<7, false>(smem + C, nullptr, rview<7>(smem + C, 0), acc, unused, ln);
       if (!last) __syncthreads();  // S and C have been read by every warp
-      ddouble_out<TOut>(acc, true, S, last ? cdst : nullptr, n, ln);
+      ddouble_out<TOut>(acc, true, smem + S, last ? cdst : nullptr, n, ln);
       if (!last) {
         __syncthreads();
-        double* t = S; S = F; F = C; C = t;  // S' in F, C' in the old S, the old C is free
+        const int t = S; S = F; F = C; C = t;  // S' in F, C' in the old S, the old C is free
       }
     }
     // the next input is arriving in: logical slot 2 (s == 0), or F (after doubling)
-    double* nxt = s == 0 ? sl[2] : F;
-    int q = 1;
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-      if (smem + j * SLOT != nxt) sl[q++] = smem + j * SLOT;
-    sl[0] = nxt;
+    const int nxt = s == 0 ? so[2] : F;
+    so[0] = nxt;
+    so[1] = nxt == 0 ? SLOT : 0;
+    so[2] = nxt == 2 * SLOT ? SLOT : 2 * SLOT;
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
