@@ -48,7 +48,7 @@ int engine();
 int k1c_resident_sms();
 cudaError_t launch_fused64d(int dtype, const void* a, void* c, void* s, const int32_t* k,
                             const int32_t* sx, const int32_t* st, const int32_t* order,
-                            int64_t batch, int n, cudaStream_t stream);
+                            int64_t batch, int n, unsigned* ticket, cudaStream_t stream);
 size_t op_bytes();
 int chain_program(bool wave, int k, bool fold, void* ops_out, int max_ops, int32_t* step_nops,
                   int max_steps, int32_t* cos_slot, int32_t* sin_slot);
@@ -260,7 +260,9 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
     if (e != cudaSuccess) return cuda_fail(e, "schedule kernels");
     csm::prof_begin(stream);
     if (!wave && n <= 64 && k1d_enabled())
-      e = csm::launch_fused64d(dtype, a, c, s, K, S, st, w.order, bf, n, stream);
+      // the schedule's histogram scratch is free again: its first word is the work counter
+      e = csm::launch_fused64d(dtype, a, c, s, K, S, st, w.order, bf, n,
+                               reinterpret_cast<unsigned*>(w.bins), stream);
     else
       e = csm::launch_fused64(dtype, wave, a, c, s, t, K, S, st, w.order, bf, n, stream);
     if (e != cudaSuccess) return cuda_fail(e, "fused64 launch");
@@ -381,6 +383,9 @@ __global__ void dmma_peak_kernel(double* out, int iters) {
 }  // namespace
 
 extern "C" {
+#ifdef CSM_TRACE
+int csm_trace_k1d_ctas(unsigned long long* out);
+#endif
 
 const char* csm_version(void) { return "cossin_b200 0.1.0 (sm_100a, FP64 DMMA)"; }
 
@@ -549,6 +554,10 @@ int csm_theta_table(int family, int precision, double* theta_cos, double* theta_
 }
 
 #ifdef CSM_TRACE
+int csm_trace_k1d_ctas(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, csm::f64k::g_k1d_cta, sizeof(unsigned long long) * 1024 * 4);
+  return 0;
+}
 int csm_trace_dump(unsigned long long* out, int cap) {
   int n = 0;
   cudaMemcpyFromSymbol(&n, csm::f64k::g_trace_n, sizeof(int));

@@ -171,12 +171,41 @@ __device__ __forceinline__ void car_set(Car& c, int j, int e, double v) {
   c.w[4 * j + 2 * e + 1] = static_cast<uint32_t>(__double2hiint(v));
 }
 
+// Power-of-two scalings without the FP64 pipe.  The two CTAs of an SM share
+// it: while one runs a product, every DMUL / DFMA of the other's epilogue
+// queues behind DMMAs (measured: a 16-DMUL epilogue took 3.5 k cycles under
+// the other CTA's product).  x * 2^-m and 2 x are exponent arithmetic
+// whenever x and the result are normal numbers -- bit for bit the product's
+// value; zeros, subnormals, infinities and NaNs take the multiply.
+// The caller tests the whole accumulator set once (exp_range_ok) and
+// branches between an all-integer and an all-multiply epilogue, so the fast
+// path really contains no FP64 instruction (a per-element select would be
+// if-converted into multiply + select).
+__device__ __forceinline__ bool exp_range_ok(const Acc& acc, int m) {
+  // every element: m < biased exponent < 0x7fe (normal, and normal after the
+  // shift by -m or +1)
+  bool ok = true;
+#pragma unroll
+  for (int P = 0; P < 8; ++P)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int ex = (__double2hiint(acc[P][e]) >> 20) & 0x7ff;
+      ok = ok && ex > m && ex < 0x7fe;
+    }
+  // warp-uniform: the TMEM stores inside the branches are .sync.aligned
+  return __all_sync(0xffffffffu, ok);
+}
+__device__ __forceinline__ double exp_add(double x, int d) {  // x * 2^d by exponent arithmetic
+  return __hiloint2double(__double2hiint(x) + d * (1 << 20), __double2loint(x));
+}
+
 template <typename TOut>
 struct DArgs {
   double* sm;     // the CTA's slots
   int o[3];       // shared-memory outputs as slot offsets in doubles (-1: not written)
   TOut* g;        // global destination of this step's final output (s == 0), or nullptr
-  double scale;
+  double scale;   // 2^-shift
+  int shift;
   int n;
   uint32_t tm;    // this thread's TMEM base (lane quarter, warp column half)
 };
@@ -214,25 +243,48 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
                  T3 = E.tm + 3 * kCarCols;
   switch (epi) {
     case D_Y:
-      D_CHUNKS({
-        Car cy;
-        D_TILES({
-          const double v0 = E.scale * p0, v1 = E.scale * p1;
-          dput(E, 0, off, v0, v1);
-          car_set(cy, j, 0, v0);
-          car_set(cy, j, 1, v1);
+      if (exp_range_ok(acc, E.shift)) {
+        D_CHUNKS({
+          Car cy;
+          D_TILES({
+            const double v0 = exp_add(p0, -E.shift), v1 = exp_add(p1, -E.shift);
+            dput(E, 0, off, v0, v1);
+            car_set(cy, j, 0, v0);
+            car_set(cy, j, 1, v1);
+          })
+          tm_st8(T0 + 8 * h, cy);
         })
-        tm_st8(T0 + 8 * h, cy);
-      })
+      } else {
+        D_CHUNKS({
+          Car cy;
+          D_TILES({
+            const double v0 = E.scale * p0, v1 = E.scale * p1;
+            dput(E, 0, off, v0, v1);
+            car_set(cy, j, 0, v0);
+            car_set(cy, j, 1, v1);
+          })
+          tm_st8(T0 + 8 * h, cy);
+        })
+      }
       break;
     case D_SIN:
-      D_CHUNKS({
-        D_TILES({
-          const double v0 = E.scale * p0, v1 = E.scale * p1;
-          dput(E, 0, off, v0, v1);
-          if (E.g) gstore<64>(E.g, E.n, r, c, v0, v1);
+      if (exp_range_ok(acc, E.shift)) {
+        D_CHUNKS({
+          D_TILES({
+            const double v0 = exp_add(p0, -E.shift), v1 = exp_add(p1, -E.shift);
+            dput(E, 0, off, v0, v1);
+            if (E.g) gstore<64>(E.g, E.n, r, c, v0, v1);
+          })
         })
-      })
+      } else {
+        D_CHUNKS({
+          D_TILES({
+            const double v0 = E.scale * p0, v1 = E.scale * p1;
+            dput(E, 0, off, v0, v1);
+            if (E.g) gstore<64>(E.g, E.n, r, c, v0, v1);
+          })
+        })
+      }
       break;
     case D_Y2:
       D_CHUNKS({
@@ -445,18 +497,32 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
   tm_wait_st();
 }
 
-// Doubling epilogues (driver.py:95-97): S' = 2 acc, or C' = 2 acc - I.
+// Doubling epilogues (driver.py:95-97): S' = 2 acc, or C' = 2 acc - I.  Off
+// the diagonal fma(2, p, -0.0) = 2 p (signed zeros included), so only the
+// diagonal elements need the FP64 pipe.
 template <typename TOut>
 __device__ __forceinline__ void ddouble_out(const Acc& acc, bool is_cos, double* dst, TOut* gdst,
                                             int n, const Lane<7>& ln) {
-  D_CHUNKS({
-    D_TILES({
-      const double v0 = is_cos ? fma(2.0, p0, -I0) : 2.0 * p0;
-      const double v1 = is_cos ? fma(2.0, p1, -I1) : 2.0 * p1;
-      if (gdst) gstore<64>(gdst, n, r, c, v0, v1);
-      else st2(dst, off, v0, v1);
+  if (exp_range_ok(acc, 0)) {
+    D_CHUNKS({
+      D_TILES({
+        double v0 = exp_add(p0, 1), v1 = exp_add(p1, 1);
+        if (is_cos && r == c) v0 = fma(2.0, p0, -1.0);
+        if (is_cos && r == c + 1) v1 = fma(2.0, p1, -1.0);
+        if (gdst) gstore<64>(gdst, n, r, c, v0, v1);
+        else st2(dst, off, v0, v1);
+      })
     })
-  })
+  } else {
+    D_CHUNKS({
+      D_TILES({
+        const double v0 = is_cos ? fma(2.0, p0, -I0) : 2.0 * p0;
+        const double v1 = is_cos ? fma(2.0, p1, -I1) : 2.0 * p1;
+        if (gdst) gstore<64>(gdst, n, r, c, v0, v1);
+        else st2(dst, off, v0, v1);
+      })
+    })
+  }
 }
 #undef D_TILES
 #undef D_CHUNKS
@@ -484,27 +550,29 @@ __device__ __forceinline__ void dload_sync(double* slot, const TIn* src, int n) 
   }
 }
 
-__device__ unsigned g_k1d_arrivals[1024];  // CTAs seen per SM (parity = arrival order)
+#ifdef CSM_TRACE
+__device__ unsigned long long g_k1d_cta[1024][4];  // per CTA: smid, start ns, end ns, matrices
+#endif
 
 template <typename TIn, typename TOut>
 __global__ void __launch_bounds__(256, 2)
 fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __restrict__ Sout,
                 const int32_t* __restrict__ K, const int32_t* __restrict__ Sx,
                 const int32_t* __restrict__ ST, const int32_t* __restrict__ order,
-                int64_t batch, int n, int fast, int delay) {
+                int64_t batch, int n, int fast, unsigned* __restrict__ ticket) {
   extern __shared__ __align__(128) double smem[];
   __shared__ int sh_b[4];
   __shared__ int sh_meta[2][4];
   __shared__ uint32_t sh_tmem;
   __shared__ DChain sh_chain[4];
   const int tid = threadIdx.x;
-  const int G = gridDim.x, cta = blockIdx.x;
+#ifdef CSM_TRACE
+  unsigned long long cta_t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(cta_t0));
+#endif
   Lane<7> ln;
   make_lane(ln, 0);
   const size_t nn = static_cast<size_t>(n) * n;
-  auto posof = [&](int i) -> long long {
-    return static_cast<long long>(i) * G + ((i & 1) ? (G - 1 - cta) : cta);
-  };
   // FAST (fp64, n == 64, aligned): asynchronous input, one matrix ahead
   const bool is_fast = sizeof(TIn) == 8 && fast != 0;
   auto fetch = [&](int b, double* slot) {  // all threads
@@ -520,25 +588,22 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
                      smem_u32(&sh_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
+  // Work distribution: order[] lists the matrices by descending cost; every
+  // CTA draws the next position from one global ticket counter (zeroed by
+  // the launcher).  The two CTAs of an SM do not get equal shares of the
+  // FP64 pipe, so a static split leaves one of them running alone at the
+  // end (measured: 15% of the kernel); tickets end them within a few cheap
+  // matrices of each other.  Thread 0 draws three turns ahead, so the
+  // atomic's latency is never waited for.
+  unsigned pend = 0;  // thread 0: the ticket of turn it + 2
   if (tid == 0) {
-    const long long p0 = posof(0), p1 = posof(1);
-    const int b0 = p0 < batch ? order[p0] : -1;
+    const unsigned t0 = atomicAdd(ticket, 1u), t1 = atomicAdd(ticket, 1u);
+    pend = atomicAdd(ticket, 1u);
+    const int b0 = t0 < batch ? order[t0] : -1;
     sh_b[0] = b0;
-    sh_b[1] = p1 < batch ? order[p1] : -1;
+    sh_b[1] = t1 < batch ? order[t1] : -1;
     if (b0 >= 0) {
       sh_meta[0][0] = K[b0]; sh_meta[0][1] = Sx[b0]; sh_meta[0][2] = ST[b0];
-    }
-    // The two CTAs of an SM start together on matrices of equal cost (the
-    // schedule is cost-sorted) and would run their products and their
-    // epilogues in lockstep; the second one to arrive starts `delay` cycles
-    // late so that its epilogues fall under the first one's products.
-    if (delay > 0) {
-      unsigned smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      if (atomicAdd(&g_k1d_arrivals[smid & 1023], 1u) & 1u) {
-        const long long t0 = clock64();
-        while (clock64() - t0 < delay) { }
-      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -551,15 +616,20 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
   int so[3] = {0, SLOT, 2 * SLOT};
   fetch(sh_b[0], smem + so[0]);
 
+#ifdef CSM_TRACE
+  if (tid == CSM_TRACE_TID) trace_count() = 0;
+#endif
   Acc acc, unused;
   for (int it = 0;; ++it) {
+    TRACE_T(14);
     cp_async_wait_all();
     __syncthreads();
     const int b = sh_b[it & 3], bn = sh_b[(it + 1) & 3];
     if (b < 0) break;
     const int k = sh_meta[it & 1][0], s = sh_meta[it & 1][1], status = sh_meta[it & 1][2];
     if (tid == 0) {  // stage ids and metadata for the coming turns
-      const long long p2 = posof(it + 2);
+      const unsigned p2 = pend;
+      pend = atomicAdd(ticket, 1u);
       if (p2 < batch) cp_async4(&sh_b[(it + 2) & 3], order + p2);
       else sh_b[(it + 2) & 3] = -1;
       if (bn >= 0) {
@@ -581,6 +651,8 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
       fetch(bn, smem + so[0]);  // the unused input's slot takes the next one
       continue;
     }
+    TRACE_T(1);
+    CSM_TRACE_EV(9, static_cast<unsigned long long>(k * 16 + s));
     const double f = ldexp(1.0, -s);  // driver.py:115, a * 2**-s (folded into the products)
     const DChain& ch = sh_chain[k == 3 ? 0 : (k == 4 ? 1 : (k == 6 ? 2 : 3))];
     const int nsteps = ch.nsteps;
@@ -594,8 +666,11 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
         cp_async_wait_all();
         __syncthreads();
       }
+      TRACE_T(2);
       gemm<7, false>(smem + so[st.l], nullptr, rview<7>(smem + so[st.r], 0), acc, unused, ln);
+      TRACE_T(3);
       if (st.two_phase) __syncthreads();  // every warp has read the operands
+      TRACE_T(8);
       if (st.reload >= 0) {
         if (is_fast) {
           fetch(b, smem + so[st.reload]);
@@ -611,6 +686,7 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
       E.o[2] = st.o2 >= 0 ? so[st.o2] : -1;
       E.g = nullptr;
       E.scale = 1.0;
+      E.shift = 0;
       E.n = n;
       E.tm = tm;
       const bool makes_cos = st.epi == D_DEG2 || st.epi == D_DEG4B || st.epi == D_DEG8C ||
@@ -620,23 +696,42 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
         if (s == 0) E.g = cdst;
       } else if (st.epi == D_SIN) {
         E.scale = f;
+        E.shift = s;
         if (s == 0) { E.o[0] = -1; E.g = sdst; }
       } else if (st.epi == D_Y) {
         E.scale = f * f;
+        E.shift = 2 * s;
       }
       depilogue(st.epi, E, acc, ln);
+      TRACE_T(4);
       __syncthreads();
+      TRACE_T(5);
     }
     // Doubling (driver.py:91-98): C = slot 2, S = slot 1, slot 0 free.
     int C = so[2], S = so[1], F = so[0];
     for (int d = 0; d < s; ++d) {
       const bool last = d == s - 1;
       if (last) fetch(bn, smem + F);  // nothing is written to shared memory any more
+      TRACE_T(6);
       gemm<7, false>(smem + S, nullptr, rview<7>(smem + C, 0), acc, unused, ln);
+      TRACE_T(10);
+#ifdef CSM_TRACE
+      {  // the accumulators' arrival (integer consumer: no FP64 instruction)
+        int sink = 0;
+#pragma unroll
+        for (int P = 0; P < 8; ++P) sink ^= __double2hiint(acc[P][0]) ^ __double2hiint(acc[P][1]);
+        if (sink == 0x12345678) sh_b[3] = 1;
+      }
+      TRACE_T(15);
+#endif
       ddouble_out<TOut>(acc, false, smem + F, last ? sdst : nullptr, n, ln);
+      TRACE_T(11);
       gemm<7, false>(smem + C, nullptr, rview<7>(smem + C, 0), acc, unused, ln);
+      TRACE_T(12);
       if (!last) __syncthreads();  // S and C have been read by every warp
+      TRACE_T(13);
       ddouble_out<TOut>(acc, true, smem + S, last ? cdst : nullptr, n, ln);
+      TRACE_T(7);
       if (!last) {
         __syncthreads();
         const int t = S; S = F; F = C; C = t;  // S' in F, C' in the old S, the old C is free
@@ -648,6 +743,17 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
     so[1] = nxt == 0 ? SLOT : 0;
     so[2] = nxt == 2 * SLOT ? SLOT : 2 * SLOT;
   }
+#ifdef CSM_TRACE
+  if (tid == 0 && blockIdx.x < 1024) {
+    unsigned smid;
+    unsigned long long t1;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    g_k1d_cta[blockIdx.x][0] = smid;
+    g_k1d_cta[blockIdx.x][1] = cta_t0;
+    g_k1d_cta[blockIdx.x][2] = t1;
+  }
+#endif
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
   if ((tid >> 5) == 0)
@@ -661,7 +767,7 @@ size_t fused64d_smem_bytes() { return 3 * static_cast<size_t>(f64k::SLOT) * size
 template <typename TIn, typename TOut>
 static cudaError_t launch_k1d(const void* a, void* c, void* s, const int32_t* k, const int32_t* sx,
                               const int32_t* st, const int32_t* order, int64_t batch, int n,
-                              cudaStream_t stream) {
+                              unsigned* ticket, cudaStream_t stream) {
   auto kern = f64k::fused64d_kernel<TIn, TOut>;
   const size_t smem = fused64d_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -670,10 +776,6 @@ static cudaError_t launch_k1d(const void* a, void* c, void* s, const int32_t* k,
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
-  static const int env_delay = [] {
-    const char* v = std::getenv("CSM_K1D_DELAY");
-    return v ? std::atoi(v) : 4000;
-  }();
   static const int env_occ = [] {
     const char* v = std::getenv("CSM_K1D_OCC");
     return v ? std::atoi(v) : 2;
@@ -707,20 +809,25 @@ static cudaError_t launch_k1d(const void* a, void* c, void* s, const int32_t* k,
   if (grid > batch) grid = batch;
   if (grid < 1) return cudaSuccess;
   const int fast = (sizeof(TIn) == 8 && n == 64 && reinterpret_cast<uintptr_t>(a) % 16 == 0) ? 1 : 0;
+  e = cudaMemsetAsync(ticket, 0, sizeof(unsigned), stream);
+  if (e != cudaSuccess) return e;
   kern<<<static_cast<unsigned>(grid), 256, smem_launch, stream>>>(
       static_cast<const TIn*>(a), static_cast<TOut*>(c), static_cast<TOut*>(s), k, sx, st, order,
-      batch, n, fast, per_sm == 2 ? env_delay : 0);
+      batch, n, fast, ticket);
   return cudaGetLastError();
 }
 
-// K1d: Taylor family, n <= 64, (k, s, status) and order[] on the device.
+// K1d: Taylor family, n <= 64, (k, s, status) and order[] on the device;
+// ticket: one device word of scratch (the work counter, zeroed here).
 cudaError_t launch_fused64d(int dtype, const void* a, void* c, void* s, const int32_t* k,
                             const int32_t* sx, const int32_t* st, const int32_t* order,
-                            int64_t batch, int n, cudaStream_t stream) {
-  if (n < 1 || n > 64) return cudaErrorInvalidValue;
-  if (dtype == 0) return launch_k1d<double, double>(a, c, s, k, sx, st, order, batch, n, stream);
-  if (dtype == 2) return launch_k1d<float, double>(a, c, s, k, sx, st, order, batch, n, stream);
-  return launch_k1d<float, float>(a, c, s, k, sx, st, order, batch, n, stream);
+                            int64_t batch, int n, unsigned* ticket, cudaStream_t stream) {
+  if (n < 1 || n > 64 || !ticket) return cudaErrorInvalidValue;
+  if (dtype == 0)
+    return launch_k1d<double, double>(a, c, s, k, sx, st, order, batch, n, ticket, stream);
+  if (dtype == 2)
+    return launch_k1d<float, double>(a, c, s, k, sx, st, order, batch, n, ticket, stream);
+  return launch_k1d<float, float>(a, c, s, k, sx, st, order, batch, n, ticket, stream);
 }
 
 }  // namespace csm
