@@ -705,7 +705,9 @@ def run_ours(args, cfg):
                      "unit": "TFLOP/s",
                      "frac": (achieved / peak) if (achieved and peak) else None,
                      "traffic": traffic,
-                     "kernel": ("fused64_kernel (K1)" if n <= 64 else
+                     "kernel": (("fused64d_kernel (K1d, two CTAs per SM)"
+                                 if kind != "cfg4" and os.environ.get("CSM_K1D", "1") != "0"
+                                 and batch > 148 else "fused64_kernel (K1)") if n <= 64 else
                                 "fused64_kernel<4> (K1c, 4-CTA clusters) + side tiled chain, "
                                 "timed as one interval" if n <= 128 else
                                 "gemm_epi_kernel (tiled chain)"),

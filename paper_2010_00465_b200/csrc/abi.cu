@@ -199,12 +199,12 @@ int fused_max() {
 // K1d (two CTAs per SM, fused64d.cu) runs the Taylor family at n <= 64;
 // CSM_K1D=0 (environment) keeps those batches on K1, for A/B measurements
 // and the bitwise cross-check test.
-bool k1d_enabled() {
-  static const bool on = [] {
+int k1_variant() {
+  static const int v = [] {
     const char* e = std::getenv("CSM_K1D");
-    return !(e && e[0] == '0');
+    return (e && e[0] == '0') ? 0 : 1;
   }();
-  return on;
+  return v;
 }
 
 // Matrices of a 64 < n <= 128 batch given to the side tiled chain.
@@ -259,8 +259,8 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
     e = csm::launch_schedule(K, S, st, bf, w.bins, w.order, stream, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "schedule kernels");
     csm::prof_begin(stream);
-    if (!wave && n <= 64 && k1d_enabled())
-      // the schedule's histogram scratch is free again: its first word is the work counter
+    // (the schedule's histogram scratch is free again: its first word is the work counter)
+    if (!wave && n <= 64 && k1_variant() == 1)
       e = csm::launch_fused64d(dtype, a, c, s, K, S, st, w.order, bf, n,
                                reinterpret_cast<unsigned*>(w.bins), stream);
     else

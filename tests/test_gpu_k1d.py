@@ -26,9 +26,14 @@ def _run(tmp_path, k1d):
 
 
 @pytest.fixture(scope="module")
-def both(tmp_path_factory, cuda):
-    d = tmp_path_factory.mktemp("k1d")
-    return _run(d, 1), _run(d, 0)
+def k1_outputs(tmp_path_factory, cuda):
+    return _run(tmp_path_factory.mktemp("k1"), 0)
+
+
+@pytest.fixture(scope="module")
+def both(tmp_path_factory, k1_outputs):
+    """(outputs of K1d, outputs of K1) on the same seeded batches."""
+    return _run(tmp_path_factory.mktemp("k1d"), 1), k1_outputs
 
 
 def test_k1d_bitwise_equals_k1(both):
