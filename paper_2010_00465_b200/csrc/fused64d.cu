@@ -653,7 +653,11 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
     }
     TRACE_T(1);
     CSM_TRACE_EV(9, static_cast<unsigned long long>(k * 16 + s));
-    const double f = ldexp(1.0, -s);  // driver.py:115, a * 2**-s (folded into the products)
+    // driver.py:115, a * 2**-s (folded into the products).  Built from the
+    // exponent: an FP64 instruction here would queue behind the other CTA's
+    // DMMAs like the epilogues' do
+    const double f = s <= 1022 ? __hiloint2double((1023 - s) << 20, 0) : ldexp(1.0, -s);
+    const double ff = s <= 511 ? __hiloint2double((1023 - 2 * s) << 20, 0) : f * f;
     const DChain& ch = sh_chain[k == 3 ? 0 : (k == 4 ? 1 : (k == 6 ? 2 : 3))];
     const int nsteps = ch.nsteps;
     const int pf_step = s == 0 ? ch.pf_step : -1, wait_step = ch.wait_step;
@@ -699,12 +703,14 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
         E.shift = s;
         if (s == 0) { E.o[0] = -1; E.g = sdst; }
       } else if (st.epi == D_Y) {
-        E.scale = f * f;
+        E.scale = ff;
         E.shift = 2 * s;
       }
       depilogue(st.epi, E, acc, ln);
       TRACE_T(4);
-      __syncthreads();
+      // (the last step of an s = 0 chain writes only global memory, and the
+      // barrier at the top of the next turn follows)
+      if (!(s == 0 && i == nsteps - 1)) __syncthreads();
       TRACE_T(5);
     }
     // Doubling (driver.py:91-98): C = slot 2, S = slot 1, slot 0 free.

@@ -25,6 +25,20 @@ def cases():
     out["n63"] = cfg2_like(rng, 333, n=63)
     out["f32_64"] = cfg2_like(rng, 600, n=64).astype(np.float32)
     out["f32_20"] = cfg2_like(rng, 600, n=20).astype(np.float32)
+    # the scaling epilogues' multiply paths and the 2**-s fallbacks: products
+    # that underflow to subnormals / zero (tiny norms), s in the hundreds and
+    # beyond 1022 (huge norms: intermediate overflow to inf / NaN, as the
+    # reference's own arithmetic gives), and batches mixing both
+    tiny = cfg2_like(rng, 200, n=64, lo=-200.0, hi=-150.0)
+    huge = cfg2_like(rng, 200, n=64, lo=100.0, hi=307.0)
+    out["subnormal_64"] = tiny
+    out["huge_64"] = huge
+    mixed = np.concatenate([tiny[:60], huge[:60], cfg2_like(rng, 80, n=64)])
+    out["mixed_extreme_64"] = mixed[rng.permutation(mixed.shape[0])]
+    out["huge_n30"] = cfg2_like(rng, 160, n=30, lo=200.0, hi=300.0)
+    # batch sizes around the persistent grid (296 CTAs, two per SM)
+    for count in (149, 295, 296, 297, 593):
+        out[f"edge_{count}"] = cfg2_like(rng, count, n=64)
     bad = cfg2_like(rng, 500, n=64)
     bad[7, 3, 4] = np.nan
     bad[123, 0, 0] = np.inf
