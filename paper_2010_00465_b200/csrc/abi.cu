@@ -46,9 +46,10 @@ void set_engine(int e);
 void set_thread_engine(int e);
 int engine();
 int k1c_resident_sms();
-cudaError_t launch_fused64d(int dtype, const void* a, void* c, void* s, const int32_t* k,
-                            const int32_t* sx, const int32_t* st, const int32_t* order,
-                            int64_t batch, int n, unsigned* ticket, cudaStream_t stream);
+cudaError_t launch_fused64d(int dtype, bool wave, const void* a, void* c, void* s, const double* t,
+                            const int32_t* k, const int32_t* sx, const int32_t* st,
+                            const int32_t* order, int64_t batch, int n, unsigned* ticket,
+                            cudaStream_t stream);
 size_t op_bytes();
 int chain_program(bool wave, int k, bool fold, void* ops_out, int max_ops, int32_t* step_nops,
                   int max_steps, int32_t* cos_slot, int32_t* sin_slot);
@@ -196,7 +197,7 @@ int fused_max() {
   return v;
 }
 
-// K1d (two CTAs per SM, fused64d.cu) runs the Taylor family at n <= 64;
+// K1d (two CTAs per SM, fused64d.cu) runs n <= 64 (both families);
 // CSM_K1D=0 (environment) keeps those batches on K1, for A/B measurements
 // and the bitwise cross-check test.
 int k1_variant() {
@@ -260,8 +261,8 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
     if (e != cudaSuccess) return cuda_fail(e, "schedule kernels");
     csm::prof_begin(stream);
     // (the schedule's histogram scratch is free again: its first word is the work counter)
-    if (!wave && n <= 64 && k1_variant() == 1)
-      e = csm::launch_fused64d(dtype, a, c, s, K, S, st, w.order, bf, n,
+    if (n <= 64 && k1_variant() == 1)
+      e = csm::launch_fused64d(dtype, wave, a, c, s, t, K, S, st, w.order, bf, n,
                                reinterpret_cast<unsigned*>(w.bins), stream);
     else
       e = csm::launch_fused64(dtype, wave, a, c, s, t, K, S, st, w.order, bf, n, stream);

@@ -65,6 +65,14 @@ enum DEpi : int8_t {
   D_DEG12D,  // o0 = cos ; o1 = inner ; T0 = sine base              (y, y2, y3, mid)
   D_KEEP12,  // o0 = T0 + acc
   D_SIN,     // o0 = sin = scale * acc
+  // wave family (y is the scaled input itself, read from its slot once)
+  D_W1,      // o0 = y2 = acc (T1) ; o1 = -y/720 + acc/40320 ; o2 = -y/5040 + acc/9! ; T0 = y
+  D_W2C,     // o0 = cos = I - y/2 + y2/24 + acc
+  D_W2S,     // o0 = s = scale * (I - y/6 + y2/120 + acc)
+  D_W8A,     // D_DEG8A with y from its slot ; T0 = y
+  D_WY2,     // D_Y2 with T0 = y copied from its slot
+  D_KEEPW8,  // o0 = scale * (T3 + acc)
+  D_KEEPW12, // o0 = scale * (T0 + acc)
 };
 
 struct __align__(8) DStep {
@@ -87,7 +95,7 @@ static_assert(sizeof(DChain) == 64, "chain table layout");
 
 // Every chain ends with cos in slot 2, sin in slot 1 and slot 0 free.
 #define DS_(l, r, e, o0, o1, o2, tp, rl) {l, r, e, o0, o1, o2, tp, rl}
-__constant__ DChain kDChains[4] = {
+__constant__ DChain kDChains[7] = {
     // [0] Taylor k=3: chain_deg2 (schemes.py:264-272)
     {3, 1, -1, {0, 0, 0, 0, 0},
      {DS_(0, 0, D_Y, 1, X, X, 0, X),        // y = A A
@@ -116,6 +124,25 @@ __constant__ DChain kDChains[4] = {
       DS_(2, 1, D_DEG12D, 2, 1, X, 1, X),   // cos (over L), inner (over mid)
       DS_(1, 2, D_KEEP12, 1, X, X, 1, X),   // sc (over inner)
       DS_(0, 1, D_SIN, 1, X, X, 1, X)}},
+    // [4] wave k=3: chain_deg4(exact_sine=True) on y = (t')^2 A (schemes.py:426-427);
+    // K1's dual product [L; L9] y2 runs as two products
+    {3, 1, -1, {0, 0, 0, 0, 0},
+     {DS_(0, 0, D_W1, 1, 2, 0, 1, X),       // y2, L, L9 (over y)
+      DS_(2, 1, D_W2C, 2, X, X, 1, X),      // cos = ... + L y2 (over L)
+      DS_(0, 1, D_W2S, 1, X, X, 1, X)}},    // s = t' (... + L9 y2) (over y2)
+    // [5] wave k=4: chain_deg8 on y
+    {4, 2, -1, {0, 0, 0, 0, 0},
+     {DS_(0, 0, D_W8A, 1, 2, X, 0, X),      // y2, L
+      DS_(1, 2, D_DEG8B, 0, 1, 2, 1, X),    // p8 (over y), L2 (over y2), R2 (over L)
+      DS_(1, 2, D_DEG8C, 2, 1, X, 1, X),    // cos (over R2), inner (over L2)
+      DS_(1, 0, D_KEEPW8, 1, X, X, 1, X)}}, // s (over inner)
+    // [6] wave k=5: chain_deg12 on y
+    {5, 4, -1, {0, 0, 0, 0, 0},
+     {DS_(0, 0, D_WY2, 1, X, X, 0, X),      // y2
+      DS_(1, 0, D_DEG12B, 2, X, X, 0, X),   // c4; y3 stays in TMEM
+      DS_(2, 2, D_DEG12C, 0, 1, X, 0, X),   // mid (over y), L (over y2)
+      DS_(1, 0, D_DEG12D, 2, 1, X, 1, X),   // cos (over c4), inner (over L)
+      DS_(1, 2, D_KEEPW12, 1, X, X, 1, X)}},// s (over inner)
 };
 #undef DS_
 
@@ -204,8 +231,9 @@ struct DArgs {
   double* sm;     // the CTA's slots
   int o[3];       // shared-memory outputs as slot offsets in doubles (-1: not written)
   TOut* g;        // global destination of this step's final output (s == 0), or nullptr
-  double scale;   // 2^-shift
+  double scale;   // 2^-shift (Taylor), t' (wave)
   int shift;
+  int yin;        // wave: slot offset of y for the epilogues that read it from shared memory
   int n;
   uint32_t tm;    // this thread's TMEM base (lane quarter, warp column half)
 };
@@ -232,9 +260,15 @@ __device__ __forceinline__ void dput(const DArgs<TOut>& E, int q, int off, doubl
   if (E.o[q] >= 0) st2(E.sm, E.o[q] + off, v0, v1);
 }
 
-template <typename TOut>
+template <bool WAVE, typename TOut>
 __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const Acc& acc,
                                           const Lane<7>& ln) {
+  // (each family's kernel compiles only its own cases: the Taylor kernel sits
+  // at the register cap, and more code in this switch makes it spill)
+  if (WAVE ? (epi == D_Y || epi == D_DEG2 || epi == D_DEG4A || epi == D_DEG4B || epi == D_DEG8A ||
+              epi == D_Y2 || epi == D_KEEP8 || epi == D_KEEP12 || epi == D_SIN)
+           : epi >= D_W1)
+    return;
   const double* x = dTables.x8;  // x[0] = x1
   const double* z8 = dTables.z8;
   const double(*a)[4] = dTables.a12;  // a[j-1][i]
@@ -243,6 +277,7 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
                  T3 = E.tm + 3 * kCarCols;
   switch (epi) {
     case D_Y:
+      if constexpr (!WAVE) {
       if (exp_range_ok(acc, E.shift)) {
         D_CHUNKS({
           Car cy;
@@ -265,9 +300,11 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
           })
           tm_st8(T0 + 8 * h, cy);
         })
+      }
       }
       break;
     case D_SIN:
+      if constexpr (!WAVE) {
       if (exp_range_ok(acc, E.shift)) {
         D_CHUNKS({
           D_TILES({
@@ -285,8 +322,10 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
           })
         })
       }
+      }
       break;
     case D_Y2:
+      if constexpr (!WAVE) {
       D_CHUNKS({
         Car cy2;
         D_TILES({
@@ -296,8 +335,10 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
         })
         tm_st8(T1 + 8 * h, cy2);
       })
+      }
       break;
     case D_DEG2:
+      if constexpr (!WAVE) {
       D_CHUNKS({
         Car cy;
         tm_ld8(T0 + 8 * h, cy);
@@ -312,8 +353,10 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
                fma(1.0 / 120.0, p1, fma(-1.0 / 6.0, y1, I1)));
         })
       })
+      }
       break;
     case D_DEG4A:
+      if constexpr (!WAVE) {
       D_CHUNKS({
         Car cy, cy2;
         tm_ld8(T0 + 8 * h, cy);
@@ -328,8 +371,10 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
         })
         tm_st8(T1 + 8 * h, cy2);
       })
+      }
       break;
     case D_DEG4B:
+      if constexpr (!WAVE) {
       D_CHUNKS({
         Car cy, cy2;
         tm_ld8(T0 + 8 * h, cy);
@@ -347,8 +392,10 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
                fma(720.0 / 5040.0, p1, fma(1.0 / 120.0, q1, fma(-1.0 / 6.0, y1, I1))));
         })
       })
+      }
       break;
     case D_DEG8A:
+      if constexpr (!WAVE) {
       D_CHUNKS({
         Car cy, cy2;
         tm_ld8(T0 + 8 * h, cy);
@@ -362,6 +409,7 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
         })
         tm_st8(T1 + 8 * h, cy2);
       })
+      }
       break;
     case D_DEG8B:
       D_CHUNKS({
@@ -411,6 +459,7 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
       break;
     case D_KEEP8:
     case D_KEEP12: {
+      if constexpr (!WAVE) {
       const uint32_t TK = epi == D_KEEP8 ? T3 : T0;
       D_CHUNKS({
         Car ck;
@@ -420,6 +469,7 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
           dput(E, 0, off, car_get(ck, j, 0) + p0, car_get(ck, j, 1) + p1);
         })
       })
+      }
       break;
     }
     case D_DEG12B:
@@ -491,6 +541,107 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
         tm_st8(T0 + 8 * h, ck);  // the sine base takes y's place
       })
       break;
+    case D_W1:
+      if constexpr (WAVE) {
+      D_CHUNKS({
+        Car cy, cy2;
+        D_TILES({
+          const double2 y = ld2(E.sm, E.yin + off);
+          car_set(cy, j, 0, y.x);
+          car_set(cy, j, 1, y.y);
+          car_set(cy2, j, 0, p0);
+          car_set(cy2, j, 1, p1);
+          const double l0 = fma(1.0 / 40320.0, p0, (-1.0 / 720.0) * y.x);
+          const double l1 = fma(1.0 / 40320.0, p1, (-1.0 / 720.0) * y.y);
+          const double m0 = fma(1.0 / 362880.0, p0, (-1.0 / 5040.0) * y.x);
+          const double m1 = fma(1.0 / 362880.0, p1, (-1.0 / 5040.0) * y.y);
+          dput(E, 0, off, p0, p1);
+          dput(E, 1, off, l0, l1);
+          dput(E, 2, off, m0, m1);  // over y, at this thread's own pair
+        })
+        tm_st8(T0 + 8 * h, cy);
+        tm_st8(T1 + 8 * h, cy2);
+      })
+      }
+      break;
+    case D_W2C:
+    case D_W2S:
+      if constexpr (WAVE) {
+      D_CHUNKS({
+        Car cy, cy2;
+        tm_ld8(T0 + 8 * h, cy);
+        tm_ld8(T1 + 8 * h, cy2);
+        tm_wait_ld(cy, cy2);
+        D_TILES({
+          const double y0 = car_get(cy, j, 0), y1 = car_get(cy, j, 1);
+          const double q0 = car_get(cy2, j, 0), q1 = car_get(cy2, j, 1);
+          double v0, v1;
+          if (epi == D_W2C) {
+            v0 = p0 + fma(1.0 / 24.0, q0, fma(-0.5, y0, I0));
+            v1 = p1 + fma(1.0 / 24.0, q1, fma(-0.5, y1, I1));
+          } else {
+            v0 = E.scale * (p0 + fma(1.0 / 120.0, q0, fma(-1.0 / 6.0, y0, I0)));
+            v1 = E.scale * (p1 + fma(1.0 / 120.0, q1, fma(-1.0 / 6.0, y1, I1)));
+          }
+          dput(E, 0, off, v0, v1);
+          if (E.g) gstore<64>(E.g, E.n, r, c, v0, v1);
+        })
+      })
+      }
+      break;
+    case D_W8A:
+      if constexpr (WAVE) {
+      D_CHUNKS({
+        Car cy, cy2;
+        D_TILES({
+          const double2 y = ld2(E.sm, E.yin + off);
+          car_set(cy, j, 0, y.x);
+          car_set(cy, j, 1, y.y);
+          dput(E, 0, off, p0, p1);
+          car_set(cy2, j, 0, p0);
+          car_set(cy2, j, 1, p1);
+          dput(E, 1, off, fma(x[1], p0, x[0] * y.x), fma(x[1], p1, x[0] * y.y));
+        })
+        tm_st8(T0 + 8 * h, cy);
+        tm_st8(T1 + 8 * h, cy2);
+      })
+      }
+      break;
+    case D_WY2:
+      if constexpr (WAVE) {
+      D_CHUNKS({
+        Car cy, cy2;
+        D_TILES({
+          const double2 y = ld2(E.sm, E.yin + off);
+          car_set(cy, j, 0, y.x);
+          car_set(cy, j, 1, y.y);
+          dput(E, 0, off, p0, p1);
+          car_set(cy2, j, 0, p0);
+          car_set(cy2, j, 1, p1);
+        })
+        tm_st8(T0 + 8 * h, cy);
+        tm_st8(T1 + 8 * h, cy2);
+      })
+      }
+      break;
+    case D_KEEPW8:
+    case D_KEEPW12: {
+      if constexpr (WAVE) {
+      const uint32_t TK = epi == D_KEEPW8 ? T3 : T0;
+      D_CHUNKS({
+        Car ck;
+        tm_ld8(TK + 8 * h, ck);
+        tm_wait_ld(ck);
+        D_TILES({
+          const double v0 = E.scale * (car_get(ck, j, 0) + p0);
+          const double v1 = E.scale * (car_get(ck, j, 1) + p1);
+          dput(E, 0, off, v0, v1);
+          if (E.g) gstore<64>(E.g, E.n, r, c, v0, v1);
+        })
+      })
+      }
+      break;
+    }
     default:
       break;
   }
@@ -536,8 +687,9 @@ __device__ __forceinline__ void dload_async(double* slot, const double* src) {
     cp_async16(slot + r * 64 + 2 * (pi ^ swz_f(r)), src + 2 * q);
   }
 }
-template <typename TIn>
-__device__ __forceinline__ void dload_sync(double* slot, const TIn* src, int n) {
+template <bool SCALE, typename TIn>
+__device__ __forceinline__ void dload_sync(double* slot, const TIn* src, int n,
+                                           double g = 1.0) {
 #pragma unroll 2
   for (int p = threadIdx.x; p < 2048; p += 256) {
     const int r = p >> 5, c = (p & 31) * 2;
@@ -546,7 +698,8 @@ __device__ __forceinline__ void dload_sync(double* slot, const TIn* src, int n) 
       if (c < n) v0 = static_cast<double>(src[r * n + c]);
       if (c + 1 < n) v1 = static_cast<double>(src[r * n + c + 1]);
     }
-    st2(slot, swz<64>(r, c), v0, v1);
+    if (SCALE) st2(slot, swz<64>(r, c), g * v0, g * v1);  // wave: y = (t')^2 A, schemes.py:424
+    else st2(slot, swz<64>(r, c), v0, v1);
   }
 }
 
@@ -554,17 +707,19 @@ __device__ __forceinline__ void dload_sync(double* slot, const TIn* src, int n) 
 __device__ unsigned long long g_k1d_cta[1024][4];  // per CTA: smid, start ns, end ns, matrices
 #endif
 
-template <typename TIn, typename TOut>
+template <typename TIn, typename TOut, bool WAVE>
 __global__ void __launch_bounds__(256, 2)
 fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __restrict__ Sout,
-                const int32_t* __restrict__ K, const int32_t* __restrict__ Sx,
+                const double* __restrict__ T, const int32_t* __restrict__ K,
+                const int32_t* __restrict__ Sx,
                 const int32_t* __restrict__ ST, const int32_t* __restrict__ order,
                 int64_t batch, int n, int fast, unsigned* __restrict__ ticket) {
   extern __shared__ __align__(128) double smem[];
   __shared__ int sh_b[4];
   __shared__ int sh_meta[2][4];
+  __shared__ double sh_t[2];
   __shared__ uint32_t sh_tmem;
-  __shared__ DChain sh_chain[4];
+  __shared__ DChain sh_chain[7];
   const int tid = threadIdx.x;
 #ifdef CSM_TRACE
   unsigned long long cta_t0;
@@ -573,8 +728,10 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
   Lane<7> ln;
   make_lane(ln, 0);
   const size_t nn = static_cast<size_t>(n) * n;
-  // FAST (fp64, n == 64, aligned): asynchronous input, one matrix ahead
-  const bool is_fast = sizeof(TIn) == 8 && fast != 0;
+  // FAST (Taylor, fp64, n == 64, aligned): asynchronous input, one matrix
+  // ahead.  The wave family scales its input by (t')^2 on the way in, so it
+  // loads at the top of the matrix's turn like the other slow cases.
+  const bool is_fast = !WAVE && sizeof(TIn) == 8 && fast != 0;
   auto fetch = [&](int b, double* slot) {  // all threads
     if (is_fast && b >= 0)
       dload_async(slot, reinterpret_cast<const double*>(Ain) + static_cast<size_t>(b) * nn);
@@ -604,6 +761,7 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
     sh_b[1] = t1 < batch ? order[t1] : -1;
     if (b0 >= 0) {
       sh_meta[0][0] = K[b0]; sh_meta[0][1] = Sx[b0]; sh_meta[0][2] = ST[b0];
+      if (WAVE) sh_t[0] = T[b0];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -636,11 +794,15 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
         cp_async4(&sh_meta[(it + 1) & 1][0], K + bn);
         cp_async4(&sh_meta[(it + 1) & 1][1], Sx + bn);
         cp_async4(&sh_meta[(it + 1) & 1][2], ST + bn);
+        if (WAVE) cp_async8v(&sh_t[(it + 1) & 1], T + bn);
       }
       cp_async_commit();
     }
-    if (!is_fast) {
-      dload_sync(smem + so[0], Ain + static_cast<size_t>(b) * nn, n);
+    // wave: t' = t / 2**s (driver.py:139), y = (t' t') a (schemes.py:424)
+    double tp = 0.0;
+    if (WAVE) tp = sh_t[it & 1] / ldexp(1.0, s);
+    if (!is_fast && status == 0) {
+      dload_sync<WAVE>(smem + so[0], Ain + static_cast<size_t>(b) * nn, n, tp * tp);
       __syncthreads();
     }
     TOut* cdst = Cout + static_cast<size_t>(b) * nn;
@@ -658,12 +820,13 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
     // DMMAs like the epilogues' do
     const double f = s <= 1022 ? __hiloint2double((1023 - s) << 20, 0) : ldexp(1.0, -s);
     const double ff = s <= 511 ? __hiloint2double((1023 - 2 * s) << 20, 0) : f * f;
-    const DChain& ch = sh_chain[k == 3 ? 0 : (k == 4 ? 1 : (k == 6 ? 2 : 3))];
+    const DChain& ch = sh_chain[WAVE ? (k == 3 ? 4 : (k == 4 ? 5 : 6))
+                                     : (k == 3 ? 0 : (k == 4 ? 1 : (k == 6 ? 2 : 3)))];
     const int nsteps = ch.nsteps;
     const int pf_step = s == 0 ? ch.pf_step : -1, wait_step = ch.wait_step;
     // cos must reach shared memory when it is a later operand: doubling, or
-    // the degree-12 chain's inner * cos
-    const bool cos_smem = s != 0 || k == 7;
+    // the degree-12 chains' inner * cos
+    const bool cos_smem = s != 0 || k == (WAVE ? 5 : 7);
     for (int i = 0; i < nsteps; ++i) {
       const DStep st = ch.step[i];
       if (i == wait_step) {  // the reloaded A
@@ -679,7 +842,7 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
         if (is_fast) {
           fetch(b, smem + so[st.reload]);
         } else {
-          dload_sync(smem + so[st.reload], Ain + static_cast<size_t>(b) * nn, n);
+          dload_sync<false>(smem + so[st.reload], Ain + static_cast<size_t>(b) * nn, n);
         }
       }
       if (i == pf_step) fetch(bn, smem + so[2]);
@@ -691,10 +854,11 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
       E.g = nullptr;
       E.scale = 1.0;
       E.shift = 0;
+      E.yin = so[0];  // (wave: y is the input itself, logical slot 0)
       E.n = n;
       E.tm = tm;
       const bool makes_cos = st.epi == D_DEG2 || st.epi == D_DEG4B || st.epi == D_DEG8C ||
-                             st.epi == D_DEG12D;
+                             st.epi == D_DEG12D || st.epi == D_W2C;
       if (makes_cos) {
         if (!cos_smem) E.o[0] = -1;
         if (s == 0) E.g = cdst;
@@ -702,11 +866,14 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
         E.scale = f;
         E.shift = s;
         if (s == 0) { E.o[0] = -1; E.g = sdst; }
+      } else if (st.epi == D_W2S || st.epi == D_KEEPW8 || st.epi == D_KEEPW12) {
+        E.scale = tp;  // s(t', y) = t' (...), schemes.py:429
+        if (s == 0) { E.o[0] = -1; E.g = sdst; }
       } else if (st.epi == D_Y) {
         E.scale = ff;
         E.shift = 2 * s;
       }
-      depilogue(st.epi, E, acc, ln);
+      depilogue<WAVE>(st.epi, E, acc, ln);
       TRACE_T(4);
       // (the last step of an s = 0 chain writes only global memory, and the
       // barrier at the top of the next turn follows)
@@ -770,11 +937,11 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
 
 size_t fused64d_smem_bytes() { return 3 * static_cast<size_t>(f64k::SLOT) * sizeof(double); }
 
-template <typename TIn, typename TOut>
-static cudaError_t launch_k1d(const void* a, void* c, void* s, const int32_t* k, const int32_t* sx,
-                              const int32_t* st, const int32_t* order, int64_t batch, int n,
-                              unsigned* ticket, cudaStream_t stream) {
-  auto kern = f64k::fused64d_kernel<TIn, TOut>;
+template <typename TIn, typename TOut, bool WAVE>
+static cudaError_t launch_k1d(const void* a, void* c, void* s, const double* t, const int32_t* k,
+                              const int32_t* sx, const int32_t* st, const int32_t* order,
+                              int64_t batch, int n, unsigned* ticket, cudaStream_t stream) {
+  auto kern = f64k::fused64d_kernel<TIn, TOut, WAVE>;
   const size_t smem = fused64d_smem_bytes();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -818,22 +985,26 @@ static cudaError_t launch_k1d(const void* a, void* c, void* s, const int32_t* k,
   e = cudaMemsetAsync(ticket, 0, sizeof(unsigned), stream);
   if (e != cudaSuccess) return e;
   kern<<<static_cast<unsigned>(grid), 256, smem_launch, stream>>>(
-      static_cast<const TIn*>(a), static_cast<TOut*>(c), static_cast<TOut*>(s), k, sx, st, order,
+      static_cast<const TIn*>(a), static_cast<TOut*>(c), static_cast<TOut*>(s), t, k, sx, st, order,
       batch, n, fast, ticket);
   return cudaGetLastError();
 }
 
-// K1d: Taylor family, n <= 64, (k, s, status) and order[] on the device;
-// ticket: one device word of scratch (the work counter, zeroed here).
-cudaError_t launch_fused64d(int dtype, const void* a, void* c, void* s, const int32_t* k,
-                            const int32_t* sx, const int32_t* st, const int32_t* order,
-                            int64_t batch, int n, unsigned* ticket, cudaStream_t stream) {
-  if (n < 1 || n > 64 || !ticket) return cudaErrorInvalidValue;
-  if (dtype == 0)
-    return launch_k1d<double, double>(a, c, s, k, sx, st, order, batch, n, ticket, stream);
-  if (dtype == 2)
-    return launch_k1d<float, double>(a, c, s, k, sx, st, order, batch, n, ticket, stream);
-  return launch_k1d<float, float>(a, c, s, k, sx, st, order, batch, n, ticket, stream);
+// K1d: n <= 64, (k, s, status) and order[] on the device; t: the wave
+// family's times (nullptr: Taylor cos/sin); ticket: one device word of
+// scratch (the work counter, zeroed here).
+cudaError_t launch_fused64d(int dtype, bool wave, const void* a, void* c, void* s, const double* t,
+                            const int32_t* k, const int32_t* sx, const int32_t* st,
+                            const int32_t* order, int64_t batch, int n, unsigned* ticket,
+                            cudaStream_t stream) {
+  if (n < 1 || n > 64 || !ticket || (wave && !t)) return cudaErrorInvalidValue;
+#define K1D_GO(TI, TO)                                                                          \
+  (wave ? launch_k1d<TI, TO, true>(a, c, s, t, k, sx, st, order, batch, n, ticket, stream)      \
+        : launch_k1d<TI, TO, false>(a, c, s, t, k, sx, st, order, batch, n, ticket, stream))
+  if (dtype == 0) return K1D_GO(double, double);
+  if (dtype == 2) return K1D_GO(float, double);
+  return K1D_GO(float, float);
+#undef K1D_GO
 }
 
 }  // namespace csm

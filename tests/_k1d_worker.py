@@ -47,9 +47,36 @@ def cases():
     return out
 
 
+def wave_cases():
+    """name -> (batch, t): the wave family (driver.py:126-146) on K1d."""
+    from tests._util import cfg2_like, laplacian_wave
+    rng = np.random.default_rng(20251)
+    out = {}
+    out["wave_lap_64"] = laplacian_wave(rng, 900, 64)        # every k, s = 0..6
+    out["wave_lap_48"] = laplacian_wave(rng, 500, 48)
+    a = cfg2_like(rng, 700, n=64, lo=-2.0, hi=3.0)
+    out["wave_gauss_64"] = (a, 10.0 ** rng.uniform(-2.0, 0.5, 700))
+    a = cfg2_like(rng, 400, n=21, lo=-1.0, hi=2.0)
+    out["wave_gauss_21"] = (a, 10.0 ** rng.uniform(-3.0, 1.0, 400))
+    a32, t32 = laplacian_wave(rng, 300, 64)
+    out["wave_f32_64"] = (a32.astype(np.float32), t32)
+    bad, tb = laplacian_wave(rng, 200, 64)
+    bad[3, 5, 5] = np.nan
+    bad[199, 0, 63] = np.inf
+    out["wave_nonfinite_64"] = (bad, tb)
+    return out
+
+
 def main(path):
     import paper_2010_00465_b200 as csm
     res = {}
+    for name, (a, t) in wave_cases().items():
+        r = csm.wave_cos_sin_batched(a, t, raise_on_error=False)
+        res[name + "/c"] = np.asarray(r.cos_part)
+        res[name + "/s"] = np.asarray(r.sin_part)
+        res[name + "/k"] = np.asarray(r.k)
+        res[name + "/sx"] = np.asarray(r.s)
+        res[name + "/st"] = np.asarray(r.status)
     for name, a in cases().items():
         r = csm.cos_sin_batched(a, raise_on_error=False)
         res[name + "/c"] = np.asarray(r.cos_part)

@@ -64,6 +64,25 @@ def test_k1d_covers_every_chain_and_deep_scaling(both):
     assert (new["huge_64/st"] == 0).sum() > 150  # (a few inputs overflow to inf: rejected)
 
 
+def test_k1d_wave_family(both):
+    """The wave chains on K1d: every k, scaling, and against the oracle."""
+    from oracle import cossin_oracle as orc
+    new, _ = both
+    assert set(np.unique(new["wave_lap_64/k"])) == {3, 4, 5}
+    assert new["wave_lap_64/sx"].max() >= 3 and new["wave_lap_64/sx"].min() == 0
+    st = new["wave_nonfinite_64/st"]
+    assert st[3] == 1 and st[199] == 1 and st.sum() == 2
+    cases = _k1d_worker.wave_cases()
+    rng = np.random.default_rng(6)
+    for name, tol in (("wave_lap_64", 1e-12), ("wave_gauss_21", 1e-12), ("wave_f32_64", 1e-5)):
+        a, t = cases[name]
+        for i in rng.choice(a.shape[0], 16, replace=False):
+            c, s, k, sc = orc.wave_cos_sin(a[i].astype(np.float64), float(t[i]))
+            assert (k, sc) == (int(new[name + "/k"][i]), int(new[name + "/sx"][i])), (name, i)
+            assert rel1(new[name + "/c"][i], c) <= tol, (name, i, k, sc)
+            assert rel1(new[name + "/s"][i], s) <= tol, (name, i, k, sc)
+
+
 def test_k1d_against_oracle(both):
     from oracle import cossin_oracle as orc
     new, _ = both
