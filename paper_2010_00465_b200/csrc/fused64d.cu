@@ -728,10 +728,9 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
   Lane<7> ln;
   make_lane(ln, 0);
   const size_t nn = static_cast<size_t>(n) * n;
-  // FAST (Taylor, fp64, n == 64, aligned): asynchronous input, one matrix
-  // ahead.  The wave family scales its input by (t')^2 on the way in, so it
-  // loads at the top of the matrix's turn like the other slow cases.
-  const bool is_fast = !WAVE && sizeof(TIn) == 8 && fast != 0;
+  // FAST (fp64, n == 64, aligned): asynchronous input, one matrix ahead.  The
+  // wave family then scales it in place, y = (t')^2 A, at the top of its turn.
+  const bool is_fast = sizeof(TIn) == 8 && fast != 0;
   auto fetch = [&](int b, double* slot) {  // all threads
     if (is_fast && b >= 0)
       dload_async(slot, reinterpret_cast<const double*>(Ain) + static_cast<size_t>(b) * nn);
@@ -803,6 +802,17 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
     if (WAVE) tp = sh_t[it & 1] / ldexp(1.0, s);
     if (!is_fast && status == 0) {
       dload_sync<WAVE>(smem + so[0], Ain + static_cast<size_t>(b) * nn, n, tp * tp);
+      __syncthreads();
+    } else if (WAVE && status == 0) {  // each thread scales the chunks it fetched
+      const double g = tp * tp;
+      double* slot = smem + so[0];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int q = tid + 256 * i, r = q >> 5, pi = q & 31;
+        const int off = r * 64 + 2 * (pi ^ swz_f(r));
+        const double2 v = ld2(slot, off);
+        st2(slot, off, g * v.x, g * v.y);
+      }
       __syncthreads();
     }
     TOut* cdst = Cout + static_cast<size_t>(b) * nn;
