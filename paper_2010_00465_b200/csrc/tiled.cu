@@ -147,8 +147,12 @@ __device__ __forceinline__ double* slot_ptr(const LaunchArgs& args, int b, int s
 // The op's linear combinations for output tile (tm, tn) of matrix b, from
 // the product tile E ([BM][LDE] in shared memory): row-contiguous
 // (coalesced) global reads of the slot terms and writes of the outputs.
+// CSM_TILED_DEDUP=1 builds the variant below that loads each distinct slot
+// term once per pair group; measured 3-7% SLOWER than the per-term loads
+// (cfg3 0.780 vs 0.834 of the DMMA peak, n = 512 0.876 vs 0.907; profiles/r2/s4/):
+// the register-resident copies cost occupancy of the loads in flight.  Off.
 #ifndef CSM_TILED_DEDUP
-#define CSM_TILED_DEDUP 1
+#define CSM_TILED_DEDUP 0
 #endif
 
 // One final (cos / sin) pair at flat index o of the caller's n x n output.
