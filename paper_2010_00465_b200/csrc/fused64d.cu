@@ -269,6 +269,9 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
               epi == D_Y2 || epi == D_KEEP8 || epi == D_KEEP12 || epi == D_SIN)
            : epi >= D_W1)
     return;
+  // this thread's TMEM stores of the previous epilogue (they completed under
+  // the product in between; the wait orders them before the reads below)
+  tm_wait_st();
   const double* x = dTables.x8;  // x[0] = x1
   const double* z8 = dTables.z8;
   const double(*a)[4] = dTables.a12;  // a[j-1][i]
@@ -645,7 +648,6 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
     default:
       break;
   }
-  tm_wait_st();
 }
 
 // Doubling epilogues (driver.py:95-97): S' = 2 acc, or C' = 2 acc - I.  Off
@@ -937,6 +939,7 @@ fused64d_kernel(const TIn* __restrict__ Ain, TOut* __restrict__ Cout, TOut* __re
     g_k1d_cta[blockIdx.x][2] = t1;
   }
 #endif
+  tm_wait_st();
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
   if ((tid >> 5) == 0)
