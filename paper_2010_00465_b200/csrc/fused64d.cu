@@ -255,6 +255,16 @@ constexpr uint32_t kCarCols = 64;  // columns per carrier (8 warps: 2 per lane q
   }
 #define D_CHUNKS(...) _Pragma("unroll") for (int h = 0; h < 4; ++h) { __VA_ARGS__ }
 
+// coef * I_rc.  SEL: without a multiply per element -- the coefficient on the
+// diagonal, coef * 0.0 (a signed zero, computed once per epilogue) elsewhere:
+// the product's value exactly, and one FP64 instruction less per term to
+// wait out the other CTA's DMMAs.  Used by the wave kernel (1.778 -> 1.767
+// ms); in the Taylor kernel, at the register cap, it spills (2.161 -> 2.177).
+template <bool SEL>
+__device__ __forceinline__ double idt(double coef, bool on) {
+  return SEL ? (on ? coef : coef * 0.0) : coef * (on ? 1.0 : 0.0);
+}
+
 template <typename TOut>
 __device__ __forceinline__ void dput(const DArgs<TOut>& E, int q, int off, double v0, double v1) {
   if (E.o[q] >= 0) st2(E.sm, E.o[q] + off, v0, v1);
@@ -427,8 +437,8 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
           car_set(cp8, j, 0, p0);
           car_set(cp8, j, 1, p1);
           dput(E, 1, off, fma(x[2], q0, p0), fma(x[2], q1, p1));
-          dput(E, 2, off, fma(x[6], p0, fma(x[5], q0, fma(x[4], y0, x[3] * I0))),
-               fma(x[6], p1, fma(x[5], q1, fma(x[4], y1, x[3] * I1))));
+          dput(E, 2, off, fma(x[6], p0, fma(x[5], q0, fma(x[4], y0, idt<WAVE>(x[3], r == c)))),
+               fma(x[6], p1, fma(x[5], q1, fma(x[4], y1, idt<WAVE>(x[3], r == c + 1)))));
         })
         tm_st8(T2 + 8 * h, cp8);
       })
@@ -448,11 +458,11 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
           const double c0 = p0 + fma(x[7], q0, fma(-0.5, y0, I0));
           const double c1 = p1 + fma(x[7], q1, fma(-0.5, y1, I1));
           // inner = z5 I + z5 y + z6 y2 + z7 p8 + z8 cos
-          const double n0 = fma(z8[8], c0, fma(z8[7], e0, fma(z8[6], q0, fma(z8[5], y0, z8[5] * I0))));
-          const double n1 = fma(z8[8], c1, fma(z8[7], e1, fma(z8[6], q1, fma(z8[5], y1, z8[5] * I1))));
+          const double n0 = fma(z8[8], c0, fma(z8[7], e0, fma(z8[6], q0, fma(z8[5], y0, idt<WAVE>(z8[5], r == c)))));
+          const double n1 = fma(z8[8], c1, fma(z8[7], e1, fma(z8[6], q1, fma(z8[5], y1, idt<WAVE>(z8[5], r == c + 1)))));
           // sin base = z0 I + z1 y + z2 y2 + z3 p8 + z4 cos
-          car_set(ck, j, 0, fma(z8[4], c0, fma(z8[3], e0, fma(z8[2], q0, fma(z8[1], y0, z8[0] * I0)))));
-          car_set(ck, j, 1, fma(z8[4], c1, fma(z8[3], e1, fma(z8[2], q1, fma(z8[1], y1, z8[0] * I1)))));
+          car_set(ck, j, 0, fma(z8[4], c0, fma(z8[3], e0, fma(z8[2], q0, fma(z8[1], y0, idt<WAVE>(z8[0], r == c))))));
+          car_set(ck, j, 1, fma(z8[4], c1, fma(z8[3], e1, fma(z8[2], q1, fma(z8[1], y1, idt<WAVE>(z8[0], r == c + 1))))));
           dput(E, 0, off, c0, c1);
           if (E.g) gstore<64>(E.g, E.n, r, c, c0, c1);
           dput(E, 1, off, n0, n1);
@@ -486,8 +496,8 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
           const double q0 = car_get(cy2, j, 0), q1 = car_get(cy2, j, 1);
           car_set(cy3, j, 0, p0);
           car_set(cy3, j, 1, p1);
-          dput(E, 0, off, fma(a[3][3], p0, fma(a[3][2], q0, fma(a[3][1], y0, a[3][0] * I0))),
-               fma(a[3][3], p1, fma(a[3][2], q1, fma(a[3][1], y1, a[3][0] * I1))));
+          dput(E, 0, off, fma(a[3][3], p0, fma(a[3][2], q0, fma(a[3][1], y0, idt<WAVE>(a[3][0], r == c)))),
+               fma(a[3][3], p1, fma(a[3][2], q1, fma(a[3][1], y1, idt<WAVE>(a[3][0], r == c + 1)))));
         })
         tm_st8(T2 + 8 * h, cy3);
       })
@@ -504,10 +514,10 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
           const double y0 = car_get(cy, j, 0), y1 = car_get(cy, j, 1);
           const double q0 = car_get(cy2, j, 0), q1 = car_get(cy2, j, 1);
           const double u0 = car_get(cy3, j, 0), u1 = car_get(cy3, j, 1);
-          const double m0 = fma(a[2][3], u0, fma(a[2][2], q0, fma(a[2][1], y0, a[2][0] * I0))) + p0;
-          const double m1 = fma(a[2][3], u1, fma(a[2][2], q1, fma(a[2][1], y1, a[2][0] * I1))) + p1;
-          const double l0 = fma(a[1][3], u0, fma(a[1][2], q0, fma(a[1][1], y0, a[1][0] * I0))) + m0;
-          const double l1 = fma(a[1][3], u1, fma(a[1][2], q1, fma(a[1][1], y1, a[1][0] * I1))) + m1;
+          const double m0 = fma(a[2][3], u0, fma(a[2][2], q0, fma(a[2][1], y0, idt<WAVE>(a[2][0], r == c)))) + p0;
+          const double m1 = fma(a[2][3], u1, fma(a[2][2], q1, fma(a[2][1], y1, idt<WAVE>(a[2][0], r == c + 1)))) + p1;
+          const double l0 = fma(a[1][3], u0, fma(a[1][2], q0, fma(a[1][1], y0, idt<WAVE>(a[1][0], r == c)))) + m0;
+          const double l1 = fma(a[1][3], u1, fma(a[1][2], q1, fma(a[1][1], y1, idt<WAVE>(a[1][0], r == c + 1)))) + m1;
           dput(E, 0, off, m0, m1);
           car_set(cm, j, 0, m0);
           car_set(cm, j, 1, m1);
@@ -531,12 +541,12 @@ __device__ __forceinline__ void depilogue(int epi, const DArgs<TOut>& E, const A
           const double q0 = car_get(cy2, j, 0), q1 = car_get(cy2, j, 1);
           const double u0 = car_get(cy3, j, 0), u1 = car_get(cy3, j, 1);
           const double d0 = car_get(cm, j, 0), d1 = car_get(cm, j, 1);
-          const double c0 = fma(a[0][3], u0, fma(a[0][2], q0, fma(a[0][1], y0, a[0][0] * I0))) + p0;
-          const double c1 = fma(a[0][3], u1, fma(a[0][2], q1, fma(a[0][1], y1, a[0][0] * I1))) + p1;
-          const double n0 = fma(z[11], c0, fma(z[10], d0, fma(z[9], u0, fma(z[8], q0, fma(z[7], y0, z[6] * I0)))));
-          const double n1 = fma(z[11], c1, fma(z[10], d1, fma(z[9], u1, fma(z[8], q1, fma(z[7], y1, z[6] * I1)))));
-          car_set(ck, j, 0, fma(z[5], c0, fma(z[4], d0, fma(z[3], u0, fma(z[2], q0, fma(z[1], y0, z[0] * I0))))));
-          car_set(ck, j, 1, fma(z[5], c1, fma(z[4], d1, fma(z[3], u1, fma(z[2], q1, fma(z[1], y1, z[0] * I1))))));
+          const double c0 = fma(a[0][3], u0, fma(a[0][2], q0, fma(a[0][1], y0, idt<WAVE>(a[0][0], r == c)))) + p0;
+          const double c1 = fma(a[0][3], u1, fma(a[0][2], q1, fma(a[0][1], y1, idt<WAVE>(a[0][0], r == c + 1)))) + p1;
+          const double n0 = fma(z[11], c0, fma(z[10], d0, fma(z[9], u0, fma(z[8], q0, fma(z[7], y0, idt<WAVE>(z[6], r == c))))));
+          const double n1 = fma(z[11], c1, fma(z[10], d1, fma(z[9], u1, fma(z[8], q1, fma(z[7], y1, idt<WAVE>(z[6], r == c + 1))))));
+          car_set(ck, j, 0, fma(z[5], c0, fma(z[4], d0, fma(z[3], u0, fma(z[2], q0, fma(z[1], y0, idt<WAVE>(z[0], r == c)))))));
+          car_set(ck, j, 1, fma(z[5], c1, fma(z[4], d1, fma(z[3], u1, fma(z[2], q1, fma(z[1], y1, idt<WAVE>(z[0], r == c + 1)))))));
           dput(E, 0, off, c0, c1);
           if (E.g) gstore<64>(E.g, E.n, r, c, c0, c1);
           dput(E, 1, off, n0, n1);
