@@ -40,7 +40,13 @@ cudaError_t launch_fused64(int dtype, bool wave, const void* a, void* c, void* s
 size_t schedule_ws_bytes();
 cudaError_t launch_schedule(const int32_t* K, const int32_t* S, const int32_t* status,
                             int64_t batch, int* bins, int32_t* order, cudaStream_t stream,
-                            int64_t* launches);
+                            int64_t* launches, bool prehist);
+bool schedule_sorted(int64_t batch);
+bool norm_select_fits(int n);
+cudaError_t launch_norm_select(int dtype, const void* a, const double* t, int64_t batch, int n,
+                               int family, int precision, int32_t* K, int32_t* S,
+                               int32_t* status, unsigned long long* normbits, int* bins,
+                               int64_t hist_count, cudaStream_t stream);
 size_t tiled_workspace_bytes(int64_t batch, int n, int eng);
 void set_engine(int e);
 void set_thread_engine(int e);
@@ -236,7 +242,7 @@ cudaStream_t side_stream() {
 // After K/S/status are on the device: run K1/K1c or the tiled chain.
 int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, void* s,
                 int64_t batch, int n, const int32_t* K, const int32_t* S, const int32_t* st,
-                const CommonWs& w, cudaStream_t stream, int eng) {
+                const CommonWs& w, cudaStream_t stream, int eng, bool prehist = false) {
   if (n == 0 || batch == 0) return CSM_SUCCESS;
   cudaError_t e;
   if (n <= fused_max()) {
@@ -257,7 +263,7 @@ int run_compute(int dtype, bool wave, const void* a, const double* t, void* c, v
           if (*p) cudaEventDestroy(*p);
       }
     } guard{{&ev_sel, &ev_done}};
-    e = csm::launch_schedule(K, S, st, bf, w.bins, w.order, stream, &g_launches);
+    e = csm::launch_schedule(K, S, st, bf, w.bins, w.order, stream, &g_launches, prehist);
     if (e != cudaSuccess) return cuda_fail(e, "schedule kernels");
     csm::prof_begin(stream);
     // (the schedule's histogram scratch is free again: its first word is the work counter)
@@ -303,6 +309,16 @@ bool self_select_enabled() {
   return on;
 }
 
+// CSM_K0_FUSED=0 keeps the separate norm1 / select / histogram launches for
+// n <= 128 too (A/B measurements and the cross-check test).
+bool k0_fused_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CSM_K0_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int pipeline(int dtype, int precision, bool wave, const void* a, const double* t, void* c,
              void* s, int64_t batch, int n, int32_t* k, int32_t* sx, int32_t* status, void* ws,
              size_t ws_bytes, void* stream_v) {
@@ -328,6 +344,24 @@ int pipeline(int dtype, int precision, bool wave, const void* a, const double* t
     ++g_launches;
     csm::prof_end(stream, 1);
     return CSM_SUCCESS;
+  }
+  if (csm::norm_select_fits(n) && k0_fused_enabled()) {
+    // n <= 128: norm, finiteness, (k, s) and the schedule's cost histogram in one launch
+    int64_t hist_n = 0;
+    if (n <= fused_max()) {
+      const int64_t bf = n > 64 ? batch - side_count(batch) : batch;
+      if (csm::schedule_sorted(bf)) hist_n = bf;
+    }
+    if (hist_n) {
+      e = cudaMemsetAsync(w.bins, 0, csm::schedule_ws_bytes(), stream);
+      if (e != cudaSuccess) return cuda_fail(e, "memset");
+    }
+    e = csm::launch_norm_select(dtype, a, t, batch, n, wave ? 1 : 0, precision, k, sx, status,
+                                w.normbits, hist_n ? w.bins : nullptr, hist_n, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "norm/select kernel");
+    ++g_launches;
+    return run_compute(dtype, wave, a, t, c, s, batch, n, k, sx, status, w, stream, eng,
+                       hist_n > 0);
   }
   e = cudaMemsetAsync(w.normbits, 0, static_cast<size_t>(batch) * 8, stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, static_cast<size_t>(batch) * 4, stream);

@@ -241,13 +241,180 @@ __global__ void iota_kernel(int32_t* __restrict__ order, int64_t batch) {
 // needed -- the latency-bound single-matrix path of configs[0].
 constexpr int64_t kUnsortedMax = 32;
 
+// True when launch_schedule sorts a batch of this size (else order = identity).
+bool schedule_sorted(int64_t batch) { return batch > kUnsortedMax; }
+
+// Scan + scatter in one block for batches a single block walks in a few
+// microseconds: the scanned bins stay in shared memory.
+constexpr int64_t kOneBlockScatterMax = 65536;
+
+__global__ void __launch_bounds__(1024)
+cost_scan_scatter_kernel(const int32_t* __restrict__ K, const int32_t* __restrict__ S,
+                         const int32_t* __restrict__ status, int64_t batch,
+                         const int* __restrict__ bins, int32_t* __restrict__ order) {
+  __shared__ int part[1024];
+  __shared__ int sb[kCostBins];
+  const int t = threadIdx.x;  // 1024 threads, 2 bins each
+  const int a0 = bins[2 * t], a1 = bins[2 * t + 1];
+  part[t] = a0 + a1;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const int v = t >= off ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  const int excl = part[t] - (a0 + a1);
+  sb[2 * t] = excl;
+  sb[2 * t + 1] = excl + a0;
+  __syncthreads();
+#pragma unroll 4
+  for (int64_t b = t; b < batch; b += 1024) {
+    int cost = status[b] == 0 ? K[b] + 2 * S[b] : 0;
+    cost = cost < kCostBins - 1 ? cost : kCostBins - 1;
+    const int pos = atomicAdd(sb + (kCostBins - 1 - cost), 1);
+    order[pos] = static_cast<int32_t>(b);
+  }
+}
+
+// K0 fused for n <= 128: one warp per matrix.  Each lane owns VEC adjacent
+// columns of every 32 VEC-column pass and accumulates them sequentially in
+// row order in the input's dtype -- the same sums, in the same order, as
+// norm1_kernel (matcore.py:100-104) -- with whole rows read as one
+// coalesced vector load per lane.  The column maximum is a warp shuffle
+// (bit patterns of non-negative doubles order like the values, as the
+// atomicMax of norm1_kernel does), lane 0 selects (k, s) like select_kernel
+// and, when bins is given, counts the matrix's cost for the schedule: no
+// memsets of normbits / status, no atomics on them, one launch instead of
+// four stream operations.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256)
+norm_select_kernel(const T* __restrict__ A, const double* __restrict__ t, int64_t batch, int n,
+                   int family, int precision, int32_t* __restrict__ K, int32_t* __restrict__ S,
+                   int32_t* __restrict__ status, unsigned long long* __restrict__ normbits,
+                   int* __restrict__ bins, int64_t hist_count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= batch) return;  // warp-uniform
+  const T* base = A + b * n * n;
+  unsigned long long mx = 0ull;
+  bool fin = true;
+  for (int j0 = 0; j0 < n; j0 += 32 * VEC) {
+    const int col = j0 + lane * VEC;
+    if (col < n) {  // n % VEC == 0: the lane's VEC columns are all inside
+      const T* p = base + col;
+      T acc[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[v] = T(0);
+#pragma unroll 8
+      for (int i = 0; i < n; ++i) {
+        T x[VEC];
+        if constexpr (VEC == 1) {
+          x[0] = __ldg(p + static_cast<int64_t>(i) * n);
+        } else if constexpr (sizeof(T) == 8) {
+          const double2 v2 = __ldg(reinterpret_cast<const double2*>(p + static_cast<int64_t>(i) * n));
+          x[0] = v2.x; x[1] = v2.y;
+        } else {
+          const float4 v4 = __ldg(reinterpret_cast<const float4*>(p + static_cast<int64_t>(i) * n));
+          x[0] = v4.x; x[1] = v4.y; x[2] = v4.z; x[3] = v4.w;
+        }
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          fin &= (x[v] - x[v] == T(0));
+          acc[v] = acc[v] + fabs(x[v]);  // sequential in row order: no reassociation
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const unsigned long long bits = static_cast<unsigned long long>(
+            __double_as_longlong(static_cast<double>(acc[v])));
+        mx = bits > mx ? bits : mx;
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(0xffffffffu, mx, off);
+    mx = o > mx ? o : mx;
+  }
+  fin = __all_sync(0xffffffffu, fin);
+  if (lane != 0) return;
+  normbits[b] = mx;
+  double norm = __longlong_as_double(static_cast<long long>(mx));
+  int st = fin ? kOk : kNonfiniteInput;
+  int k = 0, s = 0;
+  if (st == kOk) {
+    if (family == 1) {
+      const double tb = t[b];
+      norm = (tb * tb) * norm;  // driver.py:136, float(t)*float(t)*norm1(a)
+    }
+    st = select_one(norm, dTables.theta[family][precision], dTables.kk[family][precision],
+                    dTables.nent[family], dTables.log2fix, &k, &s);
+  }
+  K[b] = k;
+  S[b] = s;
+  status[b] = st;
+  if (bins && b < hist_count) {
+    int cost = st == 0 ? k + 2 * s : 0;
+    cost = cost < kCostBins - 1 ? cost : kCostBins - 1;
+    atomicAdd(bins + (kCostBins - 1 - cost), 1);  // bin 0 = most expensive
+  }
+}
+
+constexpr int kNormSelectMaxN = 128;
+bool norm_select_fits(int n) { return n > 0 && n <= kNormSelectMaxN; }
+
+// bins (zeroed by the caller) may be null: no cost histogram then.
+cudaError_t launch_norm_select(int dtype, const void* a, const double* t, int64_t batch, int n,
+                               int family, int precision, int32_t* K, int32_t* S,
+                               int32_t* status, unsigned long long* normbits, int* bins,
+                               int64_t hist_count, cudaStream_t stream) {
+  if (batch == 0) return cudaSuccess;
+  const unsigned blocks = blocks_for(batch, 8);  // 8 warps = 8 matrices per block
+  const bool al16 = (reinterpret_cast<uintptr_t>(a) & 15) == 0;
+  if (dtype == 0) {
+    const double* A = static_cast<const double*>(a);
+    if (al16 && n % 2 == 0)
+      norm_select_kernel<double, 2><<<blocks, 256, 0, stream>>>(
+          A, t, batch, n, family, precision, K, S, status, normbits, bins, hist_count);
+    else
+      norm_select_kernel<double, 1><<<blocks, 256, 0, stream>>>(
+          A, t, batch, n, family, precision, K, S, status, normbits, bins, hist_count);
+  } else {
+    const float* A = static_cast<const float*>(a);
+    if (al16 && n % 4 == 0)
+      norm_select_kernel<float, 4><<<blocks, 256, 0, stream>>>(
+          A, t, batch, n, family, precision, K, S, status, normbits, bins, hist_count);
+    else
+      norm_select_kernel<float, 1><<<blocks, 256, 0, stream>>>(
+          A, t, batch, n, family, precision, K, S, status, normbits, bins, hist_count);
+  }
+  return cudaGetLastError();
+}
+
+// prehist: the bins already hold the cost histogram of [0, batch)
+// (norm_select_kernel counted it), so the memset and the histogram launch
+// are skipped, and a batch one block can walk is scanned and scattered in
+// one launch.
 cudaError_t launch_schedule(const int32_t* K, const int32_t* S, const int32_t* status,
                             int64_t batch, int* bins, int32_t* order, cudaStream_t stream,
-                            int64_t* launches) {
+                            int64_t* launches, bool prehist) {
   if (batch == 0) return cudaSuccess;
   if (batch <= kUnsortedMax) {
     iota_kernel<<<1, 32, 0, stream>>>(order, batch);
     *launches += 1;
+    return cudaGetLastError();
+  }
+  if (prehist) {
+    if (batch <= kOneBlockScatterMax) {
+      cost_scan_scatter_kernel<<<1, 1024, 0, stream>>>(K, S, status, batch, bins, order);
+      *launches += 1;
+    } else {
+      cost_scan_kernel<<<1, 1024, 0, stream>>>(bins);
+      cost_scatter_kernel<<<blocks_for(batch, 256), 256, 0, stream>>>(K, S, status, batch, bins,
+                                                                      order);
+      *launches += 2;
+    }
     return cudaGetLastError();
   }
   cudaError_t e = cudaMemsetAsync(bins, 0, schedule_ws_bytes(), stream);
