@@ -439,7 +439,8 @@ constexpr int OZ_PEPI = 8;  // epilogue warps: two per TMEM lane quarter, 128 co
 constexpr int OZ_PTHREADS = 32 * (2 + OZ_PEPI);
 template <int NST>
 __global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la, const OzArgs oz,
-                                                            const OzConst C, int pair_tiles) {
+                                                            const OzConst C, int pair_tiles,
+                                                            int gx) {
   extern __shared__ __align__(128) int8_t osm[];
   __shared__ __align__(8) uint64_t bar_free[NST];
   __shared__ __align__(8) uint64_t bar_full[NST];
@@ -478,12 +479,21 @@ __global__ void __launch_bounds__(OZ_PTHREADS, 1) oz_gemm_p(const LaunchArgs la,
   const int nk = NP / OZ_KS;
   const size_t kb32 = NP / 32;
   const size_t lplane = static_cast<size_t>(M) * NP, rplane = static_cast<size_t>(NP) * NP;
-  // pair tile T -> x fastest, then y pair, then item x modulus
+  // pair tile T -> x fastest inside a group of gx column tiles, then y pair,
+  // then the next column group, then item x modulus.  The co-resident
+  // clusters then share gx right-operand panels (gx x 256 x NP bytes: 16 MiB
+  // at NP = 8192, gx = 8) that stay in L2 while the y pairs stream past,
+  // instead of cycling through the whole 64 MiB residue plane per y pair.
+  // gx = nx is the plain row-major walk.
   auto decode = [&](int T, int& x, int& y, int& z) {
-    x = T % nx;
-    const int r = T / nx;
-    y = 2 * (r % nyp) + static_cast<int>(rank);
-    z = r / nyp;
+    const int per_z = nx * nyp;
+    z = T / per_z;
+    const int t = T - z * per_z;
+    const int band = gx * nyp;
+    const int g = t / band, r = t - g * band;
+    const int yy = r / gx;
+    x = g * gx + (r - yy * gx);
+    y = 2 * yy + static_cast<int>(rank);
   };
   constexpr int BH = OZ_B_ST / 2;
   if (warp == 0) {

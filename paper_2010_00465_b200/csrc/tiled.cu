@@ -1442,6 +1442,21 @@ static int oz_resident_clusters() {
   return active;
 }
 
+// Column tiles per raster group of the persistent int8 GEMM (oz_gemm_p's
+// decode): 8 from NP = 8192 up (nx >= 32), where the 74 co-resident cluster
+// pairs then cover about 9 x 8 tiles -- 18 MiB of left and 16 MiB of right
+// panels live instead of the whole 64 MiB right plane -- else the whole row.
+// Measured on cfg5 (profiles/r2/s12/): GEMM 160.9 ms (row walk), 164.7 (16),
+// 154.4 (8), 167.2 (4) per step.  CSM_OZ_GX overrides it (a divisor of nx).
+static int oz_group_x(int nx) {
+  static const int env = [] {
+    const char* e = std::getenv("CSM_OZ_GX");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env > 0 && env <= nx && nx % env == 0) return env;
+  return (nx >= 32 && nx % 8 == 0) ? 8 : nx;
+}
+
 // One tiled launch (all items of plan A) through the Ozaki engine, in
 // chunks of at most cap items: maxima, residues, nm int8 GEMMs, CRT +
 // epilogue, then the accuracy guard (oz_guard) and the DMMA rerun of the
@@ -1501,7 +1516,8 @@ static cudaError_t run_oz_launch(const tk::LaunchArgs& A, const tk::OzArgs& scra
       cfg.gridDim = dim3(2 * clusters);
       cfg.blockDim = dim3(tk::OZ_PTHREADS);
       cfg.dynamicSmemBytes = tk::OZ_SMEM;
-      e = cudaLaunchKernelEx(&cfg, tk::oz_gemm_p<tk::OZ_NSTAGE>, A, O, C, pair_tiles);
+      e = cudaLaunchKernelEx(&cfg, tk::oz_gemm_p<tk::OZ_NSTAGE>, A, O, C, pair_tiles,
+                             oz_group_x(NP / tk::OZ_TN));
     } else {
       e = small ? cudaLaunchKernelEx(&cfg, tk::oz_gemm<tk::OZ_NSTAGE_SMALL>, A, O, C)
                 : cudaLaunchKernelEx(&cfg, tk::oz_gemm<tk::OZ_NSTAGE>, A, O, C);
