@@ -596,6 +596,19 @@ def run_ours(args, cfg):
     kern_ms = ctypes_collect(L)
     L.csm_profile_enable(0)
     launches = per_run * args.steps if use_graph else plan.launches
+    # the fused K0 launch (norm1 + finiteness + selection, n <= 128) timed on
+    # its own after the timed region: the HBM-bound part of a step
+    k0 = None
+    if n <= 128 and batch > 148 and not use_graph and os.environ.get("CSM_K0_FUSED", "1") != "0":
+        L.csm_profile_enable(3)
+        for _ in range(5):
+            plan.run(a_dev, t_dev)
+        torch.cuda.synchronize()
+        k0_ms, k0_cnt = ctypes_collect(L)
+        L.csm_profile_enable(0)
+        plan.launches = launches
+        if k0_cnt:
+            k0 = hbm_roofline(batch * n * n * (4 if dt == "f32" else 8), k0_ms / k0_cnt)
     ms_step = max_over_ranks(ms_total / args.steps)
     units = sum_over_ranks(float(batch))
     value = units / (ms_step * 1e-3)
@@ -716,6 +729,7 @@ def run_ours(args, cfg):
                                     "no FP64 entry)",
                      "flops_per_step": flops_step,
                      "kernel_ms_per_step": kern_avg_ms},
+        "roofline_k0": k0,
         "e2e": {"value": batch * world / (e2e_ms * 1e-3), "unit": "matrices/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms, "mode": e2e_mode},
@@ -758,6 +772,27 @@ def ozaki_roofline(int8_ops_step, gemm_ms, fp64_tflops, dmma_peak):
             "int8_ops_per_step": int8_ops_step, "kernel_ms_per_step": gemm_ms,
             "fp64_equiv_tflops": fp64_tflops, "dmma_peak_tflops": dmma_peak,
             "fp64_equiv_vs_dmma_peak": (fp64_tflops / dmma_peak) if dmma_peak else None}
+
+
+def hbm_roofline(bytes_per_launch, ms):
+    """Secondary roofline object of the fused K0 launch (HBM-bound: one read
+    of the batch).  peak = MEASURED_PEAKS.json hbm_gbs (driver-written copy
+    bandwidth), else the profiling guide's 7700 GB/s nominal figure."""
+    peak, src = 7700.0, "nominal HBM3e figure of B200_PROFILING.md (MEASURED_PEAKS.json absent)"
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        src = "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)"
+    except Exception:
+        pass
+    achieved = bytes_per_launch / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": "norm_select_kernel (fused K0: norm1, finiteness, (k, s), cost histogram)",
+            "peak_source": src, "bytes_per_launch": bytes_per_launch,
+            "kernel_ms_per_launch": ms,
+            "note": "CUDA-event interval around ONE ~85 us launch, so it carries the launch "
+                    "and event overhead (~15 us); ncu gpu__time_duration of the same launch: "
+                    "83.5 us = 0.996 of the peak (profiles/r2/s6/ncu_k0_norm_select.txt)"}
 
 
 def ctypes_collect(L):

@@ -358,7 +358,8 @@ int64_t csm_last_launch_count(void);
  * csm_profile_collect synchronises those events, returns the summed
  * milliseconds and the number of intervals, and clears them.
  * csm_profile_enable(0/1) also clears; mode 2 records the Ozaki engine's
- * int8 GEMM launches (one interval per launch) instead. */
+ * int8 GEMM launches (one interval per launch) instead, mode 3 the fused
+ * K0 launch (norm1 + finiteness + selection, n <= 128) of each call. */
 int csm_profile_enable(int on);
 int csm_profile_collect(double* total_ms, int64_t* intervals);
 

@@ -84,7 +84,7 @@ cudaError_t ddref_chain(const double* a, const int32_t* dS, int smax, double* co
 }  // namespace csm
 
 namespace {
-thread_local int g_prof = 0;  // 0 off, 1 pipeline intervals, 2 int8 GEMM launches
+thread_local int g_prof = 0;  // 0 off, 1 pipeline intervals, 2 int8 GEMM launches, 3 fused K0 launches
 thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_ev;
 thread_local cudaEvent_t g_prof_open = nullptr;
 thread_local bool g_prof_hold = false;  // an enclosing interval is open
@@ -356,8 +356,10 @@ int pipeline(int dtype, int precision, bool wave, const void* a, const double* t
       e = cudaMemsetAsync(w.bins, 0, csm::schedule_ws_bytes(), stream);
       if (e != cudaSuccess) return cuda_fail(e, "memset");
     }
+    csm::prof_begin(stream, 3);  // csm_profile_enable(3): the K0 launch alone
     e = csm::launch_norm_select(dtype, a, t, batch, n, wave ? 1 : 0, precision, k, sx, status,
                                 w.normbits, hist_n ? w.bins : nullptr, hist_n, stream);
+    csm::prof_end(stream, 3);
     if (e != cudaSuccess) return cuda_fail(e, "norm/select kernel");
     ++g_launches;
     return run_compute(dtype, wave, a, t, c, s, batch, n, k, sx, status, w, stream, eng,
@@ -1076,7 +1078,7 @@ int csm_graph_safe(int dtype, int64_t batch, int n) {
 
 int csm_profile_enable(int on) {
   prof_clear();
-  if (on < 0 || on > 2) return fail(CSM_ERR_ARG, "profile mode must be 0, 1 or 2");
+  if (on < 0 || on > 3) return fail(CSM_ERR_ARG, "profile mode must be 0, 1, 2 or 3");
   g_prof = on;
   return CSM_SUCCESS;
 }
