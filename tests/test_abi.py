@@ -193,3 +193,18 @@ def test_dist_workspace_sizes_and_argument_errors():
         assert rc == _lib.ERR_ARG
     g, p = ctypes.c_int32(), ctypes.c_int32()
     assert L.csm_dist_last_stats(ctypes.byref(g), ctypes.byref(p)) == 0
+
+
+def test_profile_modes_without_device():
+    """csm_profile_enable: 0 off, 1 pipeline intervals, 2 int8 GEMM launches,
+    3 the fused K0 launch; anything else is an argument error.  No events
+    exist without a launch, so collect returns zero intervals."""
+    import ctypes
+    lib = _lib.lib()
+    for mode in (1, 2, 3, 0):
+        assert lib.csm_profile_enable(mode) == 0
+    assert lib.csm_profile_enable(4) == _lib.ERR_ARG
+    assert lib.csm_profile_enable(-1) == _lib.ERR_ARG
+    tot, cnt = ctypes.c_double(-1.0), ctypes.c_int64(-1)
+    assert lib.csm_profile_collect(ctypes.byref(tot), ctypes.byref(cnt)) == 0
+    assert tot.value == 0.0 and cnt.value == 0
